@@ -1,0 +1,138 @@
+/*
+ * lvx_b200.h — C ABI of the B200-native LV-XAttn hot path.
+ *
+ * One shared library (paper_2502_02406_b200/liblvx_b200.so) exports the
+ * kernels that replace the numpy kernels of the reference package
+ * `lvxattn` (reference: /root/reference/pkg/src/lvxattn/kernels.py).  The
+ * ring-exchange scheduler that calls them (lvx_forward / lvx_backward /
+ * ring_forward / ring_backward / run_distributed) lives in the Python host
+ * layer `paper_2502_02406_b200.strategies`, one process per GPU over NCCL.
+ *
+ * Conventions:
+ *   - Tensors are strided [heads, rows, d] views with the last dim
+ *     contiguous; strides are in ELEMENTS.  Rank shards are views
+ *     (Q[:, qa:qb]) so a view never needs a copy.
+ *   - L is the natural-log log-sum-exp of the *scaled* scores; an empty row
+ *     is (O = 0, L = -inf), the identity of lvx_merge_states.
+ *   - GQA: q head a reads k/v head a / (q->heads / k->heads).  MHA (the
+ *     reference's only layout) is heads equal.
+ *   - Input dtypes: F32, F64 (exact-parity SIMT kernels) and BF16
+ *     (tcgen05/TMEM tensor-core kernels for d in {64,128}; SIMT otherwise).
+ *     Softmax state (O partial, L, D) and gradient accumulators are F32 for
+ *     F32/BF16 inputs and F64 for F64 inputs.
+ *   - Every call is asynchronous on the caller's cudaStream_t, never
+ *     synchronises the host, allocates nothing (scratch comes from the
+ *     caller's workspace) and keeps no global mutable state.
+ *   - Return value: LVX_OK (0) or a negative lvx_status.  The Python shim
+ *     maps LVX_EINVAL/LVX_EDTYPE to ValueError with the reference messages
+ *     (kernels.py:62-73) and LVX_ECUDA to RuntimeError.
+ */
+#ifndef LVX_B200_H
+#define LVX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LVX_ABI_VERSION 1
+
+typedef enum lvx_status {
+  LVX_OK = 0,
+  LVX_EINVAL = -1,      /* shape / stride / argument error            */
+  LVX_EDTYPE = -2,      /* unsupported or mismatched dtype             */
+  LVX_ECUDA = -3,       /* CUDA launch / runtime error                 */
+  LVX_EUNSUPPORTED = -4,/* valid request, no kernel for it (e.g. d>256) */
+  LVX_EWORKSPACE = -5   /* caller workspace smaller than required      */
+} lvx_status;
+
+typedef enum lvx_dtype {
+  LVX_F32 = 0,
+  LVX_F64 = 1,
+  LVX_BF16 = 2
+} lvx_dtype;
+
+/* A strided [heads, rows, d] view.  For row statistics (L, D) d == 1 and
+ * row_stride == 1.  Strides in elements. */
+typedef struct lvx_view {
+  void* data;
+  int64_t heads;
+  int64_t rows;
+  int64_t d;
+  int64_t head_stride;
+  int64_t row_stride;
+  int32_t dtype; /* lvx_dtype */
+  int32_t _pad;
+} lvx_view;
+
+/* ---- introspection ---------------------------------------------------- */
+int lvx_abi_version(void);
+const char* lvx_strerror(int status);
+/* 1 when the tcgen05 path would serve (q, k) on the current device. */
+int lvx_tc_eligible(const lvx_view* q, const lvx_view* k);
+
+/* ---- K1: blockwise forward -------------------------------------------
+ * Replaces kernels.py:105 blockwise_attention(Q, K, V, scale, tile_rows).
+ * (o_out, l_out) <- partial state of q against this KV block; if `prior_o`
+ * and `prior_l` are non-NULL the result is merged with that state
+ * (fused kernels.py:144 merge_states(prior, delta), as lvx_forward does at
+ * strategies.py:213).  prior may alias out.  `workspace` must hold
+ * lvx_blockwise_fwd_workspace(q, k) bytes.  k->rows == 0 yields the
+ * empty state (kernels.py:119-120) merged with prior.
+ * tile_rows is semantically a no-op (tests/test_kernels.py:99-103) and is
+ * not part of the ABI. */
+size_t lvx_blockwise_fwd_workspace(const lvx_view* q, const lvx_view* k);
+int lvx_blockwise_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                      double scale,
+                      const lvx_view* prior_o, const lvx_view* prior_l,
+                      const lvx_view* o_out, const lvx_view* l_out,
+                      void* workspace, size_t workspace_bytes, void* stream);
+/* The same operation in two launches so a ring scheduler can start the
+ * attention before the prior state has arrived over NVLink: _partial runs
+ * the tensor-core main loop into `workspace` (per-split partial states),
+ * _finish combines the splits and merges the prior (strategies.py:207-213
+ * blockwise_attention + merge_states).  Same (q, k) shapes and workspace in
+ * both calls. */
+int lvx_fwd_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v, double scale,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int lvx_fwd_finish(const lvx_view* q, const lvx_view* k,
+                   const lvx_view* prior_o, const lvx_view* prior_l,
+                   const lvx_view* o_out, const lvx_view* l_out,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K2: LSE merge ------------------------------------------------------
+ * Replaces kernels.py:144 merge_states(a, b).  out may alias a or b. */
+int lvx_merge_states(const lvx_view* oa, const lvx_view* la,
+                     const lvx_view* ob, const lvx_view* lb,
+                     const lvx_view* o_out, const lvx_view* l_out, void* stream);
+
+/* ---- K3: backward row statistic ----------------------------------------
+ * Replaces kernels.py:164 attention_row_stats(state, dO): D = rowsum(dO*O). */
+int lvx_row_stats(const lvx_view* o, const lvx_view* d_o, const lvx_view* d_out,
+                  void* stream);
+
+/* ---- K4: blockwise backward ---------------------------------------------
+ * Replaces kernels.py:192 blockwise_attention_backward(Q, K, V, L, D, dO).
+ * Adds (accumulate=1) or writes (accumulate=0) the contributions into the
+ * F32/F64 accumulators dq_acc [hq, rows_q, d], dk_acc / dv_acc
+ * [hkv, rows_kv, d] (GQA: dK/dV summed over the query-head group). */
+size_t lvx_blockwise_bwd_workspace(const lvx_view* q, const lvx_view* k);
+int lvx_blockwise_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                      const lvx_view* l, const lvx_view* dd, const lvx_view* d_o,
+                      double scale,
+                      const lvx_view* dq_acc, const lvx_view* dk_acc,
+                      const lvx_view* dv_acc, int accumulate,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- utilities ---------------------------------------------------------
+ * empty_state (kernels.py:48-53): O = 0, L = -inf. */
+int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream);
+/* dst = src converted (F32/F64/BF16 <-> F32/F64/BF16), strided views. */
+int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LVX_B200_H */

@@ -1,0 +1,30 @@
+"""B200-native LV-XAttn: distributed cross-attention for very long visual
+contexts (arXiv 2502.02406), drop-in for the reference package ``lvxattn``'s
+hot path (kernels + query/KV-rotation strategies).
+
+Kernels: hand-written sm_100a CUDA (tcgen05/TMEM/TMA) in ``liblvx_b200.so``
+behind the C ABI of ``include/lvx_b200.h``.  Schedulers: one process per GPU
+over NCCL (``strategies``).  There is no CPU fallback.
+"""
+from .comm import (ClusterError, ClusterSpec, CollectiveTimeout, DeviceContext, Instant,
+                   TransportStats, WorkerFailed)
+from .kernels import (AttentionState, GradientBundle, attention_row_stats, blockwise_attention,
+                      blockwise_attention_backward, default_scale, dense_attention,
+                      dense_attention_backward, empty_state, merge_states, project,
+                      project_backward, validate_qkv)
+from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, StrategyKind,
+                         lvx_backward, lvx_forward, partition_rows, ring_backward, ring_forward,
+                         run_distributed, run_rank)
+from . import volumes
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AttentionState", "ClusterError", "ClusterSpec", "CollectiveTimeout", "DeviceContext",
+    "GradientBundle", "Instant", "RoundRecord", "RoundTrace", "RunResult", "ShardSpec",
+    "StrategyKind", "TransportStats", "WorkerFailed", "attention_row_stats",
+    "blockwise_attention", "blockwise_attention_backward", "default_scale", "dense_attention",
+    "dense_attention_backward", "empty_state", "lvx_backward", "lvx_forward", "merge_states",
+    "partition_rows", "project", "project_backward", "ring_backward", "ring_forward",
+    "run_distributed", "run_rank", "validate_qkv", "volumes",
+]

@@ -1,0 +1,57 @@
+"""The kernel set the ring schedulers call: the CUDA library, nothing else.
+
+``CudaOps`` is the only implementation shipped with the product.  The
+schedulers in ``strategies.py`` take it from ``DeviceContext.ops`` so the
+protocol logic (rounds, block indices, buffers, byte counts) is written once;
+the CPU protocol tests substitute the oracle there (tests/ only).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import kernels as K
+
+
+class CudaOps:
+    """liblvx_b200.so kernels on the current CUDA stream."""
+
+    name = "cuda"
+
+    @staticmethod
+    def state_dtype(dt: torch.dtype) -> torch.dtype:
+        return K.state_dtype(dt)
+
+    def fwd_workspace(self, q: torch.Tensor, k: torch.Tensor) -> torch.Tensor:
+        return K.workspace(K.fwd_workspace_bytes(q, k), q.device, slot=0)
+
+    def fwd_partial(self, q, k, v, scale, ws) -> None:
+        if q.numel() and k.shape[1]:
+            K.fwd_partial(q, k, v, scale, ws)
+
+    def fwd_finish(self, q, k, ws, out_o, out_l, prior_o=None, prior_l=None) -> None:
+        if q.numel():
+            K.fwd_finish(q, k, ws, out_o, out_l, prior_o, prior_l)
+
+    def fill_empty(self, o, l) -> None:
+        if o.numel():
+            K._lib.check("lvx_fill_empty_state", K._lib.load().lvx_fill_empty_state(
+                K._lib.view(o), K._lib.view(l), K._lib.stream_ptr(o.device)))
+
+    def row_stats(self, o, d_o, out) -> None:
+        if out.numel():
+            K.row_stats_into(o, d_o, out)
+
+    def bwd_accumulate(self, q, k, v, L, D, d_o, scale, dq, dk, dv) -> None:
+        if q.numel() and k.shape[1]:
+            K.bwd_accumulate(q, k, v, L, D, d_o, scale, dq, dk, dv, accumulate=True)
+
+    # -- device timing (CUDA events on the compute stream) -----------------
+    @staticmethod
+    def event():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    @staticmethod
+    def elapsed(a, b) -> float:
+        return a.elapsed_time(b) / 1e3

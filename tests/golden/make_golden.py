@@ -1,0 +1,115 @@
+"""Generate golden vectors by running the UNMODIFIED reference package.
+
+Run in the build container (the only place ``/root/reference`` exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes ``tests/golden/golden_kernels.npz``, ``golden_strategies.npz`` and
+``golden_c1.npz``.  The GPU box never reads ``/root/reference``; it only
+reads these committed fixtures.  Inputs come from the reference's own
+``seeded_random_tensor`` (Philox) and are stored alongside the outputs.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent
+
+
+def main() -> None:
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    from lvxattn import kernels as K
+    from lvxattn.cluster import ClusterSpec
+    from lvxattn.strategies import run_distributed
+    from lvxattn.tensorio import seeded_random_tensor as srt
+
+    def qkv(h, sq, skv, d, seed):
+        return (srt(seed, (h, sq, d)), srt(seed, (h, skv, d), stream=1),
+                srt(seed, (h, skv, d), stream=2), srt(seed, (h, sq, d), stream=3))
+
+    # ---------------- per-kernel vectors --------------------------------
+    kern = {}
+    cases = [(2, 5, 9, 4, 3, 11), (1, 4, 6, 3, 64, 12), (3, 7, 33, 5, 8, 13),
+             (2, 16, 70, 8, 16, 14), (1, 3, 1, 2, 64, 15)]
+    for ci, (h, sq, skv, d, tile, seed) in enumerate(cases):
+        Q, Kt, V, dO = qkv(h, sq, skv, d, seed)
+        for dt in (np.float64, np.float32):
+            tag = f"c{ci}_{np.dtype(dt).name}"
+            q, k, v, g = (t.astype(dt) for t in (Q, Kt, V, dO))
+            st = K.blockwise_attention(q, k, v, tile_rows=tile)
+            dn = K.dense_attention(q, k, v)
+            D = K.attention_row_stats(dn, g).astype(dt)
+            dq, dk, dv = K.blockwise_attention_backward(q, k, v, dn.L, D, g)
+            kern.update({f"{tag}_Q": q, f"{tag}_K": k, f"{tag}_V": v, f"{tag}_dO": g,
+                         f"{tag}_blockO": st.O, f"{tag}_blockL": st.L,
+                         f"{tag}_denseO": dn.O, f"{tag}_denseL": dn.L, f"{tag}_D": D,
+                         f"{tag}_dQ": dq, f"{tag}_dK": dk, f"{tag}_dV": dv,
+                         f"{tag}_tile": np.array(tile)})
+            # split into two KV blocks and merge (merge_states vector)
+            cut = skv // 2
+            a = K.blockwise_attention(q, k[:, :cut], v[:, :cut])
+            b = K.blockwise_attention(q, k[:, cut:], v[:, cut:])
+            m = K.merge_states(a, b)
+            kern.update({f"{tag}_mAO": a.O, f"{tag}_mAL": a.L, f"{tag}_mBO": b.O,
+                         f"{tag}_mBL": b.L, f"{tag}_mO": m.O, f"{tag}_mL": m.L})
+    # projection
+    x = srt(26, (5, 6))
+    W = srt(27, (6, 8))
+    g = srt(28, (2, 5, 4))
+    kern["proj_x"], kern["proj_W"], kern["proj_g"] = x, W, g
+    kern["proj_out"] = K.project(x, W, 2)
+    kern["proj_dX"], kern["proj_dW"] = K.project_backward(x, W, g)
+    np.savez_compressed(OUT / "golden_kernels.npz", **kern)
+
+    # ---------------- distributed protocol vectors ----------------------
+    strat = {}
+    scases = [(1, 5, 7, 3, 1, 1), (2, 5, 7, 4, 3, 2), (2, 8, 8, 4, 4, 3),
+              (1, 2, 9, 3, 4, 4),     # empty Q shards
+              (1, 9, 2, 3, 4, 5),     # empty KV shards
+              (4, 16, 3, 5, 6, 6), (2, 7, 9, 4, 2, 7)]
+    for ci, (h, sq, skv, d, n, seed) in enumerate(scases):
+        Q, Kt, V, dO = qkv(h, sq, skv, d, seed)
+        for dt in (np.float64, np.float32):
+            q, k, v, g = (t.astype(dt) for t in (Q, Kt, V, dO))
+            for s in ("lvx", "ring"):
+                tag = f"s{ci}_{s}_{np.dtype(dt).name}"
+                res = run_distributed(s, q, k, v, dO=g, spec=ClusterSpec(n))
+                strat.update({
+                    f"{tag}_Q": q, f"{tag}_K": k, f"{tag}_V": v, f"{tag}_dO": g,
+                    f"{tag}_n": np.array(n), f"{tag}_O": res.O, f"{tag}_L": res.L,
+                    f"{tag}_dQ": res.grads.dQ, f"{tag}_dK": res.grads.dK,
+                    f"{tag}_dV": res.grads.dV,
+                    f"{tag}_fwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_forward]),
+                    f"{tag}_bwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_backward]),
+                    f"{tag}_fwd_rounds": np.array([t.num_rounds for t in res.traces_forward]),
+                })
+    np.savez_compressed(OUT / "golden_strategies.npz", **strat)
+
+    # ---------------- BASELINE configs[0] (C1) --------------------------
+    # Lq=128, Lkv=4096, 8 heads, d=64, fp32, world_size=2 ring.  Inputs are
+    # NOT stored (regenerated bit-exactly from the seed); O, L and dQ are
+    # stored whole, dK/dV on a row sample plus per-head sums.
+    h, sq, skv, d, n, seed = 8, 128, 4096, 64, 2, 2024
+    Q, Kt, V, dO = (t.astype(np.float32) for t in qkv(h, sq, skv, d, seed))
+    res = run_distributed("lvx", Q, Kt, V, dO=dO, spec=ClusterSpec(n))
+    rows = np.arange(0, skv, 61)
+    c1 = {"seed": np.array(seed), "shape": np.array([h, sq, skv, d, n]),
+          "Q_head": Q[:, :2].copy(), "O": res.O, "L": res.L, "dQ": res.grads.dQ,
+          "dK_rows": rows, "dK_sample": res.grads.dK[:, rows], "dV_sample": res.grads.dV[:, rows],
+          "dK_sum": res.grads.dK.astype(np.float64).sum(axis=(1, 2)),
+          "dV_sum": res.grads.dV.astype(np.float64).sum(axis=(1, 2)),
+          "fwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_forward]),
+          "bwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_backward])}
+    np.savez_compressed(OUT / "golden_c1.npz", **c1)
+    for f in ("golden_kernels.npz", "golden_strategies.npz", "golden_c1.npz"):
+        print(f, (OUT / f).stat().st_size, "bytes")
+
+
+if __name__ == "__main__":
+    main()
