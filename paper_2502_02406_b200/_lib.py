@@ -89,7 +89,7 @@ def view(t: torch.Tensor | None):
         hs, rs = t.stride()
         v = LvxView(t.data_ptr(), h, r, 1, hs, rs, lvx_dtype(t), 0)
     elif t.dim() == 3:
-        if t.shape[2] > 1 and t.stride(2) != 1:
+        if t.numel() and t.shape[2] > 1 and t.stride(2) != 1:
             raise ValueError("last dimension must be contiguous")
         h, r, d = t.shape
         v = LvxView(t.data_ptr(), h, r, d, t.stride(0), t.stride(1), lvx_dtype(t), 0)

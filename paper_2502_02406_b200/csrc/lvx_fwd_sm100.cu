@@ -1,0 +1,555 @@
+// tcgen05/TMEM/TMA blockwise attention forward for B200 (sm_100a).
+//
+// Replaces kernels.py:105-141 blockwise_attention for bf16 inputs with
+// d in {64, 128}; the split combine + prior merge kernel replaces the
+// merge_states call that follows it in lvx_forward (strategies.py:207-213)
+// and ring_forward (strategies.py:299-301).
+//
+// One CTA = one kv head g, two 128-row query tiles of that head's GQA group
+// (so each K/V tile fetched into shared memory feeds 256 query rows), and one
+// split of the resident KV block.  Warp roles (320 threads):
+//   warps 0-3  softmax for query tile 0 (TMEM lanes 0-127, one row per thread)
+//   warps 4-7  softmax for query tile 1
+//   warp  8    TMA producer: Q tiles once, then K_j / V_j into a 3-slot ring
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 columns): S_t = Q_t K_j^T at cols [128t, 128t+128), O_t at
+// [256 + t*D, 256 + (t+1)*D).  S_t is read by its softmax warps, which write
+// P_t = exp2(S_t*scale*log2e - m) in bf16 to shared memory (K-major, 128B
+// swizzle) for the PV MMA.  The MMA order QK(j) -> PV(j-1) lets softmax of
+// tile j overlap the PV of tile j-1.  The running max is updated lazily: O
+// in TMEM is rescaled only when the row max grows by more than 2^8, which is
+// exact (P, l and O always share one reference max).
+// Each split writes a normalised partial (O, L) in fp32 to the workspace;
+// fwd_combine_kernel merges the splits (and the prior ring state) in a fixed
+// order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "lvx_common.cuh"
+#include "lvx_sm100.cuh"
+
+namespace lvx {
+namespace {
+
+using namespace sm100;
+
+constexpr int kBM = 128;   // query rows per tile (TMEM lanes)
+constexpr int kBN = 128;   // kv rows per tile
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct FwdCfg {
+  static constexpr int PANELS = D / 64;      // 128-byte (64 x bf16) column panels
+  static constexpr int Q_BYTES = kBM * D * 2;
+  static constexpr int KV_BYTES = kBN * D * 2;
+  static constexpr int P_BYTES = kBM * kBN * 2;
+  static constexpr int STAGES = D == 128 ? 3 : 6;
+  static constexpr int NBAR = 1 + 2 * STAGES + 8;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * KV_BYTES + 2 * P_BYTES + NBAR * 8 + 16;
+  static constexpr int S_COL0 = 0;
+  static constexpr int O_COL0 = 256;
+};
+
+struct FwdParams {
+  int hq, hkv, G, rows_q, rows_kv;
+  int tpq;              // 128-row tiles per query head
+  int n_tiles;          // 128-row kv tiles in the block
+  int tiles_per_split;
+  int splits;
+  float scale_log2;     // scale * log2(e)
+  float* ws_o;          // [splits][hq][rows_q][D]
+  float* ws_l;          // [splits][hq][rows_q]
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
+  using C = FwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint8_t* sQ = sm;
+  uint8_t* sKV = sQ + 2 * C::Q_BYTES;
+  uint8_t* sP = sKV + C::STAGES * C::KV_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::STAGES;
+  uint64_t* s_full = kv_empty + C::STAGES;   // [2]
+  uint64_t* s_free = s_full + 2;             // [2]
+  uint64_t* p_full = s_free + 2;             // [2]
+  uint64_t* o_done = p_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
+  const int kv_t0 = split * p.tiles_per_split;
+  const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
+  bool active[2];
+  int qh[2], row0[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int tt = 2 * pair + t;
+    active[t] = tt < p.G * p.tpq;
+    qh[t] = g * p.G + tt / p.tpq;
+    row0[t] = (tt % p.tpq) * kBM;
+  }
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&s_free[t], 128);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      const uint32_t qbytes = (active[0] + active[1]) * C::Q_BYTES;
+      mbar_arrive_expect_tx(q_full, qbytes);
+      for (int t = 0; t < 2; ++t)
+        if (active[t])
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_3d(sQ + t * C::Q_BYTES + pn * kBM * 128, &tmQ, q_full, pn * 64, row0[t],
+                        qh[t]);
+      for (int L = 0; L < 2 * nt; ++L) {
+        const int s = L % C::STAGES, u = L / C::STAGES;
+        if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
+        const int j = L >> 1;
+        const CUtensorMap* m = (L & 1) ? &tmV : &tmK;
+        mbar_arrive_expect_tx(&kv_full[s], C::KV_BYTES);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_3d(sKV + s * C::KV_BYTES + pn * kBN * 128, m, &kv_full[s], pn * 64,
+                      (kv_t0 + j) * kBN, g);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idQK = idesc_bf16(kBM, kBN, false, false);
+      constexpr uint32_t idPV = idesc_bf16(kBM, D, false, true);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j <= nt; ++j) {
+        if (j < nt) {
+          const int L = 2 * j, s = L % C::STAGES, u = L / C::STAGES;
+          mbar_wait(&kv_full[s], u & 1);
+          tc_fence_after();
+          const uint32_t kb = smem_u32(sKV + s * C::KV_BYTES);
+          for (int t = 0; t < 2; ++t) {
+            if (!active[t]) continue;
+            if (j > 0) {
+              mbar_wait(&s_free[t], (j - 1) & 1);
+              tc_fence_after();
+            }
+            const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
+              mma_bf16_ss(tmem + C::S_COL0 + t * kBN, umma_desc_sw128(qb + off, 0, 1024),
+                          umma_desc_sw128(kb + (kk >> 2) * (kBN * 128) + (kk & 3) * 32, 0, 1024),
+                          idQK, kk > 0);
+            }
+            mma_commit(&s_full[t]);
+          }
+          mma_commit(&kv_empty[s]);
+        }
+        if (j > 0) {
+          const int jj = j - 1, L = 2 * jj + 1, s = L % C::STAGES, u = L / C::STAGES;
+          mbar_wait(&kv_full[s], u & 1);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sKV + s * C::KV_BYTES);
+          for (int t = 0; t < 2; ++t) {
+            if (!active[t]) continue;
+            mbar_wait(&p_full[t], jj & 1);
+            tc_fence_after();
+            const uint32_t pb = smem_u32(sP + t * C::P_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk) {
+              const uint32_t aoff = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
+              mma_bf16_ss(tmem + C::O_COL0 + t * D, umma_desc_sw128(pb + aoff, 0, 1024),
+                          umma_desc_sw128(vb + kk * 16 * 128, kBN * 128, 1024), idPV,
+                          (jj > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&o_done[t]);
+          }
+          mma_commit(&kv_empty[s]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int t = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    if (active[t]) {
+      const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+      const uint32_t pb = smem_u32(sP + t * C::P_BYTES) + r * 128;
+      const uint32_t sw = (uint32_t)(r & 7);
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
+        const uint32_t sa = tl + C::S_COL0 + t * kBN;
+        // pass 1 over TMEM: row max (log2 domain)
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t sv[32];
+          tmem_ld32(sa + c * 32, sv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
+        }
+        mx *= p.scale_log2;
+        const bool need = mx > m_used + kRescaleThreshold;
+        if (j > 0) {  // PV(j-1) done: P_t is free and O_t is stable
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+        }
+        const float alpha = need ? ex2(m_used - mx) : 1.f;
+        if (__any_sync(0xffffffffu, need && j > 0)) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            const uint32_t oa = tl + C::O_COL0 + t * D + c * 32;
+            tmem_ld32(oa, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st32(oa, ov);
+          }
+          tmem_wait_st();
+        }
+        if (need) {
+          l *= alpha;
+          m_used = mx;
+        }
+        // pass 2: P = exp2(S*c - m) -> bf16 -> swizzled shared memory
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t sv[32];
+          tmem_ld32(sa + c * 32, sv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            float e8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int col = c * 32 + c8 * 8 + q;
+              const float x = fmaf(__uint_as_float(sv[c8 * 8 + q]), p.scale_log2, -m_used);
+              e8[q] = col < nvalid ? ex2(x) : 0.f;
+              rs += e8[q];
+            }
+            const uint32_t chunk = (uint32_t)(c * 4 + c8);   // 16-byte chunk of the row
+            const uint32_t addr = pb + (chunk >> 3) * (kBM * 128) + (((chunk & 7u) ^ sw) << 4);
+            st_shared_v4(addr, pack_bf16(e8[0], e8[1]), pack_bf16(e8[2], e8[3]),
+                         pack_bf16(e8[4], e8[5]), pack_bf16(e8[6], e8[7]));
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&s_free[t]);   // S_t fully read: QK(j+1) may overwrite it
+        l += rs;
+        fence_proxy_async_smem();
+        mbar_arrive(&p_full[t]);
+      }
+      // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial
+      mbar_wait(&o_done[t], (nt - 1) & 1);
+      tc_fence_after();
+      const int row = row0[t] + r;
+      const bool valid = row < p.rows_q;
+      const float inv = 1.f / l;
+      const size_t slot = ((size_t)split * p.hq + qh[t]) * p.rows_q + row;
+      float* dst = p.ws_o + slot * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tl + C::O_COL0 + t * D + c * 32, ov);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            float4 v4 = make_float4(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv,
+                                    __uint_as_float(ov[e + 2]) * inv,
+                                    __uint_as_float(ov[e + 3]) * inv);
+            *reinterpret_cast<float4*>(dst + c * 32 + e) = v4;
+          }
+        }
+      }
+      if (valid) p.ws_l[slot] = (m_used + log2f(l)) * 0.69314718055994530942f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Split combine + merge with the prior state (fixed order, deterministic):
+//   L = log sum_s exp(L_s);  O = sum_s exp(L_s - L) O_s
+//   then (O, L) = merge_states(prior, (O, L))   (kernels.py:144-161)
+template <int D>
+__global__ void fwd_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_l,
+                                   int splits, int hq, int rows, View3<const float> PO,
+                                   View3<const float> PL, bool has_prior, View3<float> O,
+                                   View3<float> L) {
+  constexpr int PER = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= (int64_t)hq * rows) return;
+  const int h = (int)(gw / rows), i = (int)(gw % rows);
+  const size_t stride = (size_t)hq * rows;
+  float mx = -INFINITY;
+  for (int s = 0; s < splits; ++s) mx = fmaxf(mx, ws_l[s * stride + gw]);
+  float acc[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+  float tot = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float w = __expf(ws_l[s * stride + gw] - mx);
+    tot += w;
+    const float* src = ws_o + (s * stride + gw) * D + lane * PER;
+    if constexpr (PER == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src);
+      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+    } else {
+      const float2 v = *reinterpret_cast<const float2*>(src);
+      acc[0] += w * v.x; acc[1] += w * v.y;
+    }
+  }
+  float lse = mx + __logf(tot);
+  const float inv = 1.f / tot;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) acc[e] *= inv;
+  if (has_prior) {
+    const float lp = *PL.at(h, i);
+    const float hi = fmaxf(lp, lse);
+    const float lm = (hi == -INFINITY) ? -INFINITY : hi + log1pf(__expf(fminf(lp, lse) - hi));
+    const float safe = (lm == -INFINITY) ? 0.f : lm;
+    const float wp = __expf(lp - safe), wd = __expf(lse - safe);
+    const float* po = PO.at(h, i) + lane * PER;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = wp * po[e] + wd * acc[e];
+    lse = lm;
+  }
+  float* o = O.at(h, i) + lane * PER;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) o[e] = acc[e];
+  if (lane == 0) *L.at(h, i) = lse;
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+// bf16 [heads, rows, d] view -> 3-D TMA map with a (64, 128, 1) box, 128B swizzle.
+bool make_tma_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t rs = (uint64_t)v->row_stride * 2;
+  uint64_t hs = (uint64_t)v->head_stride * 2;
+  if (v->heads <= 1) hs = rs * (uint64_t)(v->rows > 0 ? v->rows : 1);
+  cuuint64_t dims[3] = {(cuuint64_t)v->d, (cuuint64_t)v->rows, (cuuint64_t)v->heads};
+  cuuint64_t strides[2] = {rs, hs};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, v->data, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+bool is_sm100() {
+  static int cached = -1;
+  if (cached < 0) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached = (major == 10 && minor == 0) ? 1 : 0;
+  }
+  return cached == 1;
+}
+
+bool tma_view_ok(const lvx_view* v) {
+  return v->dtype == LVX_BF16 && (reinterpret_cast<uintptr_t>(v->data) & 15) == 0 &&
+         (v->row_stride * 2) % 16 == 0 && (v->heads <= 1 || (v->head_stride * 2) % 16 == 0) &&
+         v->row_stride >= v->d && v->rows < (1ll << 31);
+}
+
+namespace {
+
+struct FwdPlan {
+  int tpq, pairs, n_tiles, tiles_per_split, splits;
+};
+
+FwdPlan plan_fwd(const lvx_view* q, const lvx_view* k) {
+  FwdPlan pl{};
+  const int G = (int)(q->heads / k->heads);
+  pl.tpq = (int)ceil_div(q->rows, kBM);
+  pl.pairs = (int)ceil_div((int64_t)G * pl.tpq, 2);
+  pl.n_tiles = (int)ceil_div(k->rows, kBN);
+  const int64_t units0 = (int64_t)pl.pairs * k->heads;
+  const int sms = device_sms();
+  // maximise modelled throughput: wave efficiency / (1 + partial-state traffic)
+  int best = 1;
+  double best_score = -1.0;
+  const int max_s = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.n_tiles / 2));
+  for (int s = 1; s <= max_s; ++s) {
+    const int tps = (int)ceil_div(pl.n_tiles, s);
+    const int real_s = (int)ceil_div(pl.n_tiles, tps);
+    const int64_t units = units0 * real_s;
+    const int64_t waves = ceil_div(units, sms);
+    const double eff = (double)units / (double)(waves * sms);
+    const double score = eff / (1.0 + 2.4 * real_s / pl.n_tiles);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = s;
+    }
+  }
+  pl.tiles_per_split = (int)ceil_div(pl.n_tiles, best);
+  pl.splits = (int)ceil_div(pl.n_tiles, pl.tiles_per_split);
+  return pl;
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+template <int D>
+int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double scale, void* ws,
+               cudaStream_t st) {
+  const FwdPlan pl = plan_fwd(q, k);
+  CUtensorMap mq, mk, mv;
+  if (!make_tma_3d(&mq, q, kBM) || !make_tma_3d(&mk, k, kBN) || !make_tma_3d(&mv, v, kBN))
+    return LVX_ECUDA;
+  FwdParams p{};
+  p.hq = (int)q->heads;
+  p.hkv = (int)k->heads;
+  p.G = p.hq / p.hkv;
+  p.rows_q = (int)q->rows;
+  p.rows_kv = (int)k->rows;
+  p.tpq = pl.tpq;
+  p.n_tiles = pl.n_tiles;
+  p.tiles_per_split = pl.tiles_per_split;
+  p.splits = pl.splits;
+  p.scale_log2 = (float)(scale * 1.4426950408889634);
+  const size_t n = (size_t)q->heads * q->rows;
+  p.ws_o = static_cast<float*>(ws);
+  p.ws_l = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.splits * n * D * 4));
+  constexpr int smem = FwdCfg<D>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return LVX_ECUDA;
+    attr = true;
+  }
+  dim3 grid(pl.pairs, pl.splits, (unsigned)k->heads);
+  fwd_kernel<D><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+}  // namespace
+
+bool tc_fwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
+  if (getenv("LVX_DISABLE_TC")) return false;
+  if (q->dtype != LVX_BF16 || (q->d != 64 && q->d != 128)) return false;
+  if (!tma_view_ok(q) || !tma_view_ok(k) || !tma_view_ok(v)) return false;
+  if (k->heads == 0 || q->heads % k->heads) return false;
+  return is_sm100();
+}
+
+size_t tc_fwd_workspace(const lvx_view* q, const lvx_view* k) {
+  if (k->rows == 0 || q->rows == 0) return 256;
+  const FwdPlan pl = plan_fwd(q, k);
+  const size_t n = (size_t)q->heads * q->rows;
+  return align256(pl.splits * n * q->d * 4) + align256(pl.splits * n * 4);
+}
+
+int tc_fwd_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v, double scale,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < tc_fwd_workspace(q, k)) return LVX_EWORKSPACE;
+  return q->d == 128 ? launch_fwd<128>(q, k, v, scale, ws, st)
+                     : launch_fwd<64>(q, k, v, scale, ws, st);
+}
+
+int tc_fwd_finish(const lvx_view* q, const lvx_view* k, const lvx_view* po, const lvx_view* pl_,
+                  const lvx_view* o, const lvx_view* l, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  if (ws_bytes < tc_fwd_workspace(q, k)) return LVX_EWORKSPACE;
+  const FwdPlan pl = plan_fwd(q, k);
+  const size_t n = (size_t)q->heads * q->rows;
+  const float* wo = static_cast<const float*>(ws);
+  const float* wl =
+      reinterpret_cast<const float*>(static_cast<const char*>(ws) + align256(pl.splits * n * q->d * 4));
+  const bool prior = po && pl_;
+  View3<const float> POv{}, PLv{};
+  if (prior) {
+    POv = View3<const float>{static_cast<const float*>(po->data), po->heads, po->rows, po->d,
+                             po->head_stride, po->row_stride};
+    PLv = View3<const float>{static_cast<const float*>(pl_->data), pl_->heads, pl_->rows, 1,
+                             pl_->head_stride, pl_->row_stride};
+  }
+  const int threads = 256;
+  const int64_t blocks = ceil_div((int64_t)n * 32, threads);
+  if (q->d == 128)
+    fwd_combine_kernel<128><<<blocks, threads, 0, st>>>(wo, wl, pl.splits, (int)q->heads,
+                                                        (int)q->rows, POv, PLv, prior,
+                                                        make_view<float>(o), make_view<float>(l));
+  else
+    fwd_combine_kernel<64><<<blocks, threads, 0, st>>>(wo, wl, pl.splits, (int)q->heads,
+                                                       (int)q->rows, POv, PLv, prior,
+                                                       make_view<float>(o), make_view<float>(l));
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+}  // namespace lvx

@@ -1,0 +1,118 @@
+"""bf16 tensor-core (tcgen05/TMEM/TMA) path vs the oracle.
+
+Tolerance (stated): max-normalised error <= 1e-2 against the
+f64 oracle evaluated on the SAME bf16-rounded inputs; the dominant error is
+P rounded to bf16 before the PV MMA (emulated bound ~2e-3 at C1)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lvx_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL_BF16 = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_02406_b200 import build
+    build.build()
+
+
+def bf16_inputs(hq, hkv, sq, skv, d, seed, q_scale=1.0):
+    Q, K, V, dO = orc.make_inputs(sq, skv, hq, d, seed, hkv=hkv)
+    Q = Q * q_scale
+    ts = [torch.from_numpy(t).to("cuda", torch.bfloat16) for t in (Q, K, V, dO)]
+    f64 = [t.double().cpu().numpy() for t in ts]
+    return ts, f64
+
+
+SHAPES = [  # hq, hkv, sq, skv, d
+    (1, 1, 128, 128, 128), (2, 2, 200, 1000, 128), (8, 2, 77, 515, 64), (4, 1, 256, 4096, 128),
+    (8, 8, 128, 4096, 64), (3, 3, 5, 7, 128), (32, 8, 64, 640, 128), (2, 1, 300, 129, 64)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_tc_forward_vs_oracle(shape):
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import _lib
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, _), (Q, K, V, _) = bf16_inputs(hq, hkv, sq, skv, d, seed=hash(shape) % 1000)
+    assert _lib.load().lvx_tc_eligible(_lib.view(q), _lib.view(k)) == 1
+    st = lvx.blockwise_attention(q, k, v)
+    torch.cuda.synchronize()
+    O, L = orc.blockwise_attention(Q, K, V)
+    eo = orc.max_norm_error(st.O.cpu().numpy(), O)
+    el = orc.max_norm_error(st.L.cpu().numpy(), L)
+    print(f"\nTC fwd {shape}: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
+def test_tc_forward_sharp_scores_rescale():
+    # Q x 8 makes the running max jump across KV tiles: exercises the lazy O rescale
+    import paper_2502_02406_b200 as lvx
+    (q, k, v, _), (Q, K, V, _) = bf16_inputs(2, 1, 130, 2000, 128, seed=9, q_scale=8.0)
+    st = lvx.blockwise_attention(q, k, v)
+    O, L = orc.blockwise_attention(Q, K, V)
+    eo = orc.max_norm_error(st.O.cpu().numpy(), O)
+    el = orc.max_norm_error(st.L.cpu().numpy(), L)
+    print(f"\nTC fwd sharp: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
+def test_tc_forward_prior_merge_and_split_combine():
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import kernels as Kn
+    (q, k, v, _), (Q, K, V, _) = bf16_inputs(4, 2, 160, 6000, 128, seed=4)
+    half = 2500
+    # prior = state of the first KV block, then fused finish merges the second
+    a = lvx.blockwise_attention(q, k[:, :half], v[:, :half])
+    O = torch.empty(q.shape, dtype=torch.float32, device="cuda")
+    L = torch.empty(q.shape[:2], dtype=torch.float32, device="cuda")
+    k2, v2 = k[:, half:].contiguous(), v[:, half:].contiguous()
+    ws = Kn.workspace(Kn.fwd_workspace_bytes(q, k2))
+    Kn.fwd_partial(q, k2, v2, 1 / np.sqrt(128), ws)
+    Kn.fwd_finish(q, k2, ws, O, L, a.O, a.L)
+    Od, Ld = orc.dense_attention(Q, K, V)
+    eo = orc.max_norm_error(O.cpu().numpy(), Od)
+    el = orc.max_norm_error(L.cpu().numpy(), Ld)
+    print(f"\nTC fwd merge: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
+def test_tc_matches_simt_bf16():
+    import paper_2502_02406_b200 as lvx
+    (q, k, v, _), _ = bf16_inputs(8, 2, 256, 3000, 128, seed=12)
+    tc = lvx.blockwise_attention(q, k, v)
+    os.environ["LVX_DISABLE_TC"] = "1"
+    try:
+        si = lvx.blockwise_attention(q, k, v)
+    finally:
+        del os.environ["LVX_DISABLE_TC"]
+    e = orc.max_norm_error(tc.O.cpu().numpy(), si.O.cpu().numpy())
+    print(f"\nTC vs SIMT bf16: {e:.2e}")
+    assert e <= TOL_BF16
+
+
+def test_tc_forward_large_vs_torch_fp32():
+    """Per-GPU round shape of C2 (Llama-3-V, n=8) at 1/8 KV: torch fp32 reference."""
+    import paper_2502_02406_b200 as lvx
+    torch.manual_seed(0)
+    hq, hkv, sq, skv, d = 32, 8, 256, 16384, 128
+    q = (torch.rand(hq, sq, d, device="cuda") * 2 - 1).bfloat16()
+    k = (torch.rand(hkv, skv, d, device="cuda") * 2 - 1).bfloat16()
+    v = (torch.rand(hkv, skv, d, device="cuda") * 2 - 1).bfloat16()
+    st = lvx.blockwise_attention(q, k, v)
+    ke = k.float().repeat_interleave(hq // hkv, 0)
+    ve = v.float().repeat_interleave(hq // hkv, 0)
+    s = (q.float() @ ke.transpose(1, 2)) / np.sqrt(d)
+    ref_l = torch.logsumexp(s, dim=-1)
+    ref_o = torch.softmax(s, dim=-1) @ ve
+    eo = ((st.O - ref_o).abs().max() / ref_o.abs().max()).item()
+    el = ((st.L - ref_l).abs().max() / ref_l.abs().max()).item()
+    print(f"\nTC fwd C2-round: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
