@@ -107,11 +107,11 @@ def dense_attention(Q, K, V, scale=None):
     if K.shape[1] == 0:
         return np.zeros((h, sq, d), out_dt), np.full((h, sq), -np.inf, out_dt)
     q, k, v = _f64(Q, expand_kv(K, h), expand_kv(V, h))
-    s = scale * np.einsum("hid,hjd->hij", q, k)
+    s = scale * (q @ k.transpose(0, 2, 1))
     m = s.max(axis=2, keepdims=True)
     w = np.exp(s - m)
     tot = w.sum(axis=2, keepdims=True)
-    o = np.einsum("hij,hjd->hid", w, v) / tot
+    o = (w @ v) / tot
     lse = (m + np.log(tot))[..., 0]
     return o.astype(out_dt), lse.astype(out_dt)
 
@@ -134,12 +134,12 @@ def blockwise_attention(Q, K, V, scale=None, tile_rows: int = 64):
     step = min(tile_rows, skv)
     for lo in range(0, skv, step):
         kt, vt = k[:, lo:lo + step], v[:, lo:lo + step]
-        st = scale * np.einsum("hid,hjd->hij", q, kt)
+        st = scale * (q @ kt.transpose(0, 2, 1))
         new_max = np.maximum(run_max, st.max(axis=2))
         p = np.exp(st - new_max[..., None])
         corr = np.exp(run_max - new_max)
         run_sum = corr * run_sum + p.sum(axis=2)
-        acc = corr[..., None] * acc + np.einsum("hij,hjd->hid", p, vt)
+        acc = corr[..., None] * acc + (p @ vt)
         run_max = new_max
     return (acc / run_sum[..., None]).astype(out_dt), \
         (run_max + np.log(run_sum)).astype(out_dt)
@@ -176,11 +176,11 @@ def blockwise_attention_backward(Q, K, V, L, D, dO, scale=None):
     hkv = K.shape[0]
     scale = default_scale(d) if scale is None else scale
     q, k, v, g, lse, dd = _f64(Q, expand_kv(K, h), expand_kv(V, h), dO, L, D)
-    p = np.exp(scale * np.einsum("hid,hjd->hij", q, k) - lse[..., None])
-    dv = np.einsum("hij,hid->hjd", p, g)
-    ds = p * (np.einsum("hid,hjd->hij", g, v) - dd[..., None])
-    dq = scale * np.einsum("hij,hjd->hid", ds, k)
-    dk = scale * np.einsum("hij,hid->hjd", ds, q)
+    p = np.exp(scale * (q @ k.transpose(0, 2, 1)) - lse[..., None])
+    dv = (p.transpose(0, 2, 1) @ g)
+    ds = p * ((g @ v.transpose(0, 2, 1)) - dd[..., None])
+    dq = scale * (ds @ k)
+    dk = scale * (ds.transpose(0, 2, 1) @ q)
     return (dq.astype(out_dt), reduce_kv_grad(dk, hkv).astype(out_dt),
             reduce_kv_grad(dv, hkv).astype(out_dt))
 
