@@ -1,0 +1,398 @@
+"""LV-XAttn fwd+bwd benchmark on B200 (BASELINE.json configs[1], Llama-3-V).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--strategy lvx|ring]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+    python bench.py --impl reference ...                   (the reference CPU path)
+
+Workload (strong scaling; total work fixed as N grows): one cross-attention
+layer, Lq = 2048 text queries, 32 query heads / 8 KV heads (GQA), head_dim 128,
+Lkv = 1,048,576 visual tokens, bf16 inputs, forward + backward.  Each rank
+holds its 1/N shard of K/V (and of Q/dO) resident in HBM; a step is one
+lvx_forward + lvx_backward (Algorithm 1 + its backward) over NCCL.
+Inputs are synthetic uniform[-1, 1] (seeded, generated on the device); every
+rank's K/V shard (>= 512 MiB) is larger than the 126 MB L2, so no L2 flush is
+needed between steps.
+
+Printed (rank 0, one JSON line): value = whole-job attention TFLOP/s
+(14 Lq Lkv hq d per step), ms_per_step = ms per layer fwd+bwd,
+the roofline of the dominant kernel, the no-communication arm (same schedule,
+hops skipped) and the overhead against it, measured NVLink
+bytes per step against the closed form and the paper's Q+O model, the
+Ring-Attention baseline (N > 1), the CPU reference timed on the host, the
+end-to-end number through the host-buffer API, clocks, and kernel launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG = dict(workload="llama3v-cross-attn-C2", s_q=2048, s_kv=1 << 20, hq=32, hkv=8, d=128)
+METRIC = "cross-attn fwd+bwd ms/layer & TFLOP/s at 1/2/4/8 B200; overhead vs no-comm bound"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--strategy", default="lvx", choices=["lvx", "ring"])
+    ap.add_argument("--no-ring-compare", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--skv", type=int, default=CFG["s_kv"], help="(dev) override Lkv")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j["bf16_tflops"], j["bf16_tflops_sustained"], j["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_rate(budget_s: float = 12.0):
+    """The reference algorithm on the host cores (oracle port of
+    strategies.py lvx fwd+bwd, numpy f64 + multithreaded BLAS), on a bounded
+    sample of the C2 workload: Lq=64 query rows x Lkv=16384 visual tokens, same
+    heads/head_dim, repeated until ``budget_s``.  Returns (TFLOP/s, sample)."""
+    import numpy as np
+    from oracle import lvx_oracle as orc
+    sq, skv = 64, 16384
+    Q, K, V, dO = orc.make_inputs(sq, skv, CFG["hq"], CFG["d"], seed=7, hkv=CFG["hkv"])
+    Q, K, V, dO = (t.astype(np.float32) for t in (Q, K, V, dO))
+    flops = orc.attention_flops(sq, skv, CFG["hq"], CFG["d"])
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        orc.simulate("lvx", Q, K, V, dO, n=1)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 50:
+            break
+    sample = (f"oracle port of lvx fwd+bwd (numpy f64, {os.cpu_count()} host threads BLAS), "
+              f"Lq={sq} x Lkv={skv}, hq=32/hkv=8, d=128, fp32 in, {reps} reps in {el:.1f}s")
+    return flops * reps / el / 1e12, sample
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals, sample = [], ""
+    for i in range(args.warmup + args.steps):
+        v, sample = cpu_reference_rate(budget_s=4.0)
+        if i >= args.warmup:
+            vals.append(v)
+    val = statistics.median(vals)
+    flops = 14.0 * CFG["s_q"] * CFG["s_kv"] * CFG["hq"] * CFG["d"]
+    ms = flops / (val * 1e12) * 1e3
+    line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**CFG, "note": "CPU sample of the workload; ms_per_step extrapolated"},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": os.cpu_count(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- native arm
+
+def native_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    from paper_2502_02406_b200 import build
+    if rank == 0 and not build.LIB.exists():
+        build.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import _lib, volumes
+    from paper_2502_02406_b200.strategies import (RoundTrace, ShardSpec, lvx_backward,
+                                                  lvx_forward, ring_backward, ring_forward)
+
+    s_q, s_kv, hq, hkv, d = CFG["s_q"], args.skv, CFG["hq"], CFG["hkv"], CFG["d"]
+    scale = 1.0 / d ** 0.5
+    shards = ShardSpec.balanced(s_q, s_kv, world)
+    qa, qb = shards.q_ranges[rank]
+    ka, kb = shards.kv_ranges[rank]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def rnd(*shape):
+        return (torch.rand(*shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+
+    q_i, k_i, v_i, do_i = rnd(hq, qb - qa, d), rnd(hkv, kb - ka, d), rnd(hkv, kb - ka, d), \
+        rnd(hq, qb - qa, d)
+    ctx = lvx.DeviceContext(rank, world, group=group, device=dev)
+    ctx_nc = lvx.DeviceContext(rank, world, group=group, device=dev, comm_enabled=False)
+    fwd, bwd = (lvx_forward, lvx_backward) if args.strategy == "lvx" else \
+        (ring_forward, ring_backward)
+
+    def step(c, traces=None, strategy=None):
+        f, b = (fwd, bwd) if strategy is None else strategy
+        tf = RoundTrace("x", "forward") if traces is not None else None
+        tb = RoundTrace("x", "backward") if traces is not None else None
+        st = f(c, shards, q_i, k_i, v_i, scale, 64, tf)
+        g = b(c, shards, q_i, k_i, v_i, st, do_i, scale, tb)
+        if traces is not None:
+            traces.append((tf, tb))
+        return st, g
+
+    def timed(c, steps, warm, strategy=None, sampler=False):
+        for _ in range(warm):
+            step(c, strategy=strategy)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        traces = []
+        launches0 = _lib.load().lvx_kernel_launches()
+        cs = ClockSampler(local) if sampler else None
+        if cs:
+            cs.__enter__()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step(c, traces, strategy)
+        e1.record()
+        torch.cuda.synchronize()
+        if cs:
+            cs.__exit__()
+        if world > 1:
+            dist.barrier()
+        launches = _lib.load().lvx_kernel_launches() - launches0
+        ms = e0.elapsed_time(e1) / steps
+        for tf, tb in traces:
+            tf.resolve()
+            tb.resolve()
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms, traces, launches, (cs.summary() if cs else None)
+
+    ms, traces, launches, clocks = timed(ctx, args.steps, args.warmup, sampler=True)
+    flops = volumes.attention_flops(s_q, s_kv, hq, d)
+    value = flops / (ms * 1e-3) / 1e12
+
+    # --- kernel roofline: dominant kernel = larger of the fwd / bwd launches
+    tf_k = statistics.mean(sum(r.compute_seconds for r in tf.rounds) for tf, _ in traces)
+    tb_k = statistics.mean(sum(r.compute_seconds for r in tb.rounds) for _, tb in traces)
+    n_rounds = len(traces[0][0].rounds)
+    rows_q = shards.q_sizes
+    # per launch (one round, one rank): 4 or 10 x |q block| x |kv shard| x hq x d
+    fwd_flops_round = 4.0 * (s_q / world) * (kb - ka) * hq * d
+    bwd_flops_round = 10.0 * (s_q / world) * (kb - ka) * hq * d
+    burst, sust, hbm, pk_kind = peaks()
+    if tb_k >= tf_k:
+        kname, kflops, kdur = "lvx_bwd (tcgen05)" if _bwd_is_tc(q_i, k_i) else "lvx_bwd (SIMT)", \
+            bwd_flops_round, tb_k / n_rounds
+    else:
+        kname, kflops, kdur = "lvx_fwd (tcgen05)", fwd_flops_round, tf_k / n_rounds
+    achieved = kflops / kdur / 1e12
+    roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": sust,
+                "unit": "TFLOP/s", "frac": achieved / sust, "traffic": None,
+                "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
+                "frac_of_burst": achieved / burst, "frac_of_nominal_2250": achieved / 2250.0,
+                "fwd_kernel_ms_per_step": tf_k * 1e3, "bwd_kernel_ms_per_step": tb_k * 1e3,
+                "fwd_tflops": 4.0 * s_q / world * (kb - ka) * hq * d * n_rounds / tf_k / 1e12,
+                "bwd_tflops": 10.0 * s_q / world * (kb - ka) * hq * d * n_rounds / tb_k / 1e12}
+
+    # --- measured NVLink bytes vs closed form and the paper's model
+    tf0, tb0 = traces[0]
+    sent = tf0.total_sent_bytes() + tb0.total_sent_bytes()
+    w = volumes.Wire.b200(hq, hkv, d, 2)
+    model = (volumes.bytes_by_worker(args.strategy, "forward", shards.q_sizes, shards.kv_sizes, w)[rank]
+             + volumes.bytes_by_worker(args.strategy, "backward", shards.q_sizes, shards.kv_sizes, w)[rank])
+    comm = {"bytes_per_step_rank0": sent, "closed_form_rank0": model,
+            "paper_q_plus_o_hop_bytes_bf16": volumes.paper_hop_bytes(s_q, world, hq, d, 2),
+            "measured_fwd_hop_bytes": (tf0.rounds[0].sent_bytes if world > 1 else 0),
+            "exposed_comm_ms_per_step": sum(r.comm_seconds for r in tf0.rounds + tb0.rounds) * 1e3}
+
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_layer": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (uniform[-1,1], seeded, generated on device)",
+           "config": {**CFG, "s_kv": s_kv, "strategy": args.strategy,
+                      "parallelism": f"kv-seq-parallel x{world} (query rotation)"
+                      if args.strategy == "lvx" else f"kv-rotation x{world}",
+                      "l2": "inputs larger than L2 (K/V shard >= 512 MiB per rank)"},
+           "roofline": roofline, "comm": comm, "clocks": clocks,
+           "gpu_launches": int(launches)}
+
+    # --- no-communication arm and the Ring baseline
+    if world > 1:
+        ms_nc, *_ = timed(ctx_nc, max(2, args.steps // 2), 1)
+        out["no_comm_ms_per_step"] = ms_nc
+        out["overhead_vs_no_comm"] = ms / ms_nc - 1.0
+        if not args.no_ring_compare and args.strategy == "lvx":
+            ms_ring, rtr, *_ = timed(ctx, max(2, args.steps // 2), 1,
+                                     strategy=(ring_forward, ring_backward))
+            out["ring_baseline"] = {"ms_per_step": ms_ring,
+                                    "value": flops / (ms_ring * 1e-3) / 1e12,
+                                    "speedup_lvx_over_ring": ms_ring / ms,
+                                    "bytes_per_step_rank0": rtr[0][0].total_sent_bytes()
+                                    + rtr[0][1].total_sent_bytes()}
+    else:
+        out["no_comm_ms_per_step"] = ms
+        out["overhead_vs_no_comm"] = 0.0
+
+    # --- end to end through the host-buffer API (pinned host -> HBM -> host)
+    if not args.no_e2e:
+        out["e2e"] = e2e_arm(args, ctx, shards, (q_i, k_i, v_i, do_i), scale, fwd, bwd, flops,
+                             world, dev)
+
+    # --- CPU reference on the host cores (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample = cpu_reference_rate()
+        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(),
+                               "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _bwd_is_tc(q, k):
+    from paper_2502_02406_b200 import _lib
+    return _lib.load().lvx_blockwise_bwd_workspace(_lib.view(q), _lib.view(k)) > 0
+
+
+def e2e_arm(args, ctx, shards, dev_inputs, scale, fwd, bwd, flops, world, dev):
+    """Each step: pinned host shard -> device, fwd+bwd, results -> pinned host."""
+    import torch
+    import torch.distributed as dist
+    host_in = [t.cpu().pin_memory() for t in dev_inputs]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    outs = None
+
+    def one():
+        nonlocal outs
+        q, k, v, g = (t.to(dev, non_blocking=True) for t in host_in)
+        st = fwd(ctx, shards, q, k, v, scale)
+        dq, dk, dv = bwd(ctx, shards, q, k, v, st, g, scale)
+        res = [st.O.to(torch.bfloat16), st.L, dq.to(torch.bfloat16), dk.to(torch.bfloat16),
+               dv.to(torch.bfloat16)]
+        if outs is None:
+            outs = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
+        for o, r in zip(outs, res):
+            o.copy_(r, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    one()
+    d2h = sum(t.numel() * t.element_size() for t in outs)
+    steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    el = (time.perf_counter() - t0) / steps
+    if world > 1:
+        t = torch.tensor([el, h2d, d2h], device=dev, dtype=torch.float64)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        el, h2d, d2h = tm[0].item(), int(t[1].item()), int(t[2].item())
+    return {"value": flops / el / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": el * 1e3,
+            "path": "pinned host shard -> HBM -> lvx_forward/lvx_backward -> pinned host "
+                    "(host-synchronised wall clock, max over ranks)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        native_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -70,6 +70,9 @@ typedef struct lvx_view {
 /* ---- introspection ---------------------------------------------------- */
 int lvx_abi_version(void);
 const char* lvx_strerror(int status);
+/* Number of kernels this library has launched in this process (a
+ * diagnostic counter; the only process-wide state, updated atomically). */
+unsigned long long lvx_kernel_launches(void);
 /* 1 when the tcgen05 path would serve (q, k) on the current device. */
 int lvx_tc_eligible(const lvx_view* q, const lvx_view* k);
 

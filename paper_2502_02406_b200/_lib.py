@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "liblvx_b200.so"
 LVX_F32, LVX_F64, LVX_BF16 = 0, 1, 2
 _DT = {torch.float32: LVX_F32, torch.float64: LVX_F64, torch.bfloat16: LVX_BF16}
 
-EXPORTS = ("lvx_abi_version", "lvx_strerror", "lvx_tc_eligible", "lvx_blockwise_fwd_workspace",
+EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eligible", "lvx_blockwise_fwd_workspace",
            "lvx_blockwise_fwd", "lvx_fwd_partial", "lvx_fwd_finish", "lvx_merge_states",
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
            "lvx_fill_empty_state", "lvx_convert")
@@ -53,6 +53,7 @@ def load() -> ctypes.CDLL:
     vp, sz, dbl, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double, ctypes.c_int
     proto = {
         "lvx_abi_version": (i32, []),
+        "lvx_kernel_launches": (ctypes.c_ulonglong, []),
         "lvx_strerror": (ctypes.c_char_p, [i32]),
         "lvx_tc_eligible": (i32, [P, P]),
         "lvx_blockwise_fwd_workspace": (sz, [P, P]),

@@ -1,8 +1,15 @@
 // C-ABI entry points (include/lvx_b200.h): argument validation and routing
 // to the tcgen05 kernels (BF16, d in {64,128}) or the exact SIMT kernels.
+#include <atomic>
+
 #include "lvx_common.cuh"
 
 using namespace lvx;
+
+namespace lvx {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+}  // namespace lvx
 
 namespace {
 
@@ -40,6 +47,10 @@ int check_state(const lvx_view* o, const lvx_view* l, const lvx_view* q) {
 extern "C" {
 
 int lvx_abi_version(void) { return LVX_ABI_VERSION; }
+
+unsigned long long lvx_kernel_launches(void) {
+  return g_launches.load(std::memory_order_relaxed);
+}
 
 const char* lvx_strerror(int s) {
   switch (s) {

@@ -85,6 +85,8 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Internal entry points implemented per translation unit (not part of the ABI).
 namespace lvx {
+// diagnostic count of kernel launches issued by this library (lvx_kernel_launches)
+void note_launch(int n = 1);
 int simt_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double scale,
              const lvx_view* prior_o, const lvx_view* prior_l, const lvx_view* o,
              const lvx_view* l, cudaStream_t st);

@@ -495,6 +495,7 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
   }
   dim3 grid(pl.pairs, pl.splits, (unsigned)k->heads);
   fwd_kernel<D><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
@@ -549,6 +550,7 @@ int tc_fwd_finish(const lvx_view* q, const lvx_view* k, const lvx_view* po, cons
     fwd_combine_kernel<64><<<blocks, threads, 0, st>>>(wo, wl, pl.splits, (int)q->heads,
                                                        (int)q->rows, POv, PLv, prior,
                                                        make_view<float>(o), make_view<float>(l));
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 

@@ -320,6 +320,7 @@ View3<const T> cview(const lvx_view* v) {
 }
 
 int launch_status() {
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
