@@ -1,0 +1,655 @@
+// tcgen05/TMEM/TMA blockwise attention backward for B200 (sm_100a).
+//
+// Replaces kernels.py:192-224 blockwise_attention_backward for bf16 inputs
+// with d in {64, 128}:  P = exp(S - L), dV = P^T dO, dP = dO V^T,
+// dS = P (dP - D), dQ = scale dS K, dK = scale dS^T Q.
+//
+// Two deterministic kernels instead of one kernel with dQ atomics (a dQ
+// atomic stream of 64 KB per (KV tile, Q tile) pair would need ~7 TB/s of L2
+// reductions at full tensor rate):
+//   bwd_dkv_kernel  KV-parallel.  One CTA owns a 128-row KV tile; dK, dV
+//                   accumulate in TMEM over every 64-row query step of the
+//                   GQA group (kernels.py:258-262 accumulate over rounds on
+//                   top of this in fp32 HBM accumulators).
+//                   MMAs: S^T = K Q^T, dP^T = V dO^T (SS); dV += P^T dO,
+//                   dK += dS^T Q (TS: P^T / dS^T live in TMEM as bf16, written
+//                   over the S^T / dP^T columns they came from).
+//   bwd_dq_kernel   Q-parallel, two 128-row query tiles per CTA sharing each
+//                   64-row K/V tile, split over the KV block.  S = Q K^T,
+//                   dP = dO V^T (SS); dQ += dS K (TS, dS in TMEM).
+// Softmax statistics enter pre-scaled: Lp = L log2(e) (+inf on padding rows,
+// so P = 0 there) and D, packed by bwd_prep_kernel into 16-byte aligned rows.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "lvx_common.cuh"
+#include "lvx_sm100.cuh"
+
+namespace lvx {
+namespace {
+
+using namespace sm100;
+
+constexpr int kStep = 64;      // q rows per step (dkv kernel) / kv rows per step (dq kernel)
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ------------------------------------------------------------------- prep
+__global__ void bwd_prep_kernel(View3<const float> L, View3<const float> Dv, int hq, int rows,
+                                int rows_pad, float* __restrict__ Lp, float* __restrict__ Dp) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)hq * rows_pad) return;
+  const int h = (int)(idx / rows_pad), r = (int)(idx % rows_pad);
+  if (r < rows) {
+    Lp[idx] = *L.at(h, r) * kLog2e;
+    Dp[idx] = *Dv.at(h, r);
+  } else {
+    Lp[idx] = INFINITY;
+    Dp[idx] = 0.f;
+  }
+}
+
+struct BwdParams {
+  int hq, hkv, G, rows_q, rows_kv, rows_pad;
+  int tq64;           // 64-row query steps per head (dkv kernel)
+  int tpq;            // 128-row query tiles per head (dq kernel)
+  int n_tiles;        // 64-row kv tiles (dq kernel)
+  int tiles_per_split, splits;
+  float scale_log2, scale;
+  const float* Lp;    // [hq][rows_pad]
+  const float* Dp;
+  float* dk; float* dv;           // fp32 accumulators [hkv][rows_kv][D] (strided)
+  int64_t dk_hs, dk_rs, dv_hs, dv_rs;
+  int accumulate;
+  float* ws_dq;       // [splits][hq][rows_q][D]
+};
+
+// ============================================================ dK / dV kernel
+template <int D>
+struct DkvCfg {
+  static constexpr int PANELS = D / 64;
+  static constexpr int KV_BYTES = 128 * D * 2;             // resident K (or V) tile
+  static constexpr int QT_BYTES = kStep * D * 2;           // one Q (or dO) step tile
+  static constexpr int SLOT = ((2 * QT_BYTES + 512 + 1023) / 1024) * 1024;
+  static constexpr int STAGES = D == 128 ? 4 : 6;
+  static constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 1;
+  static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
+  static constexpr int DV_COL = 256, DK_COL = 256 + D;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG,
+               const BwdParams p) {
+  using C = DkvCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + C::KV_BYTES;
+  uint8_t* sSlot = sV + C::KV_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + C::STAGES * C::SLOT);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;
+  uint64_t* qd_empty = qd_full + C::STAGES;
+  uint64_t* st_full = qd_empty + C::STAGES;   // [2]
+  uint64_t* pds_full = st_full + 2;           // [2]
+  uint64_t* dkv_done = pds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * 128, g = blockIdx.y;
+  const int nsteps = p.G * p.tq64;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&qd_full[s], 1);
+      mbar_init(&qd_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&st_full[b], 1);
+      mbar_init(&pds_full[b], 128);
+    }
+    mbar_init(dkv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmG);
+      mbar_arrive_expect_tx(kv_full, 2 * C::KV_BYTES);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma_load_3d(sK + pn * 128 * 128, &tmK, kv_full, pn * 64, n0, g);
+        tma_load_3d(sV + pn * 128 * 128, &tmV, kv_full, pn * 64, n0, g);
+      }
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % C::STAGES, u = i / C::STAGES;
+        if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
+        const int h = g * p.G + i / p.tq64, r0 = (i % p.tq64) * kStep;
+        uint8_t* slot = sSlot + s * C::SLOT;
+        mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 512);
+        for (int pn = 0; pn < C::PANELS; ++pn) {
+          tma_load_3d(slot + pn * kStep * 128, &tmQ, &qd_full[s], pn * 64, r0, h);
+          tma_load_3d(slot + C::QT_BYTES + pn * kStep * 128, &tmG, &qd_full[s], pn * 64, r0, h);
+        }
+        const size_t off = (size_t)h * p.rows_pad + r0;
+        bulk_load(slot + 2 * C::QT_BYTES, p.Lp + off, 256, &qd_full[s]);
+        bulk_load(slot + 2 * C::QT_BYTES + 256, p.Dp + off, 256, &qd_full[s]);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
+      constexpr uint32_t idKV = idesc_bf16(128, D, false, true);
+      const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      for (int i = 0; i <= nsteps; ++i) {
+        if (i < nsteps) {
+          const int s = i % C::STAGES, b = i & 1;
+          mbar_wait(&qd_full[s], (i / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t qb = smem_u32(sSlot + s * C::SLOT), gb = qb + C::QT_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ko = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t qo = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
+            mma_bf16_ss(tmem + b * 128, umma_desc_sw128(kb + ko, 0, 1024),
+                        umma_desc_sw128(qb + qo, 0, 1024), idS, kk > 0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ko = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t qo = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
+            mma_bf16_ss(tmem + b * 128 + 64, umma_desc_sw128(vb + ko, 0, 1024),
+                        umma_desc_sw128(gb + qo, 0, 1024), idS, kk > 0);
+          }
+          mma_commit(&st_full[b]);
+        }
+        if (i > 0) {
+          const int ii = i - 1, s = ii % C::STAGES, b = ii & 1;
+          mbar_wait(&pds_full[b], (ii >> 1) & 1);
+          tc_fence_after();
+          const uint32_t qb = smem_u32(sSlot + s * C::SLOT), gb = qb + C::QT_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < kStep / 16; ++kk)   // dV += P^T dO
+            mma_bf16_ts(tmem + C::DV_COL, tmem + b * 128 + kk * 8,
+                        umma_desc_sw128(gb + kk * 16 * 128, kStep * 128, 1024), idKV,
+                        (ii > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < kStep / 16; ++kk)   // dK += dS^T Q
+            mma_bf16_ts(tmem + C::DK_COL, tmem + b * 128 + 64 + kk * 8,
+                        umma_desc_sw128(qb + kk * 16 * 128, kStep * 128, 1024), idKV,
+                        (ii > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&qd_empty[s]);
+        }
+      }
+      mma_commit(dkv_done);
+    }
+  } else {
+    // ------------------------------------------------ softmax (kv row per thread)
+    const int r = warp * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int i = 0; i < nsteps; ++i) {
+      const int s = i % C::STAGES, b = i & 1;
+      mbar_wait(&st_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      const float* lp = reinterpret_cast<const float*>(sSlot + s * C::SLOT + 2 * C::QT_BYTES);
+      const float* dp = lp + 64;
+      uint32_t pp[32], dd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sv[32], gv[32];
+        tmem_ld32(tl + b * 128 + hh * 32, sv);
+        tmem_ld32(tl + b * 128 + 64 + hh * 32, gv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int c = hh * 32 + e;
+          const float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lp[c]));
+          const float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lp[c + 1]));
+          const float d0 = p0 * (__uint_as_float(gv[e]) - dp[c]);
+          const float d1 = p1 * (__uint_as_float(gv[e + 1]) - dp[c + 1]);
+          pp[hh * 16 + e / 2] = pack_bf16(p0, p1);
+          dd[hh * 16 + e / 2] = pack_bf16(d0, d1);
+        }
+      }
+      tmem_st32(tl + b * 128, pp);        // P^T over S^T
+      tmem_st32(tl + b * 128 + 64, dd);   // dS^T over dP^T
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&pds_full[b]);
+    }
+    // epilogue: dV, scale * dK (+)= into the fp32 accumulators
+    mbar_wait(dkv_done, 0);
+    tc_fence_after();
+    const int row = n0 + r;
+    const bool valid = row < p.rows_kv;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = which ? C::DK_COL : C::DV_COL;
+      const float mul = which ? p.scale : 1.f;
+      float* dst = which ? p.dk + (int64_t)g * p.dk_hs + (int64_t)row * p.dk_rs
+                         : p.dv + (int64_t)g * p.dv_hs + (int64_t)row * p.dv_rs;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tl + col + c * 32, v);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            float4* ptr = reinterpret_cast<float4*>(dst + c * 32 + e);
+            float4 a = make_float4(__uint_as_float(v[e]) * mul, __uint_as_float(v[e + 1]) * mul,
+                                   __uint_as_float(v[e + 2]) * mul,
+                                   __uint_as_float(v[e + 3]) * mul);
+            if (p.accumulate) {
+              const float4 o = *ptr;
+              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+            }
+            *ptr = a;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ================================================================ dQ kernel
+template <int D>
+struct DqCfg {
+  static constexpr int PANELS = D / 64;
+  static constexpr int Q_BYTES = 128 * D * 2;
+  static constexpr int KVT_BYTES = kStep * D * 2;
+  static constexpr int SLOT = 2 * KVT_BYTES;
+  static constexpr int STAGES = D == 128 ? 3 : 6;
+  static constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 1;
+  static constexpr int SMEM = 1024 + 4 * Q_BYTES + STAGES * SLOT + NBAR * 8 + 16;
+  static constexpr int DQ_COL = 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG,
+              const BwdParams p) {
+  using C = DqCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint8_t* sQ = sm;                       // [2] tiles
+  uint8_t* sG = sQ + 2 * C::Q_BYTES;      // [2] dO tiles
+  uint8_t* sKV = sG + 2 * C::Q_BYTES;     // STAGES x (K | V)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::SLOT);
+  uint64_t* qd_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::STAGES;
+  uint64_t* s_full = kv_empty + C::STAGES;   // [2]
+  uint64_t* ds_full = s_full + 2;            // [2]
+  uint64_t* dq_done = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
+  const int kv_t0 = split * p.tiles_per_split;
+  const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
+  bool active[2];
+  int qh[2], row0[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int tt = 2 * pair + t;
+    active[t] = tt < p.G * p.tpq;
+    qh[t] = g * p.G + tt / p.tpq;
+    row0[t] = (tt % p.tpq) * 128;
+  }
+
+  if (threadIdx.x == 0) {
+    mbar_init(qd_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&ds_full[t], 128);
+    }
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmG);
+      mbar_arrive_expect_tx(qd_full, (active[0] + active[1]) * 2 * C::Q_BYTES);
+      for (int t = 0; t < 2; ++t)
+        if (active[t])
+          for (int pn = 0; pn < C::PANELS; ++pn) {
+            tma_load_3d(sQ + t * C::Q_BYTES + pn * 128 * 128, &tmQ, qd_full, pn * 64, row0[t],
+                        qh[t]);
+            tma_load_3d(sG + t * C::Q_BYTES + pn * 128 * 128, &tmG, qd_full, pn * 64, row0[t],
+                        qh[t]);
+          }
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % C::STAGES, u = j / C::STAGES;
+        if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
+        uint8_t* slot = sKV + s * C::SLOT;
+        mbar_arrive_expect_tx(&kv_full[s], C::SLOT);
+        const int kr = (kv_t0 + j) * kStep;
+        for (int pn = 0; pn < C::PANELS; ++pn) {
+          tma_load_3d(slot + pn * kStep * 128, &tmK, &kv_full[s], pn * 64, kr, g);
+          tma_load_3d(slot + C::KVT_BYTES + pn * kStep * 128, &tmV, &kv_full[s], pn * 64, kr, g);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
+      constexpr uint32_t idQ = idesc_bf16(128, D, false, true);
+      mbar_wait(qd_full, 0);
+      tc_fence_after();
+      auto issue_sdp = [&](int t, int j) {
+        const int s = j % C::STAGES;
+        const uint32_t kb = smem_u32(sKV + s * C::SLOT), vb = kb + C::KVT_BYTES;
+        const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES), gb = smem_u32(sG + t * C::Q_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qo = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t ko = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
+          mma_bf16_ss(tmem + t * 128, umma_desc_sw128(qb + qo, 0, 1024),
+                      umma_desc_sw128(kb + ko, 0, 1024), idS, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qo = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t ko = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
+          mma_bf16_ss(tmem + t * 128 + 64, umma_desc_sw128(gb + qo, 0, 1024),
+                      umma_desc_sw128(vb + ko, 0, 1024), idS, kk > 0);
+        }
+        mma_commit(&s_full[t]);
+      };
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < 2; ++t)
+        if (active[t]) issue_sdp(t, 0);
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % C::STAGES;
+        const uint32_t kb = smem_u32(sKV + s * C::SLOT);
+        bool next_ready = false;
+        for (int t = 0; t < 2; ++t) {
+          if (!active[t]) continue;
+          mbar_wait(&ds_full[t], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kStep / 16; ++kk)   // dQ += dS K
+            mma_bf16_ts(tmem + C::DQ_COL + t * D, tmem + t * 128 + kk * 8,
+                        umma_desc_sw128(kb + kk * 16 * 128, kStep * 128, 1024), idQ,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          if (j + 1 < nt) {
+            if (!next_ready) {
+              const int s1 = (j + 1) % C::STAGES;
+              mbar_wait(&kv_full[s1], ((j + 1) / C::STAGES) & 1);
+              tc_fence_after();
+              next_ready = true;
+            }
+            issue_sdp(t, j + 1);
+          }
+        }
+        mma_commit(&kv_empty[s]);
+      }
+      mma_commit(dq_done);
+    }
+  } else {
+    // ------------------------------------------ softmax (query row per thread)
+    const int t = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    if (active[t]) {
+      const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+      const int row = row0[t] + r;
+      const size_t prow = (size_t)qh[t] * p.rows_pad + row;
+      const float lrow = p.Lp[prow], drow = p.Dp[prow];
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        const int nvalid = min(kStep, p.rows_kv - (kv_t0 + j) * kStep);
+        uint32_t dd[32];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t sv[32], gv[32];
+          tmem_ld32(tl + t * 128 + hh * 32, sv);
+          tmem_ld32(tl + t * 128 + 64 + hh * 32, gv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int c = hh * 32 + e;
+            const float p0 = c < nvalid ? ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow)) : 0.f;
+            const float p1 =
+                c + 1 < nvalid ? ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lrow)) : 0.f;
+            dd[hh * 16 + e / 2] =
+                pack_bf16(p0 * (__uint_as_float(gv[e]) - drow), p1 * (__uint_as_float(gv[e + 1]) - drow));
+          }
+        }
+        tmem_st32(tl + t * 128, dd);   // dS over S
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&ds_full[t]);
+      }
+      mbar_wait(dq_done, 0);
+      tc_fence_after();
+      const bool valid = row < p.rows_q;
+      float* dst = p.ws_dq + (((size_t)split * p.hq + qh[t]) * p.rows_q + row) * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tl + C::DQ_COL + t * D + c * 32, v);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + c * 32 + e) =
+                make_float4(__uint_as_float(v[e]) * p.scale, __uint_as_float(v[e + 1]) * p.scale,
+                            __uint_as_float(v[e + 2]) * p.scale, __uint_as_float(v[e + 3]) * p.scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// dq (+)= sum_s ws_dq[s]  (fixed order, deterministic)
+template <int D>
+__global__ void dq_combine_kernel(const float* __restrict__ ws, int splits, int hq, int rows,
+                                  View3<float> dQ, int accumulate) {
+  constexpr int PER = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= (int64_t)hq * rows) return;
+  const int h = (int)(gw / rows), i = (int)(gw % rows);
+  const size_t stride = (size_t)hq * rows * D;
+  float acc[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* src = ws + s * stride + (size_t)gw * D + lane * PER;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] += src[e];
+  }
+  float* o = dQ.at(h, i) + lane * PER;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) o[e] = accumulate ? o[e] + acc[e] : acc[e];
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct BwdPlan {
+  int tq64, tpq, pairs, rows_pad, n_tiles, tiles_per_split, splits;
+};
+
+BwdPlan plan_bwd(const lvx_view* q, const lvx_view* k) {
+  BwdPlan pl{};
+  const int G = (int)(q->heads / k->heads);
+  pl.tq64 = (int)ceil_div(q->rows, kStep);
+  pl.tpq = (int)ceil_div(q->rows, 128);
+  pl.rows_pad = pl.tpq * 128;
+  pl.pairs = (int)ceil_div((int64_t)G * pl.tpq, 2);
+  pl.n_tiles = (int)ceil_div(k->rows, kStep);
+  const int64_t units0 = (int64_t)pl.pairs * k->heads;
+  const int sms = device_sms();
+  int best = 1;
+  double best_score = -1.0;
+  const int max_s = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.n_tiles / 4));
+  for (int s = 1; s <= max_s; ++s) {
+    const int tps = (int)ceil_div(pl.n_tiles, s);
+    const int real_s = (int)ceil_div(pl.n_tiles, tps);
+    const int64_t units = units0 * real_s;
+    const int64_t waves = ceil_div(units, sms);
+    const double eff = (double)units / (double)(waves * sms);
+    // partial dQ traffic relative to the split's work (fp32 write + read)
+    const double score = eff / (1.0 + 1.6 * real_s / pl.n_tiles);
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = s;
+    }
+  }
+  pl.tiles_per_split = (int)ceil_div(pl.n_tiles, best);
+  pl.splits = (int)ceil_div(pl.n_tiles, pl.tiles_per_split);
+  return pl;
+}
+
+bool f32_rows_ok(const lvx_view* v) {
+  return v->dtype == LVX_F32 && (reinterpret_cast<uintptr_t>(v->data) & 15) == 0 &&
+         v->row_stride % 4 == 0 && (v->heads <= 1 || v->head_stride % 4 == 0);
+}
+
+template <int D>
+int launch_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
+               const lvx_view* Dv, const lvx_view* dO, double scale, const lvx_view* dq,
+               const lvx_view* dk, const lvx_view* dvv, int accumulate, void* ws, cudaStream_t st) {
+  const BwdPlan pl = plan_bwd(q, k);
+  BwdParams p{};
+  p.hq = (int)q->heads;
+  p.hkv = (int)k->heads;
+  p.G = p.hq / p.hkv;
+  p.rows_q = (int)q->rows;
+  p.rows_kv = (int)k->rows;
+  p.rows_pad = pl.rows_pad;
+  p.tq64 = pl.tq64;
+  p.tpq = pl.tpq;
+  p.n_tiles = pl.n_tiles;
+  p.tiles_per_split = pl.tiles_per_split;
+  p.splits = pl.splits;
+  p.scale = (float)scale;
+  p.scale_log2 = (float)(scale * 1.4426950408889634);
+  char* w = static_cast<char*>(ws);
+  const size_t lp_bytes = align256((size_t)p.hq * p.rows_pad * 4);
+  float* Lp = reinterpret_cast<float*>(w);
+  float* Dp = reinterpret_cast<float*>(w + lp_bytes);
+  p.Lp = Lp;
+  p.Dp = Dp;
+  p.ws_dq = reinterpret_cast<float*>(w + 2 * lp_bytes);
+  p.dk = static_cast<float*>(dk->data);
+  p.dv = static_cast<float*>(dvv->data);
+  p.dk_hs = dk->head_stride;
+  p.dk_rs = dk->row_stride;
+  p.dv_hs = dvv->head_stride;
+  p.dv_rs = dvv->row_stride;
+  p.accumulate = accumulate;
+
+  {
+    const int64_t total = (int64_t)p.hq * p.rows_pad;
+    bwd_prep_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+        View3<const float>{static_cast<const float*>(L->data), L->heads, L->rows, 1,
+                           L->head_stride, L->row_stride},
+        View3<const float>{static_cast<const float*>(Dv->data), Dv->heads, Dv->rows, 1,
+                           Dv->head_stride, Dv->row_stride},
+        p.hq, p.rows_q, p.rows_pad, Lp, Dp);
+    note_launch();
+  }
+  CUtensorMap mq64, mg64, mq128, mg128, mk128, mv128, mk64, mv64;
+  if (!make_tma_3d(&mq64, q, kStep) || !make_tma_3d(&mg64, dO, kStep) ||
+      !make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128) ||
+      !make_tma_3d(&mk64, k, kStep) || !make_tma_3d(&mv64, v, kStep))
+    return LVX_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DkvCfg<D>::SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DqCfg<D>::SMEM) != cudaSuccess)
+      return LVX_ECUDA;
+    attr = true;
+  }
+  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 192,
+                      DkvCfg<D>::SMEM, st>>>(mq64, mk128, mv128, mg64, p);
+  note_launch();
+  bwd_dq_kernel<D><<<dim3(pl.pairs, pl.splits, (unsigned)k->heads), 320, DqCfg<D>::SMEM, st>>>(
+      mq128, mk64, mv64, mg128, p);
+  note_launch();
+  const int64_t rows_total = (int64_t)p.hq * p.rows_q;
+  dq_combine_kernel<D><<<ceil_div(rows_total * 32, 256), 256, 0, st>>>(
+      p.ws_dq, p.splits, p.hq, p.rows_q, make_view<float>(dq), accumulate);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+}  // namespace
+
+bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
+  if (getenv("LVX_DISABLE_TC")) return false;
+  if (q->dtype != LVX_BF16 || (q->d != 64 && q->d != 128)) return false;
+  if (!tma_view_ok(q) || !tma_view_ok(k) || !tma_view_ok(v)) return false;
+  if (k->heads == 0 || q->heads % k->heads) return false;
+  return is_sm100();
+}
+
+size_t tc_bwd_workspace(const lvx_view* q, const lvx_view* k) {
+  if (q->rows == 0 || k->rows == 0) return 256;
+  const BwdPlan pl = plan_bwd(q, k);
+  const size_t lp = align256((size_t)q->heads * pl.rows_pad * 4);
+  return 2 * lp + align256((size_t)pl.splits * q->heads * q->rows * q->d * 4);
+}
+
+int tc_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
+           const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dq,
+           const lvx_view* dk, const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes,
+           cudaStream_t st) {
+  if (q->rows == 0 || k->rows == 0) return LVX_OK;
+  if (ws_bytes < tc_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  if (!tma_view_ok(dO) || !f32_rows_ok(dq) || !f32_rows_ok(dk) || !f32_rows_ok(dv))
+    return simt_bwd(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, st);
+  return q->d == 128 ? launch_bwd<128>(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, ws, st)
+                     : launch_bwd<64>(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, ws, st);
+}
+
+}  // namespace lvx

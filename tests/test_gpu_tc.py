@@ -116,3 +116,79 @@ def test_tc_forward_large_vs_torch_fp32():
     el = ((st.L - ref_l).abs().max() / ref_l.abs().max()).item()
     print(f"\nTC fwd C2-round: O err {eo:.2e}  L err {el:.2e}")
     assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
+BWD_SHAPES = [  # hq, hkv, sq, skv, d
+    (1, 1, 128, 128, 128), (2, 2, 200, 1000, 128), (8, 2, 77, 515, 64), (4, 1, 256, 2048, 128),
+    (3, 3, 5, 7, 128), (32, 8, 64, 640, 128), (2, 1, 300, 129, 64), (4, 4, 128, 3000, 64)]
+
+
+@pytest.mark.parametrize("shape", BWD_SHAPES)
+def test_tc_backward_vs_oracle(shape):
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import _lib
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(hq, hkv, sq, skv, d, seed=17 + sq)
+    O, L = orc.dense_attention(Q, K, V)
+    D = orc.attention_row_stats(O, G)
+    Lt = torch.from_numpy(L).float().cuda()
+    Dt = torch.from_numpy(D).float().cuda()
+    assert _lib.load().lvx_blockwise_bwd_workspace(_lib.view(q), _lib.view(k)) > 0
+    dq, dk, dv = lvx.blockwise_attention_backward(q, k, v, Lt, Dt, g)
+    rq, rk, rv = orc.blockwise_attention_backward(Q, K, V, L, D, G)
+    errs = [orc.max_norm_error(a.float().cpu().numpy(), b) for a, b in ((dq, rq), (dk, rk), (dv, rv))]
+    print(f"\nTC bwd {shape}: dQ {errs[0]:.2e} dK {errs[1]:.2e} dV {errs[2]:.2e}")
+    assert max(errs) <= TOL_BF16
+
+
+def test_tc_backward_accumulates():
+    from paper_2502_02406_b200 import kernels as Kn
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(4, 2, 130, 700, 128, seed=3)
+    O, L = orc.dense_attention(Q, K, V)
+    D = orc.attention_row_stats(O, G)
+    Lt, Dt = torch.from_numpy(L).float().cuda(), torch.from_numpy(D).float().cuda()
+    dq = torch.ones(q.shape, device="cuda")
+    dk = torch.ones(k.shape, device="cuda")
+    dv = torch.ones(v.shape, device="cuda")
+    Kn.bwd_accumulate(q, k, v, Lt, Dt, g, 1 / np.sqrt(128), dq, dk, dv, accumulate=True)
+    rq, rk, rv = orc.blockwise_attention_backward(Q, K, V, L, D, G)
+    for a, b in ((dq, rq), (dk, rk), (dv, rv)):
+        assert orc.max_norm_error(a.cpu().numpy() - 1.0, b) <= TOL_BF16
+
+
+def test_tc_lvx_fwd_bwd_single_gpu_vs_oracle():
+    """lvx_forward + lvx_backward (n=1 loopback schedule) on bf16 device tensors."""
+    import paper_2502_02406_b200 as lvx
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(8, 2, 192, 2500, 128, seed=21)
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(192, 2500, 1)
+    st, (dq, dk, dv), _, _ = lvx.run_rank("lvx", ctx, sh, q, k, v, g)
+    O, L = orc.dense_attention(Q, K, V)
+    rq, rk, rv = orc.dense_attention_backward(Q, K, V, O, L, G)
+    errs = {n: orc.max_norm_error(a.float().cpu().numpy(), b) for n, a, b in
+            (("O", st.O, O), ("L", st.L, L), ("dQ", dq, rq), ("dK", dk, rk), ("dV", dv, rv))}
+    print("\nlvx bf16 n=1 errors:", errs)
+    assert max(errs.values()) <= TOL_BF16
+
+
+def test_tc_backward_large_vs_torch_fp32():
+    """C2 per-round shape at 1/16 KV against torch fp32 autograd."""
+    import paper_2502_02406_b200 as lvx
+    torch.manual_seed(1)
+    hq, hkv, sq, skv, d = 32, 8, 256, 8192, 128
+    q = (torch.rand(hq, sq, d, device="cuda") * 2 - 1).bfloat16()
+    k = (torch.rand(hkv, skv, d, device="cuda") * 2 - 1).bfloat16()
+    v = (torch.rand(hkv, skv, d, device="cuda") * 2 - 1).bfloat16()
+    g = (torch.rand(hq, sq, d, device="cuda") * 2 - 1).bfloat16()
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    ke, ve = kf.repeat_interleave(hq // hkv, 0), vf.repeat_interleave(hq // hkv, 0)
+    s = (qf @ ke.transpose(1, 2)) / np.sqrt(d)
+    o = torch.softmax(s, -1) @ ve
+    o.backward(g.float())
+    L = torch.logsumexp(s, -1).detach()
+    D = (o.detach() * g.float()).sum(-1)
+    dq, dk, dv = lvx.blockwise_attention_backward(q, k, v, L, D, g)
+    errs = [((a.float() - b).abs().max() / b.abs().max()).item()
+            for a, b in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad))]
+    print(f"\nTC bwd C2-round/16: dQ {errs[0]:.2e} dK {errs[1]:.2e} dV {errs[2]:.2e}")
+    assert max(errs) <= TOL_BF16
