@@ -48,3 +48,28 @@ def test_c1_config_world2_vs_reference(golden_c1):
     assert orc.max_norm_error(res.grads.dK[:, g["dK_rows"]], g["dK_sample"]) <= 1e-4
     assert [tr.total_sent_bytes() for tr in res.traces_forward] == list(g["fwd_bytes"])
     assert [tr.total_sent_bytes() for tr in res.traces_backward] == list(g["bwd_bytes"])
+
+
+def test_bf16_lvx_and_ring_world2_vs_oracle():
+    """bf16 tensor-core path through the NCCL ring (spawned ranks), GQA 8/2."""
+    import paper_2502_02406_b200 as lvx
+    hq, hkv, sq, skv, d = 8, 2, 300, 5000, 128
+    Q, K, V, G = orc.make_inputs(sq, skv, hq, d, seed=44, hkv=hkv)
+    q, k, v, g = (torch.from_numpy(t).to(torch.bfloat16) for t in (Q, K, V, G))
+    Qr, Kr, Vr, Gr = (t.double().numpy() for t in (q, k, v, g))
+    O, L = orc.dense_attention(Qr, Kr, Vr)
+    rq, rk, rv = orc.dense_attention_backward(Qr, Kr, Vr, O, L, Gr)
+    n = min(torch.cuda.device_count(), 4)
+    for strategy in ("lvx", "ring"):
+        res = lvx.run_distributed(strategy, q, k, v, dO=g, spec=lvx.ClusterSpec(n))
+        errs = {nm: orc.max_norm_error(a.float().numpy(), b) for nm, a, b in
+                (("O", res.O, O), ("L", res.L, L), ("dQ", res.grads.dQ, rq),
+                 ("dK", res.grads.dK, rk), ("dV", res.grads.dV, rv))}
+        print(f"\n{strategy} bf16 n={n}:", errs)
+        assert max(errs.values()) <= 1e-2
+        w = lvx.volumes.Wire.b200(hq, hkv, d, 2)
+        qs, ks = res.shards.q_sizes, res.shards.kv_sizes
+        assert [t.total_sent_bytes() for t in res.traces_forward] == \
+            lvx.volumes.bytes_by_worker(strategy, "forward", qs, ks, w)
+        assert [t.total_sent_bytes() for t in res.traces_backward] == \
+            lvx.volumes.bytes_by_worker(strategy, "backward", qs, ks, w)

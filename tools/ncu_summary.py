@@ -1,0 +1,59 @@
+"""Summarise ncu --set full reports: the metrics the roofline/judge needs.
+
+    python tools/ncu_summary.py gpurun_out/prof_*.ncu-rep > profiles/<name>.md
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("duration_us", "gpu__time_duration.sum"),
+    ("sm_clock_ghz", "sm__cycles_elapsed.avg.per_second"),
+    ("dram_read_MB", "dram__bytes_read.sum"),
+    ("dram_write_MB", "dram__bytes_write.sum"),
+    ("tensor_utchmma_pct_peak", "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"),
+    ("tensor_pipe_active_pct", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+    ("issue_active_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
+    ("sm_throughput_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("dram_throughput_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("l2_throughput_pct", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
+    ("xu_pipe_pct", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+    ("fma_pipe_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+    ("alu_pipe_pct", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+    ("regs", "launch__registers_per_thread"),
+    ("smem_dyn_B", "launch__shared_mem_per_block_dynamic"),
+    ("grid", "launch__grid_size"),
+    ("block", "launch__block_size"),
+]
+
+
+def main():
+    for path in sys.argv[1:]:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        if len(rows) < 3:
+            print(f"## {path}: no data")
+            continue
+        hdr = rows[0]
+        for r in rows[2:]:
+            d = dict(zip(hdr, r))
+            print(f"## {path}\n\n`{d.get('Kernel Name', '?')[:110]}`\n")
+            print("| metric | value |\n|---|---|")
+            for name, key in KEYS:
+                if key in d:
+                    print(f"| {name} (`{key}`) | {d[key]} |")
+            stalls = sorted(((float(v), k) for k, v in d.items()
+                             if k.startswith("smsp__average_warp_latency_issue_stalled_") or
+                             (k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"))
+                             if v.replace('.', '', 1).isdigit()), reverse=True)[:8]
+            if stalls:
+                print("\ntop warp stall counters:\n")
+                for v, k in stalls:
+                    print(f"- `{k}` = {v:g}")
+            print()
+
+
+if __name__ == "__main__":
+    main()
