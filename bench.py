@@ -67,7 +67,7 @@ def peaks():
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -80,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -90,7 +90,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -103,7 +106,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "window", (0.0, float("inf")))
+        inside = [ln for ts, ln in self.lines if t0 - 0.05 <= ts <= t1 + 0.15]
+        if not inside:   # timed region shorter than one sample: nearest samples
+            inside = [ln for ts, ln in sorted(self.lines, key=lambda x: abs(x[0] - t1))[:3]]
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -225,6 +232,9 @@ def native_arm(args):
         return st, g
 
     def timed(c, steps, warm, strategy=None, sampler=False):
+        cs = ClockSampler(local) if sampler else None
+        if cs:
+            cs.__enter__()
         for _ in range(warm):
             step(c, strategy=strategy)
         torch.cuda.synchronize()
@@ -232,9 +242,7 @@ def native_arm(args):
             dist.barrier()
         traces = []
         launches0 = _lib.load().lvx_kernel_launches()
-        cs = ClockSampler(local) if sampler else None
-        if cs:
-            cs.__enter__()
+        w0 = time.time()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(steps):
@@ -242,6 +250,8 @@ def native_arm(args):
         e1.record()
         torch.cuda.synchronize()
         if cs:
+            cs.mark(w0, time.time())
+            time.sleep(0.15)
             cs.__exit__()
         if world > 1:
             dist.barrier()

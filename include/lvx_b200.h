@@ -129,6 +129,26 @@ int lvx_blockwise_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v,
                       const lvx_view* dv_acc, int accumulate,
                       void* workspace, size_t workspace_bytes, void* stream);
 
+/* The backward in its two independent halves, so the ring scheduler can
+ * compute dQ per round (it travels with the query block, strategies.py:
+ * 258-268) and dK/dV once over every query block that passed through
+ * (strategies.py:261-262 sums them over the rounds).
+ *   _dq_partial: dQ contribution of this (Q block, KV block) into `workspace`
+ *   _dq_finish:  dq_acc (+)= that contribution (after the travelling dQ has
+ *                arrived; same q/k shapes and workspace)
+ *   _dkv:        dk_acc / dv_acc (+)= contributions of every row of q.
+ * lvx_bwd_workspace(q, k) bytes serve any of the three for these shapes. */
+size_t lvx_bwd_workspace(const lvx_view* q, const lvx_view* k);
+int lvx_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                       const lvx_view* l, const lvx_view* dd, const lvx_view* d_o,
+                       double scale, void* workspace, size_t workspace_bytes, void* stream);
+int lvx_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq_acc,
+                      int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                const lvx_view* l, const lvx_view* dd, const lvx_view* d_o, double scale,
+                const lvx_view* dk_acc, const lvx_view* dv_acc, int accumulate,
+                void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- utilities ---------------------------------------------------------
  * empty_state (kernels.py:48-53): O = 0, L = -inf. */
 int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream);

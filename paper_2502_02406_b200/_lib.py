@@ -21,7 +21,8 @@ _DT = {torch.float32: LVX_F32, torch.float64: LVX_F64, torch.bfloat16: LVX_BF16}
 EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eligible", "lvx_blockwise_fwd_workspace",
            "lvx_blockwise_fwd", "lvx_fwd_partial", "lvx_fwd_finish", "lvx_merge_states",
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
-           "lvx_fill_empty_state", "lvx_convert")
+           "lvx_fill_empty_state", "lvx_convert", "lvx_bwd_workspace", "lvx_bwd_dq_partial",
+           "lvx_bwd_dq_finish", "lvx_bwd_dkv")
 
 
 class LvxView(ctypes.Structure):
@@ -65,6 +66,10 @@ def load() -> ctypes.CDLL:
         "lvx_blockwise_bwd_workspace": (sz, [P, P]),
         "lvx_blockwise_bwd": (i32, [P, P, P, P, P, P, dbl, P, P, P, i32, vp, sz, vp]),
         "lvx_fill_empty_state": (i32, [P, P, vp]),
+        "lvx_bwd_workspace": (sz, [P, P]),
+        "lvx_bwd_dq_partial": (i32, [P, P, P, P, P, P, dbl, vp, sz, vp]),
+        "lvx_bwd_dq_finish": (i32, [P, P, P, i32, vp, sz, vp]),
+        "lvx_bwd_dkv": (i32, [P, P, P, P, P, P, dbl, P, P, i32, vp, sz, vp]),
         "lvx_convert": (i32, [P, P, vp]),
     }
     for name, (res, args) in proto.items():

@@ -161,32 +161,107 @@ int lvx_row_stats(const lvx_view* o, const lvx_view* d_o, const lvx_view* dd, vo
   return row_stats(o, d_o, dd, static_cast<cudaStream_t>(stream));
 }
 
-size_t lvx_blockwise_bwd_workspace(const lvx_view* q, const lvx_view* k) {
+static size_t simt_bwd_ws(const lvx_view* q) {
+  const size_t e = q->dtype == LVX_F64 ? 8 : 4;
+  return ((size_t)q->heads * q->rows * q->d * e + 255) / 256 * 256 + 256;
+}
+
+static lvx_view simt_dq_view(const lvx_view* q, void* ws) {
+  return lvx_view{ws, q->heads, q->rows, q->d, q->rows * q->d, q->d, state_dtype(q->dtype), 0};
+}
+
+static bool use_tc_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                       const lvx_view* dO, const lvx_view* a, const lvx_view* b) {
+  return tc_bwd_eligible(q, k, v) && tc_bwd_outputs_ok(dO, a, b);
+}
+
+size_t lvx_bwd_workspace(const lvx_view* q, const lvx_view* k) {
   if (!q || !k) return 0;
-  return tc_bwd_eligible(q, k, k) ? tc_bwd_workspace(q, k) : 0;
+  return tc_bwd_eligible(q, k, k) ? tc_bwd_workspace(q, k) : simt_bwd_ws(q);
+}
+
+size_t lvx_blockwise_bwd_workspace(const lvx_view* q, const lvx_view* k) {
+  return lvx_bwd_workspace(q, k);
+}
+
+static int check_bwd_inputs(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                            const lvx_view* L, const lvx_view* D, const lvx_view* dO) {
+  int s = check_qkv(q, k, v);
+  if (s) return s;
+  if (!valid_view(L) || !valid_view(D) || !valid_view(dO)) return LVX_EINVAL;
+  const int sd = state_dtype(q->dtype);
+  if (dO->dtype != q->dtype || L->dtype != sd || D->dtype != sd) return LVX_EDTYPE;
+  if (!same_hr(dO, q) || dO->d != q->d || !same_hr(L, q) || !same_hr(D, q)) return LVX_EINVAL;
+  return LVX_OK;
+}
+
+static int check_acc(const lvx_view* a, const lvx_view* like, int sd) {
+  if (!valid_view(a)) return LVX_EINVAL;
+  if (a->dtype != sd) return LVX_EDTYPE;
+  if (!same_hr(a, like) || a->d != like->d) return LVX_EINVAL;
+  return LVX_OK;
+}
+
+int lvx_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                       const lvx_view* L, const lvx_view* D, const lvx_view* dO, double scale,
+                       void* ws, size_t ws_bytes, void* stream) {
+  int s = check_bwd_inputs(q, k, v, L, D, dO);
+  if (s) return s;
+  if (ws_bytes < lvx_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (q->heads * q->rows == 0) return LVX_OK;
+  // the tensor-core choice depends on (q, k) only, so _finish makes the same one
+  if (tc_bwd_eligible(q, k, v)) {
+    if (!tc_bwd_outputs_ok(dO, nullptr, nullptr)) return LVX_EINVAL;  // dO must align like q
+    return tc_bwd_dq_partial(q, k, v, L, D, dO, scale, ws, ws_bytes, st);
+  }
+  lvx_view w = simt_dq_view(q, ws);
+  if (k->rows == 0) return fill_empty_zero(&w, st);
+  return simt_bwd(q, k, v, L, D, dO, scale, &w, nullptr, nullptr, 0, st);
+}
+
+int lvx_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq, int accumulate,
+                      void* ws, size_t ws_bytes, void* stream) {
+  if (!valid_view(q) || !valid_view(k) || !dtype_ok(q->dtype)) return LVX_EINVAL;
+  int s = check_acc(dq, q, state_dtype(q->dtype));
+  if (s) return s;
+  if (ws_bytes < lvx_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (q->heads * q->rows == 0) return LVX_OK;
+  if (tc_bwd_eligible(q, k, k))
+    return tc_bwd_dq_finish(q, k, dq, accumulate, ws, ws_bytes, st);
+  lvx_view w = simt_dq_view(q, ws);
+  return accumulate_into(&w, dq, accumulate, st);
+}
+
+int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
+                const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dk,
+                const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  int s = check_bwd_inputs(q, k, v, L, D, dO);
+  if (s) return s;
+  const int sd = state_dtype(q->dtype);
+  if ((s = check_acc(dk, k, sd)) || (s = check_acc(dv, k, sd))) return s;
+  if (ws_bytes < lvx_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k->heads * k->rows == 0) return LVX_OK;
+  if (use_tc_bwd(q, k, v, dO, dk, dv))
+    return tc_bwd_dkv(q, k, v, L, D, dO, scale, dk, dv, accumulate, ws, ws_bytes, st);
+  if (q->heads * q->rows == 0) {
+    if (accumulate) return LVX_OK;
+    if ((s = fill_empty_zero(dk, st))) return s;
+    return fill_empty_zero(dv, st);
+  }
+  return simt_bwd(q, k, v, L, D, dO, scale, nullptr, dk, dv, accumulate, st);
 }
 
 int lvx_blockwise_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v,
                       const lvx_view* L, const lvx_view* D, const lvx_view* dO, double scale,
                       const lvx_view* dq, const lvx_view* dk, const lvx_view* dv,
                       int accumulate, void* ws, size_t ws_bytes, void* stream) {
-  int s = check_qkv(q, k, v);
+  int s = lvx_bwd_dkv(q, k, v, L, D, dO, scale, dk, dv, accumulate, ws, ws_bytes, stream);
   if (s) return s;
-  if (!valid_view(L) || !valid_view(D) || !valid_view(dO) || !valid_view(dq) ||
-      !valid_view(dk) || !valid_view(dv))
-    return LVX_EINVAL;
-  const int sd = state_dtype(q->dtype);
-  if (dO->dtype != q->dtype || L->dtype != sd || D->dtype != sd || dq->dtype != sd ||
-      dk->dtype != sd || dv->dtype != sd)
-    return LVX_EDTYPE;
-  if (!same_hr(dO, q) || dO->d != q->d || !same_hr(L, q) || !same_hr(D, q) ||
-      !same_hr(dq, q) || dq->d != q->d || !same_hr(dk, k) || dk->d != k->d ||
-      !same_hr(dv, k) || dv->d != k->d)
-    return LVX_EINVAL;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (tc_bwd_eligible(q, k, v))
-    return tc_bwd(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, ws, ws_bytes, st);
-  return simt_bwd(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, st);
+  if ((s = lvx_bwd_dq_partial(q, k, v, L, D, dO, scale, ws, ws_bytes, stream))) return s;
+  return lvx_bwd_dq_finish(q, k, dq, accumulate, ws, ws_bytes, stream);
 }
 
 int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream) {

@@ -511,6 +511,21 @@ __global__ void dq_combine_kernel(const float* __restrict__ ws, int splits, int 
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+__global__ void zero_kernel(View3<float> A) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= A.heads * A.rows * A.d) return;
+  const int64_t c = idx % A.d, r = (idx / A.d) % A.rows, h = idx / (A.d * A.rows);
+  A.at(h, r)[c] = 0.f;
+}
+
+int fill_zero_f32(const lvx_view* v, cudaStream_t st) {
+  const int64_t total = v->heads * v->rows * v->d;
+  if (!total) return LVX_OK;
+  zero_kernel<<<ceil_div(total, 256), 256, 0, st>>>(make_view<float>(v));
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
 struct BwdPlan {
   int tq64, tpq, pairs, rows_pad, n_tiles, tiles_per_split, splits;
 };
@@ -551,12 +566,8 @@ bool f32_rows_ok(const lvx_view* v) {
          v->row_stride % 4 == 0 && (v->heads <= 1 || v->head_stride % 4 == 0);
 }
 
-template <int D>
-int launch_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
-               const lvx_view* Dv, const lvx_view* dO, double scale, const lvx_view* dq,
-               const lvx_view* dk, const lvx_view* dvv, int accumulate, void* ws, cudaStream_t st) {
-  const BwdPlan pl = plan_bwd(q, k);
-  BwdParams p{};
+void fill_params(BwdParams& p, const BwdPlan& pl, const lvx_view* q, const lvx_view* k,
+                 double scale, void* ws) {
   p.hq = (int)q->heads;
   p.hkv = (int)k->heads;
   p.G = p.hq / p.hkv;
@@ -572,11 +583,38 @@ int launch_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.scale_log2 = (float)(scale * 1.4426950408889634);
   char* w = static_cast<char*>(ws);
   const size_t lp_bytes = align256((size_t)p.hq * p.rows_pad * 4);
-  float* Lp = reinterpret_cast<float*>(w);
-  float* Dp = reinterpret_cast<float*>(w + lp_bytes);
-  p.Lp = Lp;
-  p.Dp = Dp;
+  p.Lp = reinterpret_cast<float*>(w);
+  p.Dp = reinterpret_cast<float*>(w + lp_bytes);
   p.ws_dq = reinterpret_cast<float*>(w + 2 * lp_bytes);
+}
+
+int launch_prep(const BwdParams& p, const lvx_view* L, const lvx_view* Dv, cudaStream_t st) {
+  const int64_t total = (int64_t)p.hq * p.rows_pad;
+  bwd_prep_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+      View3<const float>{static_cast<const float*>(L->data), L->heads, L->rows, 1, L->head_stride,
+                         L->row_stride},
+      View3<const float>{static_cast<const float*>(Dv->data), Dv->heads, Dv->rows, 1,
+                         Dv->head_stride, Dv->row_stride},
+      p.hq, p.rows_q, p.rows_pad, const_cast<float*>(p.Lp), const_cast<float*>(p.Dp));
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+template <int D>
+int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
+               BwdParams p, const lvx_view* dk, const lvx_view* dvv, int accumulate,
+               cudaStream_t st) {
+  CUtensorMap mq64, mg64, mk128, mv128;
+  if (!make_tma_3d(&mq64, q, kStep) || !make_tma_3d(&mg64, dO, kStep) ||
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
+    return LVX_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DkvCfg<D>::SMEM) != cudaSuccess)
+      return LVX_ECUDA;
+    attr = true;
+  }
   p.dk = static_cast<float*>(dk->data);
   p.dv = static_cast<float*>(dvv->data);
   p.dk_hs = dk->head_stride;
@@ -584,41 +622,28 @@ int launch_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.dv_hs = dvv->head_stride;
   p.dv_rs = dvv->row_stride;
   p.accumulate = accumulate;
+  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 192,
+                      DkvCfg<D>::SMEM, st>>>(mq64, mk128, mv128, mg64, p);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
 
-  {
-    const int64_t total = (int64_t)p.hq * p.rows_pad;
-    bwd_prep_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
-        View3<const float>{static_cast<const float*>(L->data), L->heads, L->rows, 1,
-                           L->head_stride, L->row_stride},
-        View3<const float>{static_cast<const float*>(Dv->data), Dv->heads, Dv->rows, 1,
-                           Dv->head_stride, Dv->row_stride},
-        p.hq, p.rows_q, p.rows_pad, Lp, Dp);
-    note_launch();
-  }
-  CUtensorMap mq64, mg64, mq128, mg128, mk128, mv128, mk64, mv64;
-  if (!make_tma_3d(&mq64, q, kStep) || !make_tma_3d(&mg64, dO, kStep) ||
-      !make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
-      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128) ||
+template <int D>
+int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
+              const BwdParams& p, const BwdPlan& pl, cudaStream_t st) {
+  CUtensorMap mq128, mg128, mk64, mv64;
+  if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
       !make_tma_3d(&mk64, k, kStep) || !make_tma_3d(&mv64, v, kStep))
     return LVX_ECUDA;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DkvCfg<D>::SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              DqCfg<D>::SMEM) != cudaSuccess)
       return LVX_ECUDA;
     attr = true;
   }
-  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 192,
-                      DkvCfg<D>::SMEM, st>>>(mq64, mk128, mv128, mg64, p);
-  note_launch();
   bwd_dq_kernel<D><<<dim3(pl.pairs, pl.splits, (unsigned)k->heads), 320, DqCfg<D>::SMEM, st>>>(
       mq128, mk64, mv64, mg128, p);
-  note_launch();
-  const int64_t rows_total = (int64_t)p.hq * p.rows_q;
-  dq_combine_kernel<D><<<ceil_div(rows_total * 32, 256), 256, 0, st>>>(
-      p.ws_dq, p.splits, p.hq, p.rows_q, make_view<float>(dq), accumulate);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
@@ -633,6 +658,10 @@ bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
   return is_sm100();
 }
 
+bool tc_bwd_outputs_ok(const lvx_view* dO, const lvx_view* a, const lvx_view* b) {
+  return tma_view_ok(dO) && (!a || f32_rows_ok(a)) && (!b || f32_rows_ok(b));
+}
+
 size_t tc_bwd_workspace(const lvx_view* q, const lvx_view* k) {
   if (q->rows == 0 || k->rows == 0) return 256;
   const BwdPlan pl = plan_bwd(q, k);
@@ -640,16 +669,58 @@ size_t tc_bwd_workspace(const lvx_view* q, const lvx_view* k) {
   return 2 * lp + align256((size_t)pl.splits * q->heads * q->rows * q->d * 4);
 }
 
-int tc_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
-           const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dq,
-           const lvx_view* dk, const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes,
-           cudaStream_t st) {
+int tc_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                      const lvx_view* L, const lvx_view* D, const lvx_view* dO, double scale,
+                      void* ws, size_t ws_bytes, cudaStream_t st) {
   if (q->rows == 0 || k->rows == 0) return LVX_OK;
   if (ws_bytes < tc_bwd_workspace(q, k)) return LVX_EWORKSPACE;
-  if (!tma_view_ok(dO) || !f32_rows_ok(dq) || !f32_rows_ok(dk) || !f32_rows_ok(dv))
-    return simt_bwd(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, st);
-  return q->d == 128 ? launch_bwd<128>(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, ws, st)
-                     : launch_bwd<64>(q, k, v, L, D, dO, scale, dq, dk, dv, accumulate, ws, st);
+  const BwdPlan pl = plan_bwd(q, k);
+  BwdParams p{};
+  fill_params(p, pl, q, k, scale, ws);
+  int s = launch_prep(p, L, D, st);
+  if (s) return s;
+  return q->d == 128 ? launch_dq<128>(q, k, v, dO, p, pl, st) : launch_dq<64>(q, k, v, dO, p, pl, st);
+}
+
+int tc_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq, int accumulate,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (q->rows == 0) return LVX_OK;
+  if (ws_bytes < tc_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  const BwdPlan pl = plan_bwd(q, k);
+  BwdParams p{};
+  fill_params(p, pl, q, k, 1.0, ws);
+  const int64_t rows_total = (int64_t)p.hq * p.rows_q;
+  if (k->rows == 0) {   // no contribution: dq (+)= 0
+    if (accumulate) return LVX_OK;
+    return fill_zero_f32(dq, st);
+  }
+  if (q->d == 128)
+    dq_combine_kernel<128><<<ceil_div(rows_total * 32, 256), 256, 0, st>>>(
+        p.ws_dq, p.splits, p.hq, p.rows_q, make_view<float>(dq), accumulate);
+  else
+    dq_combine_kernel<64><<<ceil_div(rows_total * 32, 256), 256, 0, st>>>(
+        p.ws_dq, p.splits, p.hq, p.rows_q, make_view<float>(dq), accumulate);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
+               const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dk,
+               const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (k->rows == 0) return LVX_OK;
+  if (q->rows == 0) {
+    if (accumulate) return LVX_OK;
+    int s = fill_zero_f32(dk, st);
+    return s ? s : fill_zero_f32(dv, st);
+  }
+  if (ws_bytes < tc_bwd_workspace(q, k)) return LVX_EWORKSPACE;
+  const BwdPlan pl = plan_bwd(q, k);
+  BwdParams p{};
+  fill_params(p, pl, q, k, scale, ws);
+  int s = launch_prep(p, L, D, st);
+  if (s) return s;
+  return q->d == 128 ? launch_dkv<128>(q, k, v, dO, p, dk, dv, accumulate, st)
+                     : launch_dkv<64>(q, k, v, dO, p, dk, dv, accumulate, st);
 }
 
 }  // namespace lvx

@@ -90,9 +90,14 @@ void note_launch(int n = 1);
 int simt_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double scale,
              const lvx_view* prior_o, const lvx_view* prior_l, const lvx_view* o,
              const lvx_view* l, cudaStream_t st);
+// dq / dk+dv halves are selected by non-null outputs
 int simt_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
              const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dq,
              const lvx_view* dk, const lvx_view* dv, int accumulate, cudaStream_t st);
+// zero an F32/F64 view
+int fill_empty_zero(const lvx_view* a, cudaStream_t st);
+// dst (+)= src, state dtypes, same shapes
+int accumulate_into(const lvx_view* src, const lvx_view* dst, int accumulate, cudaStream_t st);
 int merge(const lvx_view* oa, const lvx_view* la, const lvx_view* ob, const lvx_view* lb,
           const lvx_view* o, const lvx_view* l, cudaStream_t st);
 int row_stats(const lvx_view* o, const lvx_view* dO, const lvx_view* D, cudaStream_t st);
@@ -108,9 +113,14 @@ int tc_fwd_finish(const lvx_view* q, const lvx_view* k, const lvx_view* prior_o,
                   const lvx_view* prior_l, const lvx_view* o, const lvx_view* l, void* ws,
                   size_t ws_bytes, cudaStream_t st);
 bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v);
+bool tc_bwd_outputs_ok(const lvx_view* dO, const lvx_view* a, const lvx_view* b);
 size_t tc_bwd_workspace(const lvx_view* q, const lvx_view* k);
-int tc_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
-           const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dq,
-           const lvx_view* dk, const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes,
-           cudaStream_t st);
+int tc_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
+                      const lvx_view* L, const lvx_view* D, const lvx_view* dO, double scale,
+                      void* ws, size_t ws_bytes, cudaStream_t st);
+int tc_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq, int accumulate,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
+int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
+               const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dk,
+               const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
 }  // namespace lvx

@@ -343,7 +343,7 @@ template <typename Tin, typename Ts, typename Acc, int DPL>
 int bwd_launch(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
                const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dq,
                const lvx_view* dk, const lvx_view* dv, int acc, cudaStream_t st) {
-  const int64_t wq = q->heads * q->rows, wk = k->heads * k->rows;
+  const int64_t wq = dq ? q->heads * q->rows : 0, wk = dk ? k->heads * k->rows : 0;
   if (wq) {
     simt_bwd_dq_kernel<Tin, Ts, Acc, DPL><<<ceil_div(wq, kWarps), kWarps * 32, 0, st>>>(
         cview<Tin>(q), cview<Tin>(k), cview<Tin>(v), cview<Ts>(L), cview<Ts>(D),
@@ -482,6 +482,52 @@ static int convert_to(const lvx_view* a, const lvx_view* b, cudaStream_t st) {
     default:
       return LVX_EDTYPE;
   }
+  return launch_status();
+}
+
+template <typename Ts>
+__global__ void accum_kernel(View3<const Ts> A, View3<Ts> B, bool acc) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = A.heads * A.rows * A.d;
+  if (idx >= total) return;
+  const int64_t c = idx % A.d, r = (idx / A.d) % A.rows, h = idx / (A.d * A.rows);
+  Ts* o = B.at(h, r) + c;
+  *o = acc ? *o + A.at(h, r)[c] : A.at(h, r)[c];
+}
+
+template <typename Ts>
+__global__ void zero_state_kernel(View3<Ts> A) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= A.heads * A.rows * A.d) return;
+  const int64_t c = idx % A.d, r = (idx / A.d) % A.rows, h = idx / (A.d * A.rows);
+  A.at(h, r)[c] = Ts(0);
+}
+
+int fill_empty_zero(const lvx_view* a, cudaStream_t st) {
+  const int64_t total = a->heads * a->rows * a->d;
+  if (!total) return LVX_OK;
+  const int threads = 256;
+  if (a->dtype == LVX_F32)
+    zero_state_kernel<float><<<ceil_div(total, threads), threads, 0, st>>>(make_view<float>(a));
+  else if (a->dtype == LVX_F64)
+    zero_state_kernel<double><<<ceil_div(total, threads), threads, 0, st>>>(make_view<double>(a));
+  else
+    return LVX_EDTYPE;
+  return launch_status();
+}
+
+int accumulate_into(const lvx_view* a, const lvx_view* b, int acc, cudaStream_t st) {
+  const int64_t total = a->heads * a->rows * a->d;
+  if (!total) return LVX_OK;
+  const int threads = 256;
+  if (a->dtype == LVX_F32 && b->dtype == LVX_F32)
+    accum_kernel<float><<<ceil_div(total, threads), threads, 0, st>>>(cview<float>(a),
+                                                                     make_view<float>(b), acc != 0);
+  else if (a->dtype == LVX_F64 && b->dtype == LVX_F64)
+    accum_kernel<double><<<ceil_div(total, threads), threads, 0, st>>>(
+        cview<double>(a), make_view<double>(b), acc != 0);
+  else
+    return LVX_EDTYPE;
   return launch_status();
 }
 

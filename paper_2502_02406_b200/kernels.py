@@ -278,6 +278,35 @@ def bwd_accumulate(q, k, v, L, D, d_o, scale: float, dq, dk, dv, accumulate: boo
         ws.data_ptr(), ws.numel(), _lib.stream_ptr(q.device)))
 
 
+def bwd_dq_partial(q, k, v, L, D, d_o, scale: float, ws: torch.Tensor) -> None:
+    """dQ contribution of (q block, this KV block) into ``ws``."""
+    _lib.check("lvx_bwd_dq_partial", _lib.load().lvx_bwd_dq_partial(
+        _lib.view(q), _lib.view(k), _lib.view(v), _lib.view(L), _lib.view(D), _lib.view(d_o),
+        float(scale), ws.data_ptr(), ws.numel(), _lib.stream_ptr(q.device)))
+
+
+def bwd_dq_finish(q, k, ws: torch.Tensor, dq, accumulate: bool = True) -> None:
+    """dq (+)= the contribution held in ``ws``."""
+    _lib.check("lvx_bwd_dq_finish", _lib.load().lvx_bwd_dq_finish(
+        _lib.view(q), _lib.view(k), _lib.view(dq), int(bool(accumulate)), ws.data_ptr(),
+        ws.numel(), _lib.stream_ptr(q.device)))
+
+
+def bwd_dkv(q, k, v, L, D, d_o, scale: float, dk, dv, accumulate: bool = True,
+            ws: torch.Tensor | None = None) -> None:
+    """dk/dv (+)= contributions of every query row in q."""
+    if ws is None:
+        ws = workspace(bwd_ws_bytes(q, k), q.device, slot=2)
+    _lib.check("lvx_bwd_dkv", _lib.load().lvx_bwd_dkv(
+        _lib.view(q), _lib.view(k), _lib.view(v), _lib.view(L), _lib.view(D), _lib.view(d_o),
+        float(scale), _lib.view(dk), _lib.view(dv), int(bool(accumulate)), ws.data_ptr(),
+        ws.numel(), _lib.stream_ptr(q.device)))
+
+
+def bwd_ws_bytes(q, k) -> int:
+    return int(_lib.load().lvx_bwd_workspace(_lib.view(q), _lib.view(k)))
+
+
 def blockwise_attention_backward(Q_block, K_block, V_block, L_full, D_full, dO_block,
                                  scale: float | None = None):
     """Additive (dQ+, dK+, dV+) of one (Q block, KV block) pair given the final

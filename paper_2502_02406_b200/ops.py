@@ -45,6 +45,23 @@ class CudaOps:
         if q.numel() and k.shape[1]:
             K.bwd_accumulate(q, k, v, L, D, d_o, scale, dq, dk, dv, accumulate=True)
 
+    # split backward used by the LV-XAttn ring (dQ travels, dK/dV once)
+    def bwd_workspace(self, q, k, slot: int = 1) -> torch.Tensor:
+        return K.workspace(K.bwd_ws_bytes(q, k), q.device, slot=slot)
+
+    def bwd_dq_partial(self, q, k, v, L, D, d_o, scale, ws) -> None:
+        if q.numel():
+            K.bwd_dq_partial(q, k, v, L, D, d_o, scale, ws)
+
+    def bwd_dq_finish(self, q, k, ws, dq, accumulate: bool) -> None:
+        if q.numel():
+            K.bwd_dq_finish(q, k, ws, dq, accumulate)
+
+    def bwd_dkv(self, q, k, v, L, D, d_o, scale, dk, dv, accumulate: bool) -> None:
+        if k.numel():
+            K.bwd_dkv(q, k, v, L, D, d_o, scale, dk, dv, accumulate,
+                      ws=self.bwd_workspace(q, k, slot=2))
+
     # -- device timing (CUDA events on the compute stream) -----------------
     @staticmethod
     def event():

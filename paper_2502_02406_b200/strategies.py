@@ -258,21 +258,40 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
                  state: AttentionState, do_block, scale: float,
                  trace: RoundTrace | None = None):
     """Query-rotation backward (strategies.py:234-276): the tuple
-    (Q, dO, L, D, dQ) of each block travels once around the ring; every rank
-    adds its K/V block's contribution, accumulating dK/dV locally and dQ
-    into the tuple.  The round n-1 send is the homecoming.
-    Returns (dQ_i, dK_i, dV_i) in the state dtype."""
+    (Q, dO, L, D, dQ) of every block travels once around the ring and every
+    rank adds its K/V block's contribution; the last dQ hop is the
+    homecoming.  Returns (dQ_i, dK_i, dV_i) in the state dtype.
+
+    B200 schedule (same messages and bytes per rank as the reference; see
+    DESIGN.md §5):
+      * the immutable part (Q, dO, L, D) of block j is sent at the START of
+        round r, overlapping this round's dQ kernel, instead of after it;
+      * dQ lags one hop: round r sends the dQ of block j+1 finished in round
+        r-1, and the received dQ of block j is folded in by the dQ finish
+        kernel after the local contribution is computed;
+      * every block's (Q, dO, L, D) passes through every rank anyway, so dK_i
+        and dV_i (the sum over rounds at strategies.py:261-262) are computed
+        ONCE after the ring over all gathered query rows — one tensor-core
+        pass with dK/dV in TMEM and a single write, instead of n passes with
+        an fp32 read-modify-write each.
+    """
     n, i, ops = ctx.n, ctx.rank, ctx.ops
     h, _, d = q_block.shape
     dev = q_block.device
     sd = ops.state_dtype(q_block.dtype)
-    qs = shards.q_sizes
+    qs, qr = shards.q_sizes, shards.q_ranges
     mq = max(qs) if qs else 0
     Qb = _Flat(h, mq, d, q_block.dtype, dev)
     Gb = _Flat(h, mq, d, q_block.dtype, dev)
     Lb = _Flat(h, mq, None, sd, dev)
     Db = _Flat(h, mq, None, sd, dev)
     dQb = _Flat(h, mq, d, sd, dev)
+    if n > 1:   # gather of every block's immutable rows for the batched dK/dV
+        s_tot = sum(qs)
+        Qg = torch.empty((h, s_tot, d), dtype=q_block.dtype, device=dev)
+        Gg = torch.empty((h, s_tot, d), dtype=q_block.dtype, device=dev)
+        Lg = torch.empty((h, s_tot), dtype=sd, device=dev)
+        Dg = torch.empty((h, s_tot), dtype=sd, device=dev)
 
     cur = 0
     q_j = _dev_copy(q_block, Qb.view(cur, qs[i]))
@@ -280,31 +299,64 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     l_j = _dev_copy(state.L, Lb.view(cur, qs[i]))
     d_j = Db.view(cur, qs[i])
     ops.row_stats(state.O, do_block, d_j)             # strategies.py:247
-    dq_j = dQb.view(cur, qs[i])
-    dq_j.zero_()
-    dk = torch.zeros(k_block.shape, dtype=sd, device=dev)
-    dv = torch.zeros(v_block.shape, dtype=sd, device=dev)
+    dq_prev = None
     blk = i
     for r in range(n):
-        j = (i - r) % n
+        j, nxt = (i - r) % n, (i - r - 1) % n
         _expect(blk, j, f"worker {i} backward round {r}")
-        t0 = ops.event() if trace is not None else None
-        ops.bwd_accumulate(q_j, k_block, v_block, l_j, d_j, do_j, scale, dq_j, dk, dv)
-        t1 = ops.event() if trace is not None else None
-        nxt = (i - r - 1) % n
-        recv = [Qb.view(1 - cur, qs[nxt]), Gb.view(1 - cur, qs[nxt]), Lb.view(1 - cur, qs[nxt]),
-                Db.view(1 - cur, qs[nxt]), dQb.view(1 - cur, qs[nxt])]
+        send = [q_j, do_j, l_j, d_j]
+        recv = [Qb.view(1 - cur, qs[nxt]), Gb.view(1 - cur, qs[nxt]),
+                Lb.view(1 - cur, qs[nxt]), Db.view(1 - cur, qs[nxt])]
+        classes = ["Q", "dO", "L", "D"]
+        dq_in = None
+        if r >= 1:   # dQ of block j+1 (finished last round) out, dQ of block j in
+            dq_in = dQb.view(r % 2, qs[j])
+            send.append(dq_prev)
+            recv.append(dq_in)
+            classes.append("dQ")
         if n == 1:
-            recv = [q_j, do_j, l_j, d_j, dq_j]
-        hop, sent = ctx.shift([q_j, do_j, l_j, d_j, dq_j], recv, ["Q", "dO", "L", "D", "dQ"])
+            recv = send
+        t0 = ops.event() if trace is not None else None
+        hop, sent = ctx.shift(send, recv, classes)
+        ws = ops.bwd_workspace(q_j, k_block)
+        ops.bwd_dq_partial(q_j, k_block, v_block, l_j, d_j, do_j, scale, ws)
+        t1 = ops.event() if trace is not None else None
+        if n > 1:
+            a, b = qr[j]
+            Qg[:, a:b].copy_(q_j)
+            Gg[:, a:b].copy_(do_j)
+            Lg[:, a:b].copy_(l_j)
+            Dg[:, a:b].copy_(d_j)
+        else:
+            Qg, Gg, Lg, Dg = q_j, do_j, l_j, d_j
         hop.wait()
         t2 = ops.event() if trace is not None else None
+        if dq_in is None:
+            dq_acc = dQb.view(0, qs[j])
+            ops.bwd_dq_finish(q_j, k_block, ws, dq_acc, accumulate=False)
+        else:
+            ops.bwd_dq_finish(q_j, k_block, ws, dq_in, accumulate=True)
+            dq_acc = dq_in
         if trace is not None:
             trace._add_timed(ops, t0, t1, t2, sent)
-        q_j, do_j, l_j, d_j, dq_j = recv
+        dq_prev = dq_acc
+        if n > 1:
+            q_j, do_j, l_j, d_j = recv[:4]
         blk, cur = nxt, 1 - cur
     _expect(blk, i, f"worker {i} backward homecoming")
-    return dq_j.clone(), dk, dv
+    # the dQ of block i+1 goes home; this rank's own dQ_i arrives
+    dq_out = torch.empty((h, qs[i], d), dtype=sd, device=dev)
+    if n == 1:
+        dq_out.copy_(dq_prev)
+    else:
+        hop, epi = ctx.shift([dq_prev], [dq_out], ["dQ"])
+        hop.wait()
+        if trace is not None:
+            trace.epilogue_bytes_by_class = epi
+    dk = torch.empty(k_block.shape, dtype=sd, device=dev)
+    dv = torch.empty(v_block.shape, dtype=sd, device=dev)
+    ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
+    return dq_out, dk, dv
 
 
 # ---------------------------------------------------------------------------

@@ -67,6 +67,43 @@ class OracleOps:
         dk += torch.from_numpy(gk).to(dk.dtype)
         dv += torch.from_numpy(gv).to(dv.dtype)
 
+    def bwd_workspace(self, q, k, slot=1):
+        return {}
+
+    def bwd_dq_partial(self, q, k, v, L, D, d_o, scale, ws):
+        if q.numel() and k.shape[1]:
+            gq, _, _ = orc.blockwise_attention_backward(_np(q), _np(k), _np(v), _np(L), _np(D),
+                                                        _np(d_o), scale)
+            ws["dq"] = gq
+        else:
+            ws["dq"] = np.zeros(tuple(q.shape))
+
+    def bwd_dq_finish(self, q, k, ws, dq, accumulate):
+        if not q.numel():
+            return
+        g = torch.from_numpy(np.asarray(ws.pop("dq"))).to(dq.dtype)
+        if accumulate:
+            dq += g
+        else:
+            dq.copy_(g)
+
+    def bwd_dkv(self, q, k, v, L, D, d_o, scale, dk, dv, accumulate):
+        if not k.numel():
+            return
+        if q.numel():
+            _, gk, gv = orc.blockwise_attention_backward(_np(q), _np(k), _np(v), _np(L),
+                                                         _np(D), _np(d_o), scale)
+        else:
+            gk, gv = np.zeros(tuple(k.shape)), np.zeros(tuple(v.shape))
+        gk = torch.from_numpy(gk).to(dk.dtype)
+        gv = torch.from_numpy(gv).to(dv.dtype)
+        if accumulate:
+            dk += gk
+            dv += gv
+        else:
+            dk.copy_(gk)
+            dv.copy_(gv)
+
     @staticmethod
     def event():
         return time.perf_counter()
