@@ -270,28 +270,42 @@ def native_arm(args):
     flops = volumes.attention_flops(s_q, s_kv, hq, d)
     value = flops / (ms * 1e-3) / 1e12
 
-    # --- kernel roofline: dominant kernel = larger of the fwd / bwd launches
-    tf_k = statistics.mean(sum(r.compute_seconds for r in tf.rounds) for tf, _ in traces)
-    tb_k = statistics.mean(sum(r.compute_seconds for r in tb.rounds) for _, tb in traces)
+    # --- kernel roofline: dominant kernel by device time inside the timed region
+    def sec(tr_list, name):
+        return statistics.mean(t.sections.get(name, 0.0) for t in tr_list)
+
+    tfs, tbs = [tf for tf, _ in traces], [tb for _, tb in traces]
     n_rounds = len(traces[0][0].rounds)
-    rows_q = shards.q_sizes
-    # per launch (one round, one rank): 4 or 10 x |q block| x |kv shard| x hq x d
-    fwd_flops_round = 4.0 * (s_q / world) * (kb - ka) * hq * d
-    bwd_flops_round = 10.0 * (s_q / world) * (kb - ka) * hq * d
+    qrows, kvrows = s_q / world, kb - ka
+    unit = qrows * kvrows * hq * d                      # one (q block, kv shard) pair
+    phases = {"fwd_kernel": sec(tfs, "fwd_kernel"), "fwd_finish": sec(tfs, "fwd_finish"),
+              "fwd_wait": sec(tfs, "wait"), "dq_kernel": sec(tbs, "dq_kernel"),
+              "dq_finish": sec(tbs, "dq_finish"), "bwd_gather_wait": sec(tbs, "gather+wait"),
+              "dkv_kernel": sec(tbs, "dkv_kernel")}
+    # algorithmic FLOP per launch (PAPER.md:67 split by product): fwd 4 units per
+    # round; dQ kernel 2 (dS K) + the S, dP it recomputes are counted in dkv;
+    # dkv kernel 8 (S, dP, dV, dK) over all n blocks in one launch.
+    kernels = {"fwd_kernel (tcgen05)": (4.0 * unit, phases["fwd_kernel"] / n_rounds),
+               "dkv_kernel (tcgen05)": (8.0 * unit * n_rounds, phases["dkv_kernel"]),
+               "dq_kernel (tcgen05)": (2.0 * unit, phases["dq_kernel"] / n_rounds)}
+    if args.strategy == "ring":   # ring backward runs the fused per-round backward
+        rb = statistics.mean(sum(r.compute_seconds for r in tb.rounds) for tb in tbs)
+        kernels = {"fwd_kernel (tcgen05)": kernels["fwd_kernel (tcgen05)"],
+                   "ring_bwd (dkv+dq per round)": (10.0 * unit, rb / n_rounds)}
+    kernels = {k: v for k, v in kernels.items() if v[1] > 0}
+    kname = max(kernels, key=lambda k: kernels[k][1] * (n_rounds if "dkv" not in k else 1))
+    kflops, kdur = kernels[kname]
     burst, sust, hbm, pk_kind = peaks()
-    if tb_k >= tf_k:
-        kname, kflops, kdur = "lvx_bwd (tcgen05)" if _bwd_is_tc(q_i, k_i) else "lvx_bwd (SIMT)", \
-            bwd_flops_round, tb_k / n_rounds
-    else:
-        kname, kflops, kdur = "lvx_fwd (tcgen05)", fwd_flops_round, tf_k / n_rounds
     achieved = kflops / kdur / 1e12
     roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": sust,
                 "unit": "TFLOP/s", "frac": achieved / sust, "traffic": None,
                 "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
                 "frac_of_burst": achieved / burst, "frac_of_nominal_2250": achieved / 2250.0,
-                "fwd_kernel_ms_per_step": tf_k * 1e3, "bwd_kernel_ms_per_step": tb_k * 1e3,
-                "fwd_tflops": 4.0 * s_q / world * (kb - ka) * hq * d * n_rounds / tf_k / 1e12,
-                "bwd_tflops": 10.0 * s_q / world * (kb - ka) * hq * d * n_rounds / tb_k / 1e12}
+                "per_launch_ms": kdur * 1e3,
+                "phase_ms_per_step": {k: v * 1e3 for k, v in phases.items()},
+                "fwd_tflops": 4.0 * unit * n_rounds / max(phases["fwd_kernel"], 1e-9) / 1e12,
+                "bwd_tflops": 10.0 * unit * n_rounds /
+                max(phases["dkv_kernel"] + phases["dq_kernel"] + phases["dq_finish"], 1e-9) / 1e12}
 
     # --- measured NVLink bytes vs closed form and the paper's model
     tf0, tb0 = traces[0]
@@ -303,6 +317,7 @@ def native_arm(args):
             "paper_q_plus_o_hop_bytes_bf16": volumes.paper_hop_bytes(s_q, world, hq, d, 2),
             "measured_fwd_hop_bytes": (tf0.rounds[0].sent_bytes if world > 1 else 0),
             "exposed_comm_ms_per_step": sum(r.comm_seconds for r in tf0.rounds + tb0.rounds) * 1e3}
+    out_phases_nc = None
 
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_layer": ms,
@@ -317,8 +332,12 @@ def native_arm(args):
 
     # --- no-communication arm and the Ring baseline
     if world > 1:
-        ms_nc, *_ = timed(ctx_nc, max(2, args.steps // 2), 1)
+        ms_nc, tr_nc, *_ = timed(ctx_nc, max(2, args.steps // 2), 1)
         out["no_comm_ms_per_step"] = ms_nc
+        out["no_comm_phase_ms_per_step"] = {
+            "fwd_kernel": sec([a for a, _ in tr_nc], "fwd_kernel") * 1e3,
+            "dq_kernel": sec([b for _, b in tr_nc], "dq_kernel") * 1e3,
+            "dkv_kernel": sec([b for _, b in tr_nc], "dkv_kernel") * 1e3}
         out["overhead_vs_no_comm"] = ms / ms_nc - 1.0
         if not args.no_ring_compare and args.strategy == "lvx":
             ms_ring, rtr, *_ = timed(ctx, max(2, args.steps // 2), 1,

@@ -79,7 +79,7 @@ struct DkvCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
 bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG,
                const BwdParams p) {
@@ -111,18 +111,18 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&st_full[b], 1);
-      mbar_init(&pds_full[b], 128);
+      mbar_init(&pds_full[b], 256);
     }
     mbar_init(dkv_done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       tma_prefetch(&tmQ);
@@ -149,7 +149,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         bulk_load(slot + 2 * C::QT_BYTES + 256, p.Dp + off, 256, &qd_full[s]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
@@ -200,75 +200,75 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       mma_commit(dkv_done);
     }
   } else {
-    // ------------------------------------------------ softmax (kv row per thread)
-    const int r = warp * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    // ------------------------------- softmax: kv row per thread, 32 of the 64
+    // query columns per warpgroup (wg), so two warps share each TMEM lane quarter
+    const int wg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     for (int i = 0; i < nsteps; ++i) {
       const int s = i % C::STAGES, b = i & 1;
       mbar_wait(&st_full[b], (i >> 1) & 1);
       tc_fence_after();
-      const float* lp = reinterpret_cast<const float*>(sSlot + s * C::SLOT + 2 * C::QT_BYTES);
-      const float* dp = lp + 64;
-      uint32_t pp[32], dd[32];
+      uint32_t sv[32], gv[32];
+      tmem_ld32(tl + b * 128 + wg * 32, sv);
+      tmem_ld32(tl + b * 128 + 64 + wg * 32, gv);
+      const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 128;
+      float lp[32], dp[32];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sv[32], gv[32];
-        tmem_ld32(tl + b * 128 + hh * 32, sv);
-        tmem_ld32(tl + b * 128 + 64 + hh * 32, gv);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int c = hh * 32 + e;
-          const float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lp[c]));
-          const float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lp[c + 1]));
-          const float d0 = p0 * (__uint_as_float(gv[e]) - dp[c]);
-          const float d1 = p1 * (__uint_as_float(gv[e + 1]) - dp[c + 1]);
-          pp[hh * 16 + e / 2] = pack_bf16(p0, p1);
-          dd[hh * 16 + e / 2] = pack_bf16(d0, d1);
-        }
+      for (int c = 0; c < 32; c += 4) {
+        const float4 a = ld_shared_f4(lds + c * 4);
+        const float4 e = ld_shared_f4(lds + 256 + c * 4);
+        lp[c] = a.x; lp[c + 1] = a.y; lp[c + 2] = a.z; lp[c + 3] = a.w;
+        dp[c] = e.x; dp[c + 1] = e.y; dp[c + 2] = e.z; dp[c + 3] = e.w;
       }
-      tmem_st32(tl + b * 128, pp);        // P^T over S^T
-      tmem_st32(tl + b * 128 + 64, dd);   // dS^T over dP^T
+      tmem_wait_ld();
+      uint32_t pp[16], dd[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lp[e]));
+        const float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lp[e + 1]));
+        pp[e / 2] = pack_bf16(p0, p1);
+        dd[e / 2] = pack_bf16(p0 * (__uint_as_float(gv[e]) - dp[e]),
+                              p1 * (__uint_as_float(gv[e + 1]) - dp[e + 1]));
+      }
+      tmem_st16(tl + b * 128 + wg * 16, pp);        // P^T over S^T
+      tmem_st16(tl + b * 128 + 64 + wg * 16, dd);   // dS^T over dP^T
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&pds_full[b]);
     }
-    // epilogue: dV, scale * dK (+)= into the fp32 accumulators
+    // epilogue: warpgroup 0 drains dV, warpgroup 1 drains scale * dK, into the
+    // fp32 accumulators (one read-modify-write when accumulating)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
     const int row = n0 + r;
     const bool valid = row < p.rows_kv;
+    const uint32_t col = wg ? C::DK_COL : C::DV_COL;
+    const float mul = wg ? p.scale : 1.f;
+    float* dst = wg ? p.dk + (int64_t)g * p.dk_hs + (int64_t)row * p.dk_rs
+                    : p.dv + (int64_t)g * p.dv_hs + (int64_t)row * p.dv_rs;
 #pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t col = which ? C::DK_COL : C::DV_COL;
-      const float mul = which ? p.scale : 1.f;
-      float* dst = which ? p.dk + (int64_t)g * p.dk_hs + (int64_t)row * p.dk_rs
-                         : p.dv + (int64_t)g * p.dv_hs + (int64_t)row * p.dv_rs;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tl + col + c * 32, v);
-        tmem_wait_ld();
-        if (valid) {
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tl + col + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            float4* ptr = reinterpret_cast<float4*>(dst + c * 32 + e);
-            float4 a = make_float4(__uint_as_float(v[e]) * mul, __uint_as_float(v[e + 1]) * mul,
-                                   __uint_as_float(v[e + 2]) * mul,
-                                   __uint_as_float(v[e + 3]) * mul);
-            if (p.accumulate) {
-              const float4 o = *ptr;
-              a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
-            }
-            *ptr = a;
+        for (int e = 0; e < 32; e += 4) {
+          float4* ptr = reinterpret_cast<float4*>(dst + c * 32 + e);
+          float4 a = make_float4(__uint_as_float(v[e]) * mul, __uint_as_float(v[e + 1]) * mul,
+                                 __uint_as_float(v[e + 2]) * mul, __uint_as_float(v[e + 3]) * mul);
+          if (p.accumulate) {
+            const float4 o = *ptr;
+            a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
           }
+          *ptr = a;
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -622,7 +622,7 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.dv_hs = dvv->head_stride;
   p.dv_rs = dvv->row_stride;
   p.accumulate = accumulate;
-  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 192,
+  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 320,
                       DkvCfg<D>::SMEM, st>>>(mq64, mk128, mv128, mg64, p);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;

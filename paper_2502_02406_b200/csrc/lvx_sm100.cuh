@@ -153,6 +153,24 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
 // UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1.
 //   K-major operand:  SBO = byte stride between 8-row groups (1024 for dense
 //                     128-byte rows); LBO unused.
@@ -182,6 +200,20 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (offloads the MUFU unit, which bounds softmax on B200):
+// round-to-nearest split x = j + f, f in [-0.5, 0.5], degree-3 minimax of 2^f
+// (max relative error 7.5e-5, far below bf16 rounding of P), exponent add.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;          // 1.5 * 2^23
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  const float p = fmaf(fmaf(fmaf(0.0551716531f, f, 0.2426111615f), f, 0.6932609919f), f,
+                       0.9999280713f);
+  const int ji = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (ji << 23));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {

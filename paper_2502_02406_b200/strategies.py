@@ -117,7 +117,9 @@ class RoundTrace:
     rounds: list = field(default_factory=list)
     epilogue_bytes_by_class: dict = field(default_factory=dict)
     epilogue_comm_seconds: float = 0.0
+    sections: dict = field(default_factory=dict)   # named device-timed phases (seconds)
     _pending: list = field(default_factory=list, repr=False)
+    _pending_sec: list = field(default_factory=list, repr=False)
 
     def add_round(self, compute_seconds, comm_seconds, sent_bytes_by_class) -> None:
         self.rounds.append(RoundRecord(len(self.rounds), compute_seconds, comm_seconds,
@@ -127,8 +129,15 @@ class RoundTrace:
         self.add_round(0.0, 0.0, sent)
         self._pending.append((len(self.rounds) - 1, ops, t0, t1, t2))
 
+    def section(self, name: str, ops, a, b) -> None:
+        """Accumulate the device time between events a and b under ``name``."""
+        self._pending_sec.append((name, ops, a, b))
+
     def resolve(self) -> None:
         """Convert device events into seconds (call after a synchronize)."""
+        for name, ops, a, b in self._pending_sec:
+            self.sections[name] = self.sections.get(name, 0.0) + ops.elapsed(a, b)
+        self._pending_sec = []
         for idx, ops, t0, t1, t2 in self._pending:
             rec = self.rounds[idx]
             rec.compute_seconds = ops.elapsed(t0, t1)
@@ -234,7 +243,11 @@ def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block
         t2 = ops.event() if trace is not None else None
         ops.fwd_finish(q_cur, k_block, ws, o_r, l_r, o_r, l_r)   # merge(recv, delta)
         if trace is not None:
+            t3 = ops.event()
             trace._add_timed(ops, t0, t1, t2, sent)
+            trace.section("fwd_kernel", ops, t0, t1)
+            trace.section("fwd_finish", ops, t2, t3)
+            trace.section("wait", ops, t1, t2)
         o_s, l_s, q_cur = o_r, l_r, q_r
         send_block, q_block_id, cur = j, j_next, 1 - cur
 
@@ -338,7 +351,11 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
             ops.bwd_dq_finish(q_j, k_block, ws, dq_in, accumulate=True)
             dq_acc = dq_in
         if trace is not None:
+            t3 = ops.event()
             trace._add_timed(ops, t0, t1, t2, sent)
+            trace.section("dq_kernel", ops, t0, t1)
+            trace.section("gather+wait", ops, t1, t2)
+            trace.section("dq_finish", ops, t2, t3)
         dq_prev = dq_acc
         if n > 1:
             q_j, do_j, l_j, d_j = recv[:4]
@@ -355,7 +372,10 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
             trace.epilogue_bytes_by_class = epi
     dk = torch.empty(k_block.shape, dtype=sd, device=dev)
     dv = torch.empty(v_block.shape, dtype=sd, device=dev)
+    t4 = ops.event() if trace is not None else None
     ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
+    if trace is not None:
+        trace.section("dkv_kernel", ops, t4, ops.event())
     return dq_out, dk, dv
 
 
@@ -398,6 +418,8 @@ def ring_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
         ops.fwd_partial(q_block, k_cur, v_cur, scale, ws)
         ops.fwd_finish(q_block, k_cur, ws, O, L, O, L)       # merge(state, delta)
         t1 = ops.event() if trace is not None else None
+        if trace is not None:
+            trace.section("fwd_kernel", ops, t0, t1)
         if hop is not None:
             hop.wait()
             k_cur, v_cur = Kb.view(1 - cur, ks[nxt]), Vb.view(1 - cur, ks[nxt])

@@ -19,6 +19,7 @@ SHAPES = {  # hq, hkv, rows_q, rows_kv, d
     "c2full": (32, 8, 2048, 1 << 20, 128),    # Llama-3-V, n=1
     "c4round": (8, 8, 128, 65536, 64),        # OpenFlamingo, n=8
     "c3round": (28, 4, 690, 65536, 128),      # Owl3 256K, n=4 (ragged rows)
+    "c2gath": (32, 8, 2048, 131072, 128),     # Llama-3-V n=8: batched dK/dV over all blocks
 }
 
 
@@ -72,6 +73,13 @@ def main():
         res["bwd_ms"] = ms3
         res["bwd_tflops"] = bf / ms3 / 1e9
         res["bwd_frac_of_peak"] = res["bwd_tflops"] / peaks["bf16_tflops"]
+        wsb = K.workspace(K.bwd_ws_bytes(q, k), dev, slot=3)
+        res["bwd_dkv_ms"] = t(lambda: K.bwd_dkv(q, k, v, L, D, g, scale, dk, dv, False, ws=wsb))
+        res["bwd_dq_ms"] = t(lambda: (K.bwd_dq_partial(q, k, v, L, D, g, scale, wsb),
+                                      K.bwd_dq_finish(q, k, wsb, dq, True)))
+        # tensor work actually issued: dkv 4 GEMMs, dq 3 GEMMs of 2*sq*skv*hq*d each
+        res["dkv_tensor_tflops"] = 8.0 * sq * skv * hq * d / res["bwd_dkv_ms"] / 1e9
+        res["dq_tensor_tflops"] = 6.0 * sq * skv * hq * d / res["bwd_dq_ms"] / 1e9
     print(json.dumps(res))
 
 
