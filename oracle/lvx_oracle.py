@@ -410,3 +410,41 @@ def ring_backward_bytes(kv_sizes, hkv, d, b):
 def attention_flops(s_q, s_kv, hq, d, backward: bool = True) -> float:
     """4 (fwd) + 10 (bwd) x Sq Skv h d (analytics.py:113-115)."""
     return (14.0 if backward else 4.0) * s_q * s_kv * hq * d
+
+
+# ---------------------------------------------------------------------------
+# cross-attention block with K/V recompute — pkg/src/lvxattn/mllm.py
+# ---------------------------------------------------------------------------
+
+
+def _flat_heads(t):
+    h, s, d = t.shape
+    return np.ascontiguousarray(t.transpose(1, 0, 2)).reshape(s, h * d)
+
+
+def _unflat_heads(t, h):
+    s, hd = t.shape
+    return np.ascontiguousarray(t.reshape(s, h, hd // h).transpose(1, 0, 2))
+
+
+def ca_block_forward(x, y, w_q, w_k, w_v, w_o, hq, hkv=None, scale=None):
+    """mllm.py:290-301: q = x W_Q, k = y W_K, v = y W_V, attention,
+    out = x + flatten(O) W_O.  Returns (out, O, L)."""
+    hkv = hq if hkv is None else hkv
+    q, k, v = project(x, w_q, hq), project(y, w_k, hkv), project(y, w_v, hkv)
+    O, L = blockwise_attention(q, k, v, scale)
+    return x + _flat_heads(O) @ w_o, O, L
+
+
+def ca_block_backward(g, x, O, L, y, w_q, w_k, w_v, w_o, hq, hkv=None, scale=None):
+    """mllm.py:343-370 (either policy — both recompute q from x; K/V come
+    from y).  Returns (d_x, d_y, g_wq, g_wk, g_wv, g_wo)."""
+    hkv = hq if hkv is None else hkv
+    d_o = _unflat_heads(g @ w_o.T, hq)
+    g_wo = _flat_heads(O).T @ g
+    q, k, v = project(x, w_q, hq), project(y, w_k, hkv), project(y, w_v, hkv)
+    dq, dk, dv = dense_attention_backward(q, k, v, O, L, d_o, scale)
+    d_x_q, g_wq = project_backward(x, w_q, dq)
+    d_y_k, g_wk = project_backward(y, w_k, dk)
+    d_y_v, g_wv = project_backward(y, w_v, dv)
+    return g + d_x_q, d_y_k + d_y_v, g_wq, g_wk, g_wv, g_wo

@@ -260,8 +260,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             for (int q = 0; q < 8; ++q) {
               const int col = c * 32 + c8 * 8 + q;
               const float x = fmaf(__uint_as_float(sv[c8 * 8 + q]), p.scale_log2, -m_used);
-              const float ev = q < 6 ? ex2(x) : ex2_poly(x);   // 25 % off the MUFU pipe
-              e8[q] = col < nvalid ? ev : 0.f;
+              e8[q] = col < nvalid ? ex2(x) : 0.f;
               rs += e8[q];
             }
             const uint32_t chunk = (uint32_t)(c * 4 + c8);   // 16-byte chunk of the row

@@ -1,0 +1,173 @@
+"""Cross-attention layer with the MLLM-specific K/V activation recompute
+(§3.2; reference ``src/mllm.py:290-301`` forward CA block and
+``:343-370`` backward CA branch), distributed over the LV-XAttn ring.
+
+Each rank keeps its shard of the text tokens ``x_i`` (rows of the query
+block) and of the visual tokens ``y_i`` (rows of the KV block) resident;
+the weights are replicated.  Every projection is row-local, so:
+
+  forward   q_i = x_i W_Q;  [k_i | v_i] = y_i [W_K | W_V]  (one GEMM);
+            (O_i, L_i) = lvx_forward(...);  out_i = x_i + flat(O_i) W_O.
+            RECOMPUTE_KV saves only (x_i, O_i, L_i) — K/V are dropped
+            (``src/mllm.py:296-300``); STORE_KV also keeps k_i, v_i.
+  backward  d_o = g W_O^T; q_i re-projected from x_i (both policies,
+            ``:352``); k_i, v_i re-projected from the shared y_i under
+            RECOMPUTE (``:358-360``); lvx_backward; d_x = g + dQ W_Q^T;
+            d_y_i = dK W_K^T + dV W_V^T (``:365-368``); weight gradients are
+            partial sums over the rank's rows and are all-reduced (the
+            reference is single-worker, so this collective is new).
+
+The projection GEMMs run on cuBLAS through torch (plain library GEMMs);
+fusing the K/V recompute into the attention kernels' producer is the next
+step.  ``OpCounter`` counts forward-direction projection FLOP
+done inside the backward, like ``src/mllm.py:242-253``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+import torch.distributed as dist
+
+from .comm import DeviceContext
+from .kernels import AttentionState, default_scale
+from .strategies import (ShardSpec, lvx_backward, lvx_forward, ring_backward, ring_forward)
+
+
+class ActivationPolicy(str, Enum):
+    STORE_KV = "store"
+    RECOMPUTE_KV = "recompute"
+
+
+@dataclass
+class CrossAttentionWeights:
+    """W_Q [e, hq*d], W_K / W_V [e, hkv*d], W_O [hq*d, e] (head k owns
+    columns [k*d, (k+1)*d), ``src/kernels.py:228-229``)."""
+
+    w_q: torch.Tensor
+    w_k: torch.Tensor
+    w_v: torch.Tensor
+    w_o: torch.Tensor
+    hq: int
+    hkv: int
+
+    @property
+    def d(self) -> int:
+        return self.w_q.shape[1] // self.hq
+
+    def kv_weight(self) -> torch.Tensor:
+        return torch.cat([self.w_k, self.w_v], dim=1)
+
+
+@dataclass
+class CrossAttentionGrads:
+    d_x: torch.Tensor
+    d_y: torch.Tensor
+    w_q: torch.Tensor
+    w_k: torch.Tensor
+    w_v: torch.Tensor
+    w_o: torch.Tensor
+
+
+@dataclass
+class OpCounter:
+    """Forward-direction projection FLOP performed inside the backward."""
+
+    projection_flops: int = 0
+
+    def add(self, rows: int, d_in: int, d_out: int) -> None:
+        self.projection_flops += 2 * rows * d_in * d_out
+
+
+@dataclass
+class SavedCA:
+    policy: ActivationPolicy
+    x: torch.Tensor
+    state: AttentionState
+    kv: tuple | None = None
+    extras: dict = field(default_factory=dict)
+
+
+def _heads(flat: torch.Tensor, heads: int) -> torch.Tensor:
+    """[S, heads*d] -> [heads, S, d] contiguous (``src/kernels.py:236-240``)."""
+    s = flat.shape[0]
+    return flat.view(s, heads, -1).transpose(0, 1).contiguous()
+
+
+def _flat(t: torch.Tensor) -> torch.Tensor:
+    """[heads, S, d] -> [S, heads*d] (``src/mllm.py:256-258``)."""
+    h, s, d = t.shape
+    return t.transpose(0, 1).reshape(s, h * d)
+
+
+def project_kv(y: torch.Tensor, w: CrossAttentionWeights):
+    """K/V from the visual tokens with ONE GEMM y [S, e] @ [W_K | W_V]."""
+    kv = y @ w.kv_weight()
+    hkd = w.hkv * w.d
+    return _heads(kv[:, :hkd], w.hkv), _heads(kv[:, hkd:], w.hkv)
+
+
+def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: torch.Tensor,
+               w: CrossAttentionWeights, policy: ActivationPolicy = ActivationPolicy.RECOMPUTE_KV,
+               scale: float | None = None, strategy: str = "lvx"):
+    """Returns (out_i = x_i + flat(O_i) W_O, saved)."""
+    policy = ActivationPolicy(policy)
+    scale = default_scale(w.d) if scale is None else scale
+    q = _heads(x_i @ w.w_q, w.hq)
+    k, v = project_kv(y_i, w)
+    fwd = lvx_forward if strategy == "lvx" else ring_forward
+    st = fwd(ctx, shards, q, k, v, scale)
+    saved = SavedCA(policy=policy, x=x_i, state=st,
+                    kv=(k, v) if policy is ActivationPolicy.STORE_KV else None)
+    del q, k, v   # under RECOMPUTE nothing but y_i remains for the visual side
+    out = x_i + _flat(st.O.to(x_i.dtype)) @ w.w_o
+    return out, saved
+
+
+def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved: SavedCA,
+                y_i: torch.Tensor, w: CrossAttentionWeights, scale: float | None = None,
+                strategy: str = "lvx", counter: OpCounter | None = None,
+                group=None) -> CrossAttentionGrads:
+    """Backward of ``ca_forward`` (``src/mllm.py:343-370``).  Weight gradients
+    are all-reduced over the process group when n > 1."""
+    scale = default_scale(w.d) if scale is None else scale
+    dt = g_i.dtype
+    d_o = _heads(g_i @ w.w_o.T, w.hq)
+    g_wo = _flat(saved.state.O.to(dt)).T @ g_i
+    q = _heads(saved.x @ w.w_q, w.hq)
+    if counter is not None:
+        counter.add(saved.x.shape[0], w.w_q.shape[0], w.w_q.shape[1])
+    if saved.policy is ActivationPolicy.STORE_KV:
+        k, v = saved.kv
+    else:   # the MLLM-specific recompute from the one shared y
+        k, v = project_kv(y_i, w)
+        if counter is not None:
+            counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
+            counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
+    bwd = lvx_backward if strategy == "lvx" else ring_backward
+    dq, dk, dv = bwd(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
+    del k, v
+    dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
+    d_x = g_i + dq @ w.w_q.T
+    g_wq = saved.x.T @ dq
+    dkv = torch.cat([dk, dv], dim=1)
+    d_y = dkv @ w.kv_weight().T
+    g_wkv = y_i.T @ dkv
+    hkd = w.hkv * w.d
+    g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
+    if ctx.n > 1:
+        for t in (g_wq, g_wk, g_wv, g_wo):
+            dist.all_reduce(t, group=group if group is not None else ctx.group)
+    return CrossAttentionGrads(d_x=d_x, d_y=d_y, w_q=g_wq, w_k=g_wk, w_v=g_wv, w_o=g_wo)
+
+
+def activation_bytes(saved: SavedCA) -> int:
+    """Bytes this layer keeps alive between forward and backward (the
+    per-layer categories of ``src/mllm.py:190-209``): x, O, L (+ K, V)."""
+    n = saved.x.numel() * saved.x.element_size()
+    n += saved.state.O.numel() * saved.state.O.element_size()
+    n += saved.state.L.numel() * saved.state.L.element_size()
+    if saved.kv is not None:
+        n += sum(t.numel() * t.element_size() for t in saved.kv)
+    return n

@@ -30,3 +30,9 @@ def golden_strategies():
 def golden_c1():
     import numpy as np
     return dict(np.load(GOLDEN / "golden_c1.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_mllm_ca():
+    import numpy as np
+    return dict(np.load(GOLDEN / "golden_mllm_ca.npz"))

@@ -107,7 +107,38 @@ def main() -> None:
           "fwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_forward]),
           "bwd_bytes": np.array([t.total_sent_bytes() for t in res.traces_backward])}
     np.savez_compressed(OUT / "golden_c1.npz", **c1)
-    for f in ("golden_kernels.npz", "golden_strategies.npz", "golden_c1.npz"):
+    # ---------------- MLLM cross-attention block (recompute) -------------
+    # one block, CA at position 0, MLP weights zeroed so the block is exactly
+    # the CA layer (x + tanh(x*0)*0 = x): pins the CA math incl. K/V recompute
+    from dataclasses import replace as _replace
+    from lvxattn.mllm import (ActivationPolicy, ModelParams, ToyMllmConfig, mllm_backward,
+                              mllm_forward, OpCounter)
+    cfg = ToyMllmConfig(num_lm_blocks=1, ca_positions=(0,), d_embed=12, h=2, d=6, frames=3,
+                        tokens_per_frame=7, s_q=9, dtype="f64")
+    params = ModelParams.init_random(cfg, seed=3)
+    for blk in params.lm:
+        blk.w1[...] = 0.0
+        blk.w2[...] = 0.0
+    x0 = srt(61, (cfg.s_q, cfg.d_embed))
+    y = srt(62, (cfg.s_kv, cfg.d_embed))
+    gout = srt(63, (cfg.s_q, cfg.d_embed))
+    ca = {}
+    for pol in (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV):
+        out, saved, ledger = mllm_forward(x0, y, params, cfg, pol)
+        cnt = OpCounter()
+        gr = mllm_backward(gout, saved, y, params, cfg, pol, counter=cnt)
+        p0 = params.ca[0]
+        ca.update({f"{pol.value}_out": out, f"{pol.value}_dx": gr.d_x0, f"{pol.value}_dy": gr.d_y,
+                   f"{pol.value}_gwq": gr.ca[0].w_q, f"{pol.value}_gwk": gr.ca[0].w_k,
+                   f"{pol.value}_gwv": gr.ca[0].w_v, f"{pol.value}_gwo": gr.ca[0].w_o,
+                   f"{pol.value}_flops": np.array(cnt.projection_flops)})
+    ca.update({"x": x0, "y": y, "g": gout, "w_q": params.ca[0].w_q, "w_k": params.ca[0].w_k,
+               "w_v": params.ca[0].w_v, "w_o": params.ca[0].w_o,
+               "dims": np.array([cfg.h, cfg.d, cfg.d_embed])})
+    np.savez_compressed(OUT / "golden_mllm_ca.npz", **ca)
+
+    for f in ("golden_kernels.npz", "golden_strategies.npz", "golden_c1.npz",
+              "golden_mllm_ca.npz"):
         print(f, (OUT / f).stat().st_size, "bytes")
 
 

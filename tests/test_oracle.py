@@ -110,3 +110,19 @@ def test_gqa_adapter_consistent():
     assert orc.max_norm_error(dq, dqm) <= 1e-14
     assert orc.max_norm_error(dk, orc.reduce_kv_grad(dkm, 2)) <= 1e-14
     assert orc.max_norm_error(dv, orc.reduce_kv_grad(dvm, 2)) <= 1e-14
+
+
+def test_ca_block_matches_reference_mllm(golden_mllm_ca):
+    g = golden_mllm_ca
+    h, d, e = (int(v) for v in g["dims"])
+    out, O, L = orc.ca_block_forward(g["x"], g["y"], g["w_q"], g["w_k"], g["w_v"], g["w_o"], h)
+    for pol in ("store", "recompute"):
+        assert orc.max_norm_error(out, g[f"{pol}_out"]) <= 1e-12
+    dx, dy, gq, gk, gv, go = orc.ca_block_backward(g["g"], g["x"], O, L, g["y"], g["w_q"],
+                                                   g["w_k"], g["w_v"], g["w_o"], h)
+    for pol in ("store", "recompute"):
+        for a, b in ((dx, "dx"), (dy, "dy"), (gq, "gwq"), (gk, "gwk"), (gv, "gwv"), (go, "gwo")):
+            assert orc.max_norm_error(a, g[f"{pol}_{b}"]) <= 1e-12, (pol, b)
+    # the recompute policy does exactly two extra y projections (mllm.py:358-363)
+    s_kv = g["y"].shape[0]
+    assert int(g["recompute_flops"]) - int(g["store_flops"]) == 2 * 2 * s_kv * e * h * d

@@ -90,3 +90,62 @@ def test_gloo_gqa_lvx_and_ring_agree_with_oracle():
     for O, L, dQ, dK, dV, *_ in outs:
         for a, b in ((O, Od), (L, Ld), (dQ, dq), (dK, dk), (dV, dv)):
             assert orc.max_norm_error(a, b) <= 1e-12
+
+
+def _ca_worker(rank, n, port, golden, policy, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=n)
+        from paper_2502_02406_b200.comm import DeviceContext
+        from paper_2502_02406_b200.recompute import (CrossAttentionWeights, OpCounter, ca_backward,
+                                                     ca_forward)
+        from paper_2502_02406_b200.strategies import ShardSpec
+        from tests.oracle_ops import OracleOps
+        g = golden
+        h, d, e = (int(v) for v in g["dims"])
+        T = lambda a: torch.from_numpy(a)  # noqa: E731
+        w = CrossAttentionWeights(T(g["w_q"]), T(g["w_k"]), T(g["w_v"]), T(g["w_o"]), h, h)
+        sh = ShardSpec.balanced(g["x"].shape[0], g["y"].shape[0], n)
+        (qa, qb), (ka, kb) = sh.q_ranges[rank], sh.kv_ranges[rank]
+        ctx = DeviceContext(rank, n, group=dist.group.WORLD, device="cpu", ops=OracleOps())
+        x_i, y_i, g_i = T(g["x"][qa:qb]), T(g["y"][ka:kb]), T(g["g"][qa:qb])
+        out, saved = ca_forward(ctx, sh, x_i, y_i, w, policy)
+        cnt = OpCounter()
+        gr = ca_backward(ctx, sh, g_i, saved, y_i, w, counter=cnt)
+        parts = [None] * n
+        dist.all_gather_object(parts, (rank, out.numpy(), gr.d_x.numpy(), gr.d_y.numpy(),
+                                       cnt.projection_flops))
+        if rank == 0:
+            parts.sort(key=lambda p: p[0])
+            q.put(("ok", np.concatenate([p[1] for p in parts]),
+                   np.concatenate([p[2] for p in parts]), np.concatenate([p[3] for p in parts]),
+                   gr.w_q.numpy(), gr.w_k.numpy(), gr.w_v.numpy(), gr.w_o.numpy(),
+                   sum(p[4] for p in parts)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put(("err", rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("policy", ["recompute", "store"])
+def test_gloo_cross_attention_recompute_matches_reference(golden_mllm_ca, policy):
+    n = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    ps = [ctx.Process(target=_ca_worker, args=(r, n, port, golden_mllm_ca, policy, q))
+          for r in range(n)]
+    for p in ps:
+        p.start()
+    msg = q.get()
+    for p in ps:
+        p.join(timeout=120)
+    assert msg[0] == "ok", msg
+    _, out, dx, dy, gq, gk, gv, go, flops = msg
+    g = golden_mllm_ca
+    pol = policy
+    for a, b in ((out, "out"), (dx, "dx"), (dy, "dy"), (gq, "gwq"), (gk, "gwk"), (gv, "gwv"),
+                 (go, "gwo")):
+        assert orc.max_norm_error(a, g[f"{pol}_{b}"]) <= 1e-12, b
+    assert flops == int(g[f"{pol}_flops"])
