@@ -332,13 +332,34 @@ def native_arm(args):
 
     # --- no-communication arm and the Ring baseline
     if world > 1:
+        # no-communication arm: the identical schedule with every
+        # hop skipped.  Measured as interleaved A/B step pairs so power-cap and
+        # clock drift hit both arms equally; also reported from a separate block.
+        pairs = max(3, args.steps)
+        a_ms, b_ms = [], []
+        for _ in range(pairs):
+            for c, acc in ((ctx, a_ms), (ctx_nc, b_ms)):
+                torch.cuda.synchronize()
+                dist.barrier()
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record()
+                step(c)
+                eb.record()
+                torch.cuda.synchronize()
+                t = torch.tensor([ea.elapsed_time(eb)], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                acc.append(t.item())
+        ms_a, ms_b = statistics.median(a_ms), statistics.median(b_ms)
+        out["no_comm_ms_per_step"] = ms_b
+        out["overhead_vs_no_comm"] = ms_a / ms_b - 1.0
+        out["no_comm_ab"] = {"pairs": pairs, "comm_ms_median": ms_a, "no_comm_ms_median": ms_b,
+                             "comm_ms": a_ms, "no_comm_ms": b_ms}
         ms_nc, tr_nc, *_ = timed(ctx_nc, max(2, args.steps // 2), 1)
-        out["no_comm_ms_per_step"] = ms_nc
+        out["no_comm_block_ms_per_step"] = ms_nc
         out["no_comm_phase_ms_per_step"] = {
             "fwd_kernel": sec([a for a, _ in tr_nc], "fwd_kernel") * 1e3,
             "dq_kernel": sec([b for _, b in tr_nc], "dq_kernel") * 1e3,
             "dkv_kernel": sec([b for _, b in tr_nc], "dkv_kernel") * 1e3}
-        out["overhead_vs_no_comm"] = ms / ms_nc - 1.0
         if not args.no_ring_compare and args.strategy == "lvx":
             ms_ring, rtr, *_ = timed(ctx, max(2, args.steps // 2), 1,
                                      strategy=(ring_forward, ring_backward))

@@ -10,15 +10,17 @@
 // split of the resident KV block.  Warp roles (320 threads):
 //   warps 0-3  softmax for query tile 0 (TMEM lanes 0-127, one row per thread)
 //   warps 4-7  softmax for query tile 1
-//   warp  8    TMA producer: Q tiles once, then K_j / V_j into a 3-slot ring
+//   warp  8    TMA producer: Q tiles once, then K_j / V_j into a 5-slot
+//              128B-swizzled ring (10 slots at d=64)
 //   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
 // TMEM (512 columns): S_t = Q_t K_j^T at cols [128t, 128t+128), O_t at
-// [256 + t*D, 256 + (t+1)*D).  S_t is read by its softmax warps, which write
-// P_t = exp2(S_t*scale*log2e - m) in bf16 to shared memory (K-major, 128B
-// swizzle) for the PV MMA.  The MMA order QK(j) -> PV(j-1) lets softmax of
-// tile j overlap the PV of tile j-1.  The running max is updated lazily: O
-// in TMEM is rescaled only when the row max grows by more than 2^8, which is
-// exact (P, l and O always share one reference max).
+// [256 + t*D, 256 + (t+1)*D).  The softmax warps read S_t in two passes (row
+// max, then exp2) and write P_t = exp2(S_t*scale*log2e - m) as bf16 pairs
+// back OVER S_t; PV_t is a TS MMA reading P_t from TMEM.  tcgen05.mma runs in
+// issue order, so the stream PV_t(j) -> QK_t(j+1) needs no extra barrier and
+// the commit after QK_t(j) also proves PV_t(j-1) done.  The running max is
+// updated lazily: O in TMEM is rescaled only when the row max grows by more
+// than 2^8, which is exact (P, l and O always share one reference max).
 // Each split writes a normalised partial (O, L) in fp32 to the workspace;
 // fwd_combine_kernel merges the splits (and the prior ring state) in a fixed
 // order.
@@ -46,10 +48,9 @@ struct FwdCfg {
   static constexpr int PANELS = D / 64;      // 128-byte (64 x bf16) column panels
   static constexpr int Q_BYTES = kBM * D * 2;
   static constexpr int KV_BYTES = kBN * D * 2;
-  static constexpr int P_BYTES = kBM * kBN * 2;
-  static constexpr int STAGES = D == 128 ? 3 : 6;
-  static constexpr int NBAR = 1 + 2 * STAGES + 8;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * KV_BYTES + 2 * P_BYTES + NBAR * 8 + 16;
+  static constexpr int STAGES = D == 128 ? 5 : 10;
+  static constexpr int NBAR = 1 + 2 * STAGES + 6;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * KV_BYTES + NBAR * 8 + 16;
   static constexpr int S_COL0 = 0;
   static constexpr int O_COL0 = 256;
 };
@@ -75,14 +76,12 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
   uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
   uint8_t* sQ = sm;
   uint8_t* sKV = sQ + 2 * C::Q_BYTES;
-  uint8_t* sP = sKV + C::STAGES * C::KV_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::KV_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::STAGES;
   uint64_t* s_full = kv_empty + C::STAGES;   // [2]
-  uint64_t* s_free = s_full + 2;             // [2]
-  uint64_t* p_full = s_free + 2;             // [2]
+  uint64_t* p_full = s_full + 2;             // [2]
   uint64_t* o_done = p_full + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
@@ -108,7 +107,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&s_free[t], 128);
       mbar_init(&p_full[t], 128);
       mbar_init(&o_done[t], 1);
     }
@@ -146,56 +144,58 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    // Tensor-pipe order per KV tile j and query tile t:
+    //   ... PV_t(j-1) -> QK_t(j) -> [softmax_t(j) writes P over S_t] -> PV_t(j) -> QK_t(j+1)
+    // tcgen05.mma executes in issue order, so QK_t(j+1) overwrites S_t/P_t only
+    // after PV_t(j) has consumed P_t, and the s_full commit after QK_t(j)
+    // also certifies that PV_t(j-1) is complete (O_t stable for a rescale).
     if (lane == 0) {
       constexpr uint32_t idQK = idesc_bf16(kBM, kBN, false, false);
       constexpr uint32_t idPV = idesc_bf16(kBM, D, false, true);
+      auto slot_of = [&](int L) { return L % C::STAGES; };
+      auto wait_load = [&](int L) {
+        mbar_wait(&kv_full[slot_of(L)], (L / C::STAGES) & 1);
+        tc_fence_after();
+      };
+      auto issue_qk = [&](int t, int j) {
+        const uint32_t kb = smem_u32(sKV + slot_of(2 * j) * C::KV_BYTES);
+        const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
+          mma_bf16_ss(tmem + C::S_COL0 + t * kBN, umma_desc_sw128(qb + off, 0, 1024),
+                      umma_desc_sw128(kb + (kk >> 2) * (kBN * 128) + (kk & 3) * 32, 0, 1024),
+                      idQK, kk > 0);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t vb = smem_u32(sKV + slot_of(2 * j + 1) * C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
+          mma_bf16_ts(tmem + C::O_COL0 + t * D, tmem + C::S_COL0 + t * kBN + kk * 8,
+                      umma_desc_sw128(vb + kk * 16 * 128, kBN * 128, 1024), idPV,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&o_done[t]);
+      };
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int j = 0; j <= nt; ++j) {
-        if (j < nt) {
-          const int L = 2 * j, s = L % C::STAGES, u = L / C::STAGES;
-          mbar_wait(&kv_full[s], u & 1);
+      wait_load(0);
+      for (int t = 0; t < 2; ++t)
+        if (active[t]) issue_qk(t, 0);
+      mma_commit(&kv_empty[slot_of(0)]);            // K_0 consumed
+      for (int j = 0; j < nt; ++j) {
+        wait_load(2 * j + 1);                       // V_j
+        if (j + 1 < nt) wait_load(2 * j + 2);       // K_{j+1}
+        for (int t = 0; t < 2; ++t) {
+          if (!active[t]) continue;
+          mbar_wait(&p_full[t], j & 1);
           tc_fence_after();
-          const uint32_t kb = smem_u32(sKV + s * C::KV_BYTES);
-          for (int t = 0; t < 2; ++t) {
-            if (!active[t]) continue;
-            if (j > 0) {
-              mbar_wait(&s_free[t], (j - 1) & 1);
-              tc_fence_after();
-            }
-            const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
-              mma_bf16_ss(tmem + C::S_COL0 + t * kBN, umma_desc_sw128(qb + off, 0, 1024),
-                          umma_desc_sw128(kb + (kk >> 2) * (kBN * 128) + (kk & 3) * 32, 0, 1024),
-                          idQK, kk > 0);
-            }
-            mma_commit(&s_full[t]);
-          }
-          mma_commit(&kv_empty[s]);
+          issue_pv(t, j);
+          if (j + 1 < nt) issue_qk(t, j + 1);
         }
-        if (j > 0) {
-          const int jj = j - 1, L = 2 * jj + 1, s = L % C::STAGES, u = L / C::STAGES;
-          mbar_wait(&kv_full[s], u & 1);
-          tc_fence_after();
-          const uint32_t vb = smem_u32(sKV + s * C::KV_BYTES);
-          for (int t = 0; t < 2; ++t) {
-            if (!active[t]) continue;
-            mbar_wait(&p_full[t], jj & 1);
-            tc_fence_after();
-            const uint32_t pb = smem_u32(sP + t * C::P_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk) {
-              const uint32_t aoff = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
-              mma_bf16_ss(tmem + C::O_COL0 + t * D, umma_desc_sw128(pb + aoff, 0, 1024),
-                          umma_desc_sw128(vb + kk * 16 * 128, kBN * 128, 1024), idPV,
-                          (jj > 0 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(&o_done[t]);
-          }
-          mma_commit(&kv_empty[s]);
-        }
+        mma_commit(&kv_empty[slot_of(2 * j + 1)]);  // V_j consumed
+        if (j + 1 < nt) mma_commit(&kv_empty[slot_of(2 * j + 2)]);   // K_{j+1} consumed
       }
     }
   } else {
@@ -203,11 +203,9 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     const int t = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     if (active[t]) {
       const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-      const uint32_t pb = smem_u32(sP + t * C::P_BYTES) + r * 128;
-      const uint32_t sw = (uint32_t)(r & 7);
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j) {
-        mbar_wait(&s_full[t], j & 1);
+        mbar_wait(&s_full[t], j & 1);   // QK_t(j) done, hence PV_t(j-1) done
         tc_fence_after();
         const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
         const uint32_t sa = tl + C::S_COL0 + t * kBN;
@@ -218,18 +216,19 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
           uint32_t sv[32];
           tmem_ld32(sa + c * 32, sv);
           tmem_wait_ld();
+          if (nvalid == kBN) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
+          }
         }
         mx *= p.scale_log2;
         const bool need = mx > m_used + kRescaleThreshold;
-        if (j > 0) {  // PV(j-1) done: P_t is free and O_t is stable
-          mbar_wait(&o_done[t], (j - 1) & 1);
-          tc_fence_after();
-        }
         const float alpha = need ? ex2(m_used - mx) : 1.f;
-        if (__any_sync(0xffffffffu, need && j > 0)) {
+        if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
@@ -240,39 +239,36 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
             tmem_st32(oa, ov);
           }
-          tmem_wait_st();
         }
         if (need) {
           l *= alpha;
           m_used = mx;
         }
-        // pass 2: P = exp2(S*c - m) -> bf16 -> swizzled shared memory
+        // pass 2: P = exp2(S*c - m) -> bf16 pairs written over S_t (chunk c of
+        // S is read before packed columns [16c, 16c+16) are overwritten)
         float rs = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t sv[32];
+          uint32_t sv[32], pk[16];
           tmem_ld32(sa + c * 32, sv);
           tmem_wait_ld();
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
-            float e8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int col = c * 32 + c8 * 8 + q;
-              const float x = fmaf(__uint_as_float(sv[c8 * 8 + q]), p.scale_log2, -m_used);
-              e8[q] = col < nvalid ? ex2(x) : 0.f;
-              rs += e8[q];
+          for (int e = 0; e < 32; e += 2) {
+            const int col = c * 32 + e;
+            float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used));
+            float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used));
+            if (nvalid < kBN) {
+              p0 = col < nvalid ? p0 : 0.f;
+              p1 = col + 1 < nvalid ? p1 : 0.f;
             }
-            const uint32_t chunk = (uint32_t)(c * 4 + c8);   // 16-byte chunk of the row
-            const uint32_t addr = pb + (chunk >> 3) * (kBM * 128) + (((chunk & 7u) ^ sw) << 4);
-            st_shared_v4(addr, pack_bf16(e8[0], e8[1]), pack_bf16(e8[2], e8[3]),
-                         pack_bf16(e8[4], e8[5]), pack_bf16(e8[6], e8[7]));
+            rs += p0 + p1;
+            pk[e / 2] = pack_bf16(p0, p1);
           }
+          tmem_st16(sa + c * 16, pk);
         }
-        tc_fence_before();
-        mbar_arrive(&s_free[t]);   // S_t fully read: QK(j+1) may overwrite it
+        tmem_wait_st();
         l += rs;
-        fence_proxy_async_smem();
+        tc_fence_before();
         mbar_arrive(&p_full[t]);
       }
       // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial

@@ -1,0 +1,70 @@
+"""K/V recompute cross-attention layer on the GPU (bf16 tensor-core path)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import lvx_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _setup(e=256, hq=4, hkv=2, d=64, sq=96, skv=700, seed=8):
+    from paper_2502_02406_b200.recompute import CrossAttentionWeights
+    rnd = lambda s, st, sc=1.0: orc.seeded_random_tensor(seed, s, scale=sc, stream=st)  # noqa: E731
+    ws = 0.5 / np.sqrt(e)
+    x, y, g = rnd((sq, e), 1), rnd((skv, e), 2), rnd((sq, e), 3)
+    wq, wk, wv, wo = rnd((e, hq * d), 4, ws), rnd((e, hkv * d), 5, ws), rnd((e, hkv * d), 6, ws), \
+        rnd((hq * d, e), 7, ws)
+    bf = lambda a: torch.from_numpy(a).to("cuda", torch.bfloat16)  # noqa: E731
+    w = CrossAttentionWeights(bf(wq), bf(wk), bf(wv), bf(wo), hq, hkv)
+    host = {k: t.double().cpu().numpy() for k, t in
+            dict(x=bf(x), y=bf(y), g=bf(g), wq=w.w_q, wk=w.w_k, wv=w.w_v, wo=w.w_o).items()}
+    return w, bf(x), bf(y), bf(g), host
+
+
+def test_recompute_equals_store_and_saves_kv_memory():
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200.recompute import (ActivationPolicy, OpCounter, activation_bytes,
+                                                 ca_backward, ca_forward)
+    w, x, y, g, _ = _setup()
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
+    res, mem, ops = {}, {}, {}
+    for pol in (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV):
+        out, saved = ca_forward(ctx, sh, x, y, w, pol)
+        mem[pol] = activation_bytes(saved)
+        cnt = OpCounter()
+        gr = ca_backward(ctx, sh, g, saved, y, w, counter=cnt)
+        ops[pol] = cnt.projection_flops
+        res[pol] = [out, gr.d_x, gr.d_y, gr.w_q, gr.w_k, gr.w_v, gr.w_o]
+    for a, b in zip(res[ActivationPolicy.STORE_KV], res[ActivationPolicy.RECOMPUTE_KV]):
+        assert torch.equal(a, b)          # cuBLAS recompute reproduces K/V bit for bit
+    kv_bytes = 2 * y.shape[0] * w.hkv * w.d * 2
+    assert mem[ActivationPolicy.STORE_KV] - mem[ActivationPolicy.RECOMPUTE_KV] == kv_bytes
+    e = x.shape[1]
+    assert ops[ActivationPolicy.RECOMPUTE_KV] - ops[ActivationPolicy.STORE_KV] == \
+        2 * 2 * y.shape[0] * e * w.hkv * w.d
+
+
+def test_recompute_layer_vs_oracle():
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200.recompute import ActivationPolicy, ca_backward, ca_forward
+    w, x, y, g, h = _setup()
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
+    out, saved = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV)
+    gr = ca_backward(ctx, sh, g, saved, y, w)
+    ro, O, L = orc.ca_block_forward(h["x"], h["y"], h["wq"], h["wk"], h["wv"], h["wo"], w.hq, w.hkv)
+    rdx, rdy, rq, rk, rv, rwo = orc.ca_block_backward(h["g"], h["x"], O, L, h["y"], h["wq"],
+                                                      h["wk"], h["wv"], h["wo"], w.hq, w.hkv)
+    errs = {n: orc.max_norm_error(a.double().cpu().numpy(), b) for n, a, b in
+            (("out", out, ro), ("d_x", gr.d_x, rdx), ("d_y", gr.d_y, rdy), ("w_q", gr.w_q, rq),
+             ("w_k", gr.w_k, rk), ("w_v", gr.w_v, rv), ("w_o", gr.w_o, rwo))}
+    print("\nrecompute CA layer bf16 vs f64 oracle:", errs)
+    assert max(errs.values()) <= 3e-2   # bf16 projections + bf16 attention operands
