@@ -151,10 +151,13 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {   // converged warp; one elected lane issues (see lvx_fwd_sm100.cu)
       constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
       constexpr uint32_t idKV = idesc_bf16(128, D, false, true);
-      const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+      const uint64_t dk0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
+      const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
+      const uint64_t ds0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);            // K-major Q / dO
+      const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), kStep * 128, 1024);  // MN-major Q / dO
       mbar_wait(kv_full, 0);
       tc_fence_after();
       for (int i = 0; i <= nsteps; ++i) {
@@ -162,42 +165,45 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
           const int s = i % C::STAGES, b = i & 1;
           mbar_wait(&qd_full[s], (i / C::STAGES) & 1);
           tc_fence_after();
-          const uint32_t qb = smem_u32(sSlot + s * C::SLOT), gb = qb + C::QT_BYTES;
+          if (elect_one()) {
+            const uint64_t qd = ds0 + ((s * C::SLOT) >> 4), gd = qd + (C::QT_BYTES >> 4);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t ko = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-            const uint32_t qo = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
-            mma_bf16_ss(tmem + b * 128, umma_desc_sw128(kb + ko, 0, 1024),
-                        umma_desc_sw128(qb + qo, 0, 1024), idS, kk > 0);
-          }
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t ko = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+              const uint32_t qo = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + b * 128, dk0 + ko, qd + qo, idS, kk > 0);
+            }
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t ko = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-            const uint32_t qo = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
-            mma_bf16_ss(tmem + b * 128 + 64, umma_desc_sw128(vb + ko, 0, 1024),
-                        umma_desc_sw128(gb + qo, 0, 1024), idS, kk > 0);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t ko = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+              const uint32_t qo = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + b * 128 + 64, dv0 + ko, gd + qo, idS, kk > 0);
+            }
+            mma_commit(&st_full[b]);
           }
-          mma_commit(&st_full[b]);
+          __syncwarp();
         }
         if (i > 0) {
           const int ii = i - 1, s = ii % C::STAGES, b = ii & 1;
           mbar_wait(&pds_full[b], (ii >> 1) & 1);
           tc_fence_after();
-          const uint32_t qb = smem_u32(sSlot + s * C::SLOT), gb = qb + C::QT_BYTES;
+          if (elect_one()) {
+            const uint64_t qm = dm0 + ((s * C::SLOT) >> 4), gm = qm + (C::QT_BYTES >> 4);
 #pragma unroll
-          for (int kk = 0; kk < kStep / 16; ++kk)   // dV += P^T dO
-            mma_bf16_ts(tmem + C::DV_COL, tmem + b * 128 + kk * 8,
-                        umma_desc_sw128(gb + kk * 16 * 128, kStep * 128, 1024), idKV,
-                        (ii > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < kStep / 16; ++kk)   // dV += P^T dO
+              mma_bf16_ts(tmem + C::DV_COL, tmem + b * 128 + kk * 8, gm + ((kk * 16 * 128) >> 4),
+                          idKV, (ii > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < kStep / 16; ++kk)   // dK += dS^T Q
-            mma_bf16_ts(tmem + C::DK_COL, tmem + b * 128 + 64 + kk * 8,
-                        umma_desc_sw128(qb + kk * 16 * 128, kStep * 128, 1024), idKV,
-                        (ii > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&qd_empty[s]);
+            for (int kk = 0; kk < kStep / 16; ++kk)   // dK += dS^T Q
+              mma_bf16_ts(tmem + C::DK_COL, tmem + b * 128 + 64 + kk * 8,
+                          qm + ((kk * 16 * 128) >> 4), idKV, (ii > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(&qd_empty[s]);
+          }
+          __syncwarp();
         }
       }
-      mma_commit(dkv_done);
+      if (elect_one()) mma_commit(dkv_done);
+      __syncwarp();
     }
   } else {
     // ------------------------------- softmax: kv row per thread, 32 of the 64
@@ -282,7 +288,7 @@ struct DqCfg {
   static constexpr int KVT_BYTES = kStep * D * 2;
   static constexpr int SLOT = 2 * KVT_BYTES;
   static constexpr int STAGES = D == 128 ? 3 : 6;
-  static constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 1;
+  static constexpr int NBAR = 1 + 2 * STAGES + 8 + 1;
   static constexpr int SMEM = 1024 + 4 * Q_BYTES + STAGES * SLOT + NBAR * 8 + 16;
   static constexpr int DQ_COL = 256;
 };
@@ -303,8 +309,10 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* qd_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::STAGES;
-  uint64_t* s_full = kv_empty + C::STAGES;   // [2]
-  uint64_t* ds_full = s_full + 2;            // [2]
+  uint64_t* s_full = kv_empty + C::STAGES;   // [2] S_t(j) in TMEM
+  uint64_t* s_read = s_full + 2;             // [2] softmax has read S_t(j)
+  uint64_t* dp_full = s_read + 2;            // [2] dP_t(j) in TMEM
+  uint64_t* ds_full = dp_full + 2;           // [2] dS_t(j) written over dP_t
   uint64_t* dq_done = ds_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
@@ -330,6 +338,8 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
+      mbar_init(&s_read[t], 128);
+      mbar_init(&dp_full[t], 1);
       mbar_init(&ds_full[t], 128);
     }
     mbar_init(dq_done, 1);
@@ -369,61 +379,89 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
+    {   // converged warp; one elected lane issues
       constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
       constexpr uint32_t idQ = idesc_bf16(128, D, false, true);
+      const uint64_t dq0 = umma_desc_sw128(smem_u32(sQ), 0, 1024);
+      const uint64_t dg0 = umma_desc_sw128(smem_u32(sG), 0, 1024);
+      const uint64_t dkv0 = umma_desc_sw128(smem_u32(sKV), 0, 1024);           // K-major K / V
+      const uint64_t dkm0 = umma_desc_sw128(smem_u32(sKV), kStep * 128, 1024); // MN-major K
       mbar_wait(qd_full, 0);
       tc_fence_after();
-      auto issue_sdp = [&](int t, int j) {
-        const int s = j % C::STAGES;
-        const uint32_t kb = smem_u32(sKV + s * C::SLOT), vb = kb + C::KVT_BYTES;
-        const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES), gb = smem_u32(sG + t * C::Q_BYTES);
+      // Per query tile t the tensor pipe sees
+      //   S_t(j+1) [after softmax read S_t(j)]  ...  dQ_t(j) [dS over dP_t] -> dP_t(j+1)
+      // so the exponentials of step j+1 overlap dQ_t(j); only dS = P(dP - D)
+      // sits between dP_t(j) and dQ_t(j).
+      auto issue_s = [&](int t, int j) {
+        if (elect_one()) {
+          const uint64_t a = dq0 + ((t * C::Q_BYTES) >> 4);
+          const uint64_t b = dkv0 + (((j % C::STAGES) * C::SLOT) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t qo = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          const uint32_t ko = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
-          mma_bf16_ss(tmem + t * 128, umma_desc_sw128(qb + qo, 0, 1024),
-                      umma_desc_sw128(kb + ko, 0, 1024), idS, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t qo = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t ko = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + t * 128, a + qo, b + ko, idS, kk > 0);
+          }
+          mma_commit(&s_full[t]);
         }
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t qo = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          const uint32_t ko = (kk >> 2) * (kStep * 128) + (kk & 3) * 32;
-          mma_bf16_ss(tmem + t * 128 + 64, umma_desc_sw128(gb + qo, 0, 1024),
-                      umma_desc_sw128(vb + ko, 0, 1024), idS, kk > 0);
-        }
-        mma_commit(&s_full[t]);
+        __syncwarp();
       };
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
+      auto issue_dp = [&](int t, int j) {
+        if (elect_one()) {
+          const uint64_t a = dg0 + ((t * C::Q_BYTES) >> 4);
+          const uint64_t b = dkv0 + (((j % C::STAGES) * C::SLOT + C::KVT_BYTES) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t qo = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t ko = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + t * 128 + 64, a + qo, b + ko, idS, kk > 0);
+          }
+          mma_commit(&dp_full[t]);
+        }
+        __syncwarp();
+      };
+      auto issue_dq = [&](int t, int j) {
+        if (elect_one()) {
+          const uint64_t b = dkm0 + (((j % C::STAGES) * C::SLOT) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < kStep / 16; ++kk)   // dQ += dS K (A = dS in TMEM over dP_t)
+            mma_bf16_ts(tmem + C::DQ_COL + t * D, tmem + t * 128 + 64 + kk * 8,
+                        b + ((kk * 16 * 128) >> 4), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+      };
+      auto wait_kv = [&](int j) {
+        mbar_wait(&kv_full[j % C::STAGES], (j / C::STAGES) & 1);
+        tc_fence_after();
+      };
+      wait_kv(0);
       for (int t = 0; t < 2; ++t)
-        if (active[t]) issue_sdp(t, 0);
+        if (active[t]) {
+          issue_s(t, 0);
+          issue_dp(t, 0);
+        }
       for (int j = 0; j < nt; ++j) {
-        const int s = j % C::STAGES;
-        const uint32_t kb = smem_u32(sKV + s * C::SLOT);
-        bool next_ready = false;
+        if (j + 1 < nt) {
+          wait_kv(j + 1);
+          for (int t = 0; t < 2; ++t) {
+            if (!active[t]) continue;
+            mbar_wait(&s_read[t], j & 1);
+            tc_fence_after();
+            issue_s(t, j + 1);
+          }
+        }
         for (int t = 0; t < 2; ++t) {
           if (!active[t]) continue;
           mbar_wait(&ds_full[t], j & 1);
           tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kStep / 16; ++kk)   // dQ += dS K
-            mma_bf16_ts(tmem + C::DQ_COL + t * D, tmem + t * 128 + kk * 8,
-                        umma_desc_sw128(kb + kk * 16 * 128, kStep * 128, 1024), idQ,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-          if (j + 1 < nt) {
-            if (!next_ready) {
-              const int s1 = (j + 1) % C::STAGES;
-              mbar_wait(&kv_full[s1], ((j + 1) / C::STAGES) & 1);
-              tc_fence_after();
-              next_ready = true;
-            }
-            issue_sdp(t, j + 1);
-          }
+          issue_dq(t, j);
+          if (j + 1 < nt) issue_dp(t, j + 1);
         }
-        mma_commit(&kv_empty[s]);
+        if (elect_one()) mma_commit(&kv_empty[j % C::STAGES]);
+        __syncwarp();
       }
-      mma_commit(dq_done);
+      if (elect_one()) mma_commit(dq_done);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------ softmax (query row per thread)
@@ -434,27 +472,41 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const size_t prow = (size_t)qh[t] * p.rows_pad + row;
       const float lrow = p.Lp[prow], drow = p.Dp[prow];
       for (int j = 0; j < nt; ++j) {
+        const int nvalid = min(kStep, p.rows_kv - (kv_t0 + j) * kStep);
+        // phase A: P = exp2(S*c - Lp) as soon as S_t(j) lands; S_t is then free
         mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
-        const int nvalid = min(kStep, p.rows_kv - (kv_t0 + j) * kStep);
+        float pv[64];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t sv[32];
+          tmem_ld32(tl + t * 128 + hh * 32, sv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float x = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow));
+            pv[hh * 32 + e] = (hh * 32 + e < nvalid) ? x : 0.f;
+          }
+          if (hh == 1) {
+            tc_fence_before();
+            mbar_arrive(&s_read[t]);
+          }
+        }
+        // phase B: dS = P (dP - D), bf16 pairs over dP_t
+        mbar_wait(&dp_full[t], j & 1);
+        tc_fence_after();
         uint32_t dd[32];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          uint32_t sv[32], gv[32];
-          tmem_ld32(tl + t * 128 + hh * 32, sv);
+          uint32_t gv[32];
           tmem_ld32(tl + t * 128 + 64 + hh * 32, gv);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int c = hh * 32 + e;
-            const float p0 = c < nvalid ? ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow)) : 0.f;
-            const float p1 =
-                c + 1 < nvalid ? ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lrow)) : 0.f;
-            dd[hh * 16 + e / 2] =
-                pack_bf16(p0 * (__uint_as_float(gv[e]) - drow), p1 * (__uint_as_float(gv[e + 1]) - drow));
-          }
+          for (int e = 0; e < 32; e += 2)
+            dd[hh * 16 + e / 2] = pack_bf16(pv[hh * 32 + e] * (__uint_as_float(gv[e]) - drow),
+                                            pv[hh * 32 + e + 1] * (__uint_as_float(gv[e + 1]) - drow));
         }
-        tmem_st32(tl + t * 128, dd);   // dS over S
+        tmem_st32(tl + t * 128 + 64, dd);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&ds_full[t]);

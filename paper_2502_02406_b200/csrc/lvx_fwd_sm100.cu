@@ -149,41 +149,55 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     // tcgen05.mma executes in issue order, so QK_t(j+1) overwrites S_t/P_t only
     // after PV_t(j) has consumed P_t, and the s_full commit after QK_t(j)
     // also certifies that PV_t(j-1) is complete (O_t stable for a rescale).
-    if (lane == 0) {
+    // The whole warp runs the schedule (waits are warp-wide); one elected lane
+    // issues.  Descriptors are built once per tile and advanced by adding the
+    // byte offset >> 4 to the low word.
+    {
       constexpr uint32_t idQK = idesc_bf16(kBM, kBN, false, false);
       constexpr uint32_t idPV = idesc_bf16(kBM, D, false, true);
+      const uint64_t dq0 = umma_desc_sw128(smem_u32(sQ), 0, 1024);
+      const uint64_t dkv0 = umma_desc_sw128(smem_u32(sKV), 0, 1024);
+      const uint64_t dv0 = umma_desc_sw128(smem_u32(sKV), kBN * 128, 1024);
       auto slot_of = [&](int L) { return L % C::STAGES; };
       auto wait_load = [&](int L) {
         mbar_wait(&kv_full[slot_of(L)], (L / C::STAGES) & 1);
         tc_fence_after();
       };
       auto issue_qk = [&](int t, int j) {
-        const uint32_t kb = smem_u32(sKV + slot_of(2 * j) * C::KV_BYTES);
-        const uint32_t qb = smem_u32(sQ + t * C::Q_BYTES);
+        if (elect_one()) {
+          const uint64_t a = dq0 + ((t * C::Q_BYTES) >> 4);
+          const uint64_t b = dkv0 + ((slot_of(2 * j) * C::KV_BYTES) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (kBM * 128) + (kk & 3) * 32;
-          mma_bf16_ss(tmem + C::S_COL0 + t * kBN, umma_desc_sw128(qb + off, 0, 1024),
-                      umma_desc_sw128(kb + (kk >> 2) * (kBN * 128) + (kk & 3) * 32, 0, 1024),
-                      idQK, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ao = ((kk >> 2) * (kBM * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t bo = ((kk >> 2) * (kBN * 128) + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + C::S_COL0 + t * kBN, a + ao, b + bo, idQK, kk > 0);
+          }
+          mma_commit(&s_full[t]);
         }
-        mma_commit(&s_full[t]);
+        __syncwarp();
       };
       auto issue_pv = [&](int t, int j) {
-        const uint32_t vb = smem_u32(sKV + slot_of(2 * j + 1) * C::KV_BYTES);
+        if (elect_one()) {
+          const uint64_t b = dv0 + ((slot_of(2 * j + 1) * C::KV_BYTES) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
-          mma_bf16_ts(tmem + C::O_COL0 + t * D, tmem + C::S_COL0 + t * kBN + kk * 8,
-                      umma_desc_sw128(vb + kk * 16 * 128, kBN * 128, 1024), idPV,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&o_done[t]);
+          for (int kk = 0; kk < kBN / 16; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
+            mma_bf16_ts(tmem + C::O_COL0 + t * D, tmem + C::S_COL0 + t * kBN + kk * 8,
+                        b + ((kk * 16 * 128) >> 4), idPV, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&o_done[t]);
+        }
+        __syncwarp();
+      };
+      auto release = [&](int L) {
+        if (elect_one()) mma_commit(&kv_empty[slot_of(L)]);
+        __syncwarp();
       };
       mbar_wait(q_full, 0);
       tc_fence_after();
       wait_load(0);
       for (int t = 0; t < 2; ++t)
         if (active[t]) issue_qk(t, 0);
-      mma_commit(&kv_empty[slot_of(0)]);            // K_0 consumed
+      release(0);                                   // K_0 consumed
       for (int j = 0; j < nt; ++j) {
         wait_load(2 * j + 1);                       // V_j
         if (j + 1 < nt) wait_load(2 * j + 2);       // K_{j+1}
@@ -194,8 +208,8 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
           issue_pv(t, j);
           if (j + 1 < nt) issue_qk(t, j + 1);
         }
-        mma_commit(&kv_empty[slot_of(2 * j + 1)]);  // V_j consumed
-        if (j + 1 < nt) mma_commit(&kv_empty[slot_of(2 * j + 2)]);   // K_{j+1} consumed
+        release(2 * j + 1);                         // V_j consumed
+        if (j + 1 < nt) release(2 * j + 2);         // K_{j+1} consumed
       }
     }
   } else {

@@ -13,6 +13,16 @@
 namespace lvx {
 namespace sm100 {
 
+// one lane of a converged warp; MMA issue and commit go through this so the
+// descriptor math stays in uniform registers (no per-MMA R2UR / ELECT loops)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
