@@ -227,6 +227,10 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         dp[c] = e.x; dp[c + 1] = e.y; dp[c + 2] = e.z; dp[c + 3] = e.w;
       }
       tmem_wait_ld();
+      // both warpgroups must have read S^T / dP^T before either packs its
+      // bf16 half over them: warpgroup 1's packed columns [16, 32) lie inside
+      // warpgroup 0's input columns [0, 32) (the same TMEM lanes)
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       uint32_t pp[16], dd[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {

@@ -192,3 +192,26 @@ def test_tc_backward_large_vs_torch_fp32():
             for a, b in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad))]
     print(f"\nTC bwd C2-round/16: dQ {errs[0]:.2e} dK {errs[1]:.2e} dV {errs[2]:.2e}")
     assert max(errs) <= TOL_BF16
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 200, 1000, 128), (8, 2, 130, 700, 64), (32, 8, 256, 2048, 128)])
+def test_tc_kernels_bit_deterministic(shape):
+    """No atomics anywhere: repeated launches must be bit-identical.  Doubles
+    as a race detector for the warp-specialised pipelines (a TMEM/SMEM hazard
+    shows up as run-to-run differences)."""
+    import paper_2502_02406_b200 as lvx
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(hq, hkv, sq, skv, d, seed=77)
+    O, L = orc.dense_attention(Q, K, V)
+    D = orc.attention_row_stats(O, G)
+    Lt, Dt = torch.from_numpy(L).float().cuda(), torch.from_numpy(D).float().cuda()
+    base = None
+    for _ in range(12):
+        st = lvx.blockwise_attention(q, k, v)
+        grads = lvx.blockwise_attention_backward(q, k, v, Lt, Dt, g)
+        cur = [st.O.clone(), st.L.clone()] + [t.clone() for t in grads]
+        if base is None:
+            base = cur
+        else:
+            for a, b in zip(cur, base):
+                assert torch.equal(a, b)
