@@ -260,6 +260,8 @@ def simulate(strategy: str, Q, K, V, dO=None, n: int = 1, scale=None, tile_rows:
     the destination rank, so round semantics are identical to the threaded
     reference (strategies.py:193-231 lvx fwd, :243-276 lvx bwd, :287-311 ring
     fwd, :322-361 ring bwd)."""
+    if strategy == "head":
+        return _simulate_head(Q, K, V, dO, n, scale)
     if strategy not in ("lvx", "ring"):
         raise ValueError(f"unknown strategy {strategy!r}")
     h, sq, d = Q.shape
@@ -362,6 +364,34 @@ def simulate(strategy: str, Q, K, V, dO=None, n: int = 1, scale=None, tile_rows:
         res.dK = np.concatenate([home[i][0] for i in range(n)], axis=1)
         res.dV = np.concatenate([home[i][1] for i in range(n)], axis=1)
     res.bwd_bytes = bwd_b
+    return res
+
+
+def _simulate_head(Q, K, V, dO, n, scale):
+    """Head parallelism (strategies.py:364-432): every rank attends over the
+    full sequence for h/n heads; results equal the dense oracle.  Bytes are
+    the per-message payloads of the two all-to-alls per pass, src != dst."""
+    h, sq, d = Q.shape
+    hk = K.shape[0]
+    if h % n or hk % n:
+        raise ValueError(f"head count {h} not divisible by workers {n}")
+    dt = np.result_type(Q, K, V)
+    b = np.dtype(dt).itemsize
+    qs = [b_ - a for a, b_ in partition_rows(sq, n)]
+    ks = [b_ - a for a, b_ in partition_rows(K.shape[1], n)]
+    O, L = dense_attention(Q, K, V, scale)
+    fwd = [(n - 1) * (qs[i] * h + 2 * ks[i] * hk) // n * d * b +
+           sum(qs[w] for w in range(n) if w != i) * (h // n) * (d + 1) * b for i in range(n)]
+    if n == 1:
+        fwd = [0]
+    res = SimResult(O=O.astype(dt), L=L.astype(dt), fwd_bytes=fwd, fwd_rounds=1)
+    if dO is None:
+        return res
+    dq, dk, dv = dense_attention_backward(Q, K, V, O, L, dO, scale)
+    res.dQ, res.dK, res.dV = dq, dk, dv
+    res.bwd_bytes = [0] if n == 1 else [
+        ((n - 1) * qs[i] * h // n + sum(qs[w] * h + 2 * ks[w] * hk for w in range(n) if w != i)
+         // n) * d * b for i in range(n)]
     return res
 
 

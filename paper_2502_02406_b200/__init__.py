@@ -13,6 +13,7 @@ from .kernels import (AttentionState, GradientBundle, attention_row_stats, block
                       dense_attention_backward, empty_state, merge_states, project,
                       project_backward, validate_qkv)
 from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, StrategyKind,
+                         head_parallel_backward, head_parallel_forward,
                          lvx_backward, lvx_forward, partition_rows, ring_backward, ring_forward,
                          run_distributed, run_rank)
 from . import volumes

@@ -200,3 +200,33 @@ class DeviceContext:
         works = dist.batch_isend_irecv(ops) if ops else []
         self.stats.record(self.rank, self.successor, payload_nbytes(send))
         return _Shift(works), sent
+
+    def all_to_all(self, chunks: list, recv: list, classes: list | None = None):
+        """Deliver ``chunks[w]`` (a list of tensors) to rank w and receive
+        ``recv[w]`` (preallocated, same structure) from rank w
+        (cluster.py:274-291).  The self chunk is copied locally and never
+        touches the transport; bytes are counted per destination for w != rank.
+        Returns (handle, sent bytes by class)."""
+        if len(chunks) != self.n or len(recv) != self.n:
+            raise ClusterError(f"worker {self.rank}: all_to_all expects {self.n} chunks, "
+                               f"got {len(chunks)}")
+        classes = classes or [str(k) for k in range(len(chunks[0]))]
+        sent = {c: 0 for c in classes}
+        ops, local = [], list(zip(chunks[self.rank], recv[self.rank]))
+        for w in range(self.n):
+            if w == self.rank:
+                continue
+            nb = payload_nbytes(chunks[w])
+            for c, t in zip(classes, chunks[w]):
+                sent[c] += t.numel() * t.element_size()
+            if self.comm_enabled:
+                peer = self._global[w]
+                for t in chunks[w]:
+                    if t.numel():
+                        ops.append(dist.P2POp(dist.isend, t.contiguous(), peer, self.group))
+                for t in recv[w]:
+                    if t.numel():
+                        ops.append(dist.P2POp(dist.irecv, t, peer, self.group))
+                self.stats.record(self.rank, w, nb)
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return _Shift(works, local), sent

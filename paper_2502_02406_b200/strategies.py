@@ -491,6 +491,125 @@ def ring_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_blo
 
 
 # ---------------------------------------------------------------------------
+# Head parallelism (DeepSpeed-Ulysses style), the reference's third strategy
+# ---------------------------------------------------------------------------
+
+def _check_heads(h: int, hk: int, n: int) -> None:
+    if h % n != 0:
+        raise ValueError(f"head count {h} not divisible by workers {n}")
+    if hk % n != 0:
+        raise ValueError(f"kv head count {hk} not divisible by workers {n}")
+
+
+def head_parallel_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
+                          scale: float, tile_rows: int = DEFAULT_TILE_ROWS,
+                          trace: RoundTrace | None = None):
+    """All-to-all from sequence sharding to head sharding, local attention on
+    the owned heads over the full sequence, all-to-all back
+    (strategies.py:364-400).  Requires hq and hkv divisible by n (GQA keeps
+    whole groups together).  Returns (own state, saved for backward)."""
+    n, i, ops = ctx.n, ctx.rank, ctx.ops
+    h, _, d = q_block.shape
+    hk = k_block.shape[0]
+    _check_heads(h, hk, n)
+    hpw, kpw = h // n, hk // n
+    dev = q_block.device
+    sd = ops.state_dtype(q_block.dtype)
+    qs, ks = shards.q_sizes, shards.kv_sizes
+    s_q, s_kv = sum(qs), sum(ks)
+    q_full = torch.empty((hpw, s_q, d), dtype=q_block.dtype, device=dev)
+    k_full = torch.empty((kpw, s_kv, d), dtype=k_block.dtype, device=dev)
+    v_full = torch.empty((kpw, s_kv, d), dtype=v_block.dtype, device=dev)
+    chunks = [[q_block[w * hpw:(w + 1) * hpw].contiguous(),
+               k_block[w * kpw:(w + 1) * kpw].contiguous(),
+               v_block[w * kpw:(w + 1) * kpw].contiguous()] for w in range(n)]
+    recv = [[torch.empty((hpw, qs[w], d), dtype=q_block.dtype, device=dev),
+             torch.empty((kpw, ks[w], d), dtype=k_block.dtype, device=dev),
+             torch.empty((kpw, ks[w], d), dtype=v_block.dtype, device=dev)] for w in range(n)]
+    t0 = ops.event() if trace is not None else None
+    hop, g_sent = ctx.all_to_all(chunks, recv, ["Q", "K", "V"])
+    hop.wait()
+    for w in range(n):
+        (qa, qb), (ka, kb) = shards.q_ranges[w], shards.kv_ranges[w]
+        q_full[:, qa:qb].copy_(recv[w][0])
+        k_full[:, ka:kb].copy_(recv[w][1])
+        v_full[:, ka:kb].copy_(recv[w][2])
+    t1 = ops.event() if trace is not None else None
+    O = torch.empty((hpw, s_q, d), dtype=sd, device=dev)
+    L = torch.empty((hpw, s_q), dtype=sd, device=dev)
+    if s_kv == 0:
+        ops.fill_empty(O, L)
+    else:
+        ws = ops.fwd_workspace(q_full, k_full)
+        ops.fwd_partial(q_full, k_full, v_full, scale, ws)
+        ops.fwd_finish(q_full, k_full, ws, O, L)
+    t2 = ops.event() if trace is not None else None
+    out_chunks = [[O[:, qa:qb].contiguous(), L[:, qa:qb].contiguous()]
+                  for qa, qb in shards.q_ranges]
+    back = [[torch.empty((hpw, qs[i], d), dtype=sd, device=dev),
+             torch.empty((hpw, qs[i]), dtype=sd, device=dev)] for _ in range(n)]
+    hop, s_sent = ctx.all_to_all(out_chunks, back, ["O", "L"])
+    hop.wait()
+    o_i = torch.cat([b[0] for b in back], dim=0)
+    l_i = torch.cat([b[1] for b in back], dim=0)
+    if trace is not None:
+        t3 = ops.event()
+        trace._add_timed(ops, t1, t2, t3, {"QKV_gather": sum(g_sent.values()),
+                                           "OL_scatter": sum(s_sent.values())})
+        trace.section("fwd_kernel", ops, t1, t2)
+        trace.section("all_to_all", ops, t0, t1)
+    return AttentionState(O=o_i, L=l_i), (q_full, k_full, v_full, AttentionState(O=O, L=L))
+
+
+def head_parallel_backward(ctx: DeviceContext, shards: ShardSpec, saved, do_block, scale: float,
+                           trace: RoundTrace | None = None):
+    """Mirror of the forward: all-to-all dO to head sharding, local backward on
+    the owned heads, all-to-all dQ/dK/dV back (strategies.py:403-432)."""
+    n, i, ops = ctx.n, ctx.rank, ctx.ops
+    q_full, k_full, v_full, st = saved
+    hpw, s_q, d = q_full.shape
+    kpw, s_kv, _ = k_full.shape
+    dev = q_full.device
+    sd = ops.state_dtype(q_full.dtype)
+    qs, ks = shards.q_sizes, shards.kv_sizes
+    chunks = [[do_block[w * hpw:(w + 1) * hpw].contiguous()] for w in range(n)]
+    recv = [[torch.empty((hpw, qs[w], d), dtype=do_block.dtype, device=dev)] for w in range(n)]
+    t0 = ops.event() if trace is not None else None
+    hop, g_sent = ctx.all_to_all(chunks, recv, ["dO"])
+    hop.wait()
+    do_full = torch.empty((hpw, s_q, d), dtype=do_block.dtype, device=dev)
+    for w in range(n):
+        qa, qb = shards.q_ranges[w]
+        do_full[:, qa:qb].copy_(recv[w][0])
+    t1 = ops.event() if trace is not None else None
+    D = torch.empty((hpw, s_q), dtype=sd, device=dev)
+    ops.row_stats(st.O, do_full, D)
+    dq = torch.empty((hpw, s_q, d), dtype=sd, device=dev)
+    dk = torch.empty((kpw, s_kv, d), dtype=sd, device=dev)
+    dv = torch.empty((kpw, s_kv, d), dtype=sd, device=dev)
+    ws = ops.bwd_workspace(q_full, k_full)
+    ops.bwd_dq_partial(q_full, k_full, v_full, st.L, D, do_full, scale, ws)
+    ops.bwd_dq_finish(q_full, k_full, ws, dq, accumulate=False)
+    ops.bwd_dkv(q_full, k_full, v_full, st.L, D, do_full, scale, dk, dv, accumulate=False)
+    t2 = ops.event() if trace is not None else None
+    out = [[dq[:, qa:qb].contiguous(), dk[:, ka:kb].contiguous(), dv[:, ka:kb].contiguous()]
+           for (qa, qb), (ka, kb) in zip(shards.q_ranges, shards.kv_ranges)]
+    back = [[torch.empty((hpw, qs[i], d), dtype=sd, device=dev),
+             torch.empty((kpw, ks[i], d), dtype=sd, device=dev),
+             torch.empty((kpw, ks[i], d), dtype=sd, device=dev)] for _ in range(n)]
+    hop, s_sent = ctx.all_to_all(out, back, ["dQ", "dK", "dV"])
+    hop.wait()
+    if trace is not None:
+        t3 = ops.event()
+        trace._add_timed(ops, t1, t2, t3, {"dO_gather": sum(g_sent.values()),
+                                           "grad_scatter": sum(s_sent.values())})
+        trace.section("bwd_kernel", ops, t1, t2)
+        trace.section("all_to_all", ops, t0, t1)
+    return (torch.cat([b[0] for b in back], dim=0), torch.cat([b[1] for b in back], dim=0),
+            torch.cat([b[2] for b in back], dim=0))
+
+
+# ---------------------------------------------------------------------------
 # driver — strategies.py:435-551
 # ---------------------------------------------------------------------------
 
@@ -520,18 +639,21 @@ def run_rank(strategy: str, ctx: DeviceContext, shards: ShardSpec, q_i, k_i, v_i
     tf = RoundTrace(strategy=strategy.value, phase="forward") if trace else None
     tb = RoundTrace(strategy=strategy.value, phase="backward") if (trace and do_i is not None) \
         else None
+    saved = None
     if strategy in (StrategyKind.LVX, StrategyKind.SINGLE):
         st = lvx_forward(ctx, shards, q_i, k_i, v_i, scale, tile_rows, tf)
     elif strategy is StrategyKind.RING:
         st = ring_forward(ctx, shards, q_i, k_i, v_i, scale, tile_rows, tf)
     else:
-        raise NotImplementedError("head-parallel (Ulysses) is the next row of SURVEY.md §8(f)")
+        st, saved = head_parallel_forward(ctx, shards, q_i, k_i, v_i, scale, tile_rows, tf)
     grads = None
     if do_i is not None:
         if strategy in (StrategyKind.LVX, StrategyKind.SINGLE):
             grads = lvx_backward(ctx, shards, q_i, k_i, v_i, st, do_i, scale, tb)
-        else:
+        elif strategy is StrategyKind.RING:
             grads = ring_backward(ctx, shards, q_i, k_i, v_i, st, do_i, scale, tb)
+        else:
+            grads = head_parallel_backward(ctx, shards, saved, do_i, scale, tb)
     return st, grads, tf, tb
 
 
@@ -579,9 +701,7 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
     if strategy is StrategyKind.SINGLE and n != 1:
         raise ValueError("single-worker strategy requires n=1")
     if strategy is StrategyKind.HEAD_PARALLEL:
-        if h % n != 0:
-            raise ValueError(f"head count {h} not divisible by workers {n}")
-        raise NotImplementedError("head-parallel (Ulysses) is the next row of SURVEY.md §8(f)")
+        _check_heads(h, K.shape[0], n)
     shards = ShardSpec.balanced(s_q, s_kv, n)
 
     (Qt, kind), (Kt, _), (Vt, _) = _to_torch(Q), _to_torch(K), _to_torch(V)

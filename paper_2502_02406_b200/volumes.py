@@ -98,8 +98,41 @@ def ring_backward_bytes_by_worker(kv_sizes, w: Wire) -> list[int]:
             _rows_bytes(w, ("dK", "dV"), kv_sizes[(i + 1) % n]) for i in range(n)]
 
 
+def head_parallel_forward_bytes_by_worker(q_sizes, kv_sizes, w: Wire) -> list[int]:
+    """Gather (Q, K, V head chunks of the own rows) to n-1 ranks, scatter
+    (O, L) rows back (volumes.py:123-137); hq, hkv divisible by n."""
+    n = len(q_sizes)
+    if n == 1:
+        return [0]
+    out = []
+    for i in range(n):
+        gather = (n - 1) * (q_sizes[i] * w.row_bytes("Q") +
+                            kv_sizes[i] * (w.row_bytes("K") + w.row_bytes("V"))) // n
+        scatter = sum(q_sizes[x] for x in range(n) if x != i) * \
+            (w.row_bytes("O") + w.row_bytes("L")) // n
+        out.append(gather + scatter)
+    return out
+
+
+def head_parallel_backward_bytes_by_worker(q_sizes, kv_sizes, w: Wire) -> list[int]:
+    """Gather dO head chunks, scatter (dQ, dK, dV) rows (volumes.py:140-152)."""
+    n = len(q_sizes)
+    if n == 1:
+        return [0]
+    out = []
+    for i in range(n):
+        gather = (n - 1) * q_sizes[i] * w.row_bytes("dO") // n
+        scatter = sum(q_sizes[x] * w.row_bytes("dQ") +
+                      kv_sizes[x] * (w.row_bytes("dK") + w.row_bytes("dV"))
+                      for x in range(n) if x != i) // n
+        out.append(gather + scatter)
+    return out
+
+
 def bytes_by_worker(strategy: str, phase: str, q_sizes, kv_sizes, w: Wire) -> list[int]:
-    fn = {("lvx", "forward"): lambda: lvx_forward_bytes_by_worker(q_sizes, w),
+    fn = {("head", "forward"): lambda: head_parallel_forward_bytes_by_worker(q_sizes, kv_sizes, w),
+          ("head", "backward"): lambda: head_parallel_backward_bytes_by_worker(q_sizes, kv_sizes, w),
+          ("lvx", "forward"): lambda: lvx_forward_bytes_by_worker(q_sizes, w),
           ("lvx", "backward"): lambda: lvx_backward_bytes_by_worker(q_sizes, w),
           ("ring", "forward"): lambda: ring_forward_bytes_by_worker(kv_sizes, w),
           ("ring", "backward"): lambda: ring_backward_bytes_by_worker(kv_sizes, w)}

@@ -77,7 +77,9 @@ def main() -> None:
         Q, Kt, V, dO = qkv(h, sq, skv, d, seed)
         for dt in (np.float64, np.float32):
             q, k, v, g = (t.astype(dt) for t in (Q, Kt, V, dO))
-            for s in ("lvx", "ring"):
+            for s in ("lvx", "ring", "head"):
+                if s == "head" and h % n:
+                    continue
                 tag = f"s{ci}_{s}_{np.dtype(dt).name}"
                 res = run_distributed(s, q, k, v, dO=g, spec=ClusterSpec(n))
                 strat.update({

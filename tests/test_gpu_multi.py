@@ -73,3 +73,27 @@ def test_bf16_lvx_and_ring_world2_vs_oracle():
             lvx.volumes.bytes_by_worker(strategy, "forward", qs, ks, w)
         assert [t.total_sent_bytes() for t in res.traces_backward] == \
             lvx.volumes.bytes_by_worker(strategy, "backward", qs, ks, w)
+
+
+def test_head_parallel_bf16_world_vs_oracle():
+    """Ulysses head parallelism (§8(f) next 1) through NCCL all-to-all."""
+    import paper_2502_02406_b200 as lvx
+    n = min(torch.cuda.device_count(), 4)
+    hq, hkv, sq, skv, d = 8, 4, 200, 3000, 128
+    Q, K, V, G = orc.make_inputs(sq, skv, hq, d, seed=52, hkv=hkv)
+    q, k, v, g = (torch.from_numpy(t).to(torch.bfloat16) for t in (Q, K, V, G))
+    Qr, Kr, Vr, Gr = (t.double().numpy() for t in (q, k, v, g))
+    O, L = orc.dense_attention(Qr, Kr, Vr)
+    rq, rk, rv = orc.dense_attention_backward(Qr, Kr, Vr, O, L, Gr)
+    res = lvx.run_distributed("head", q, k, v, dO=g, spec=lvx.ClusterSpec(n))
+    errs = {nm: orc.max_norm_error(a.float().numpy(), b) for nm, a, b in
+            (("O", res.O, O), ("L", res.L, L), ("dQ", res.grads.dQ, rq),
+             ("dK", res.grads.dK, rk), ("dV", res.grads.dV, rv))}
+    print(f"\nhead bf16 n={n}:", errs)
+    assert max(errs.values()) <= 1e-2
+    w = lvx.volumes.Wire.b200(hq, hkv, d, 2)
+    qs, ks = res.shards.q_sizes, res.shards.kv_sizes
+    assert [t.total_sent_bytes() for t in res.traces_forward] == \
+        lvx.volumes.bytes_by_worker("head", "forward", qs, ks, w)
+    assert [t.total_sent_bytes() for t in res.traces_backward] == \
+        lvx.volumes.bytes_by_worker("head", "backward", qs, ks, w)
