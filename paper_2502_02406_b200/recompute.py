@@ -90,9 +90,11 @@ class SavedCA:
 
 
 def _heads(flat: torch.Tensor, heads: int) -> torch.Tensor:
-    """[S, heads*d] -> [heads, S, d] contiguous (``src/kernels.py:236-240``)."""
+    """[S, heads*d] -> [heads, S, d] as a zero-copy strided view
+    (``src/kernels.py:236-240`` reshapes and copies): the tensor-core kernels
+    take any 16-byte-multiple head/row strides through their TMA maps."""
     s = flat.shape[0]
-    return flat.view(s, heads, -1).transpose(0, 1).contiguous()
+    return flat.view(s, heads, -1).transpose(0, 1)
 
 
 def _flat(t: torch.Tensor) -> torch.Tensor:
