@@ -63,19 +63,32 @@ struct BwdParams {
   int64_t dk_hs, dk_rs, dv_hs, dv_rs;
   int accumulate;
   float* ws_dq;       // [splits][hq][rows_q][D]
+  int debug;          // LVX_BWD_DEBUG (profiling only): 1 = skip exp / dS math
 };
 
 // ============================================================ dK / dV kernel
+// 128-row query steps so every SS MMA has N = 128 (A 4 KB + B 4 KB per 64
+// clk = the 128 B/clk SMEM read rate; 64-row steps re-read the 128-row A
+// operand twice as often and capped the kernel at ~80 % of peak).  TMEM:
+//   R1 [0,128)    S^T(i), then P^T(i) packed bf16 in its first 64 columns
+//   R2 [128,256)  dP^T(i), then dS^T(i) packed bf16
+//   dV [256, 256+D), dK [256+D, 256+2D)
+// Two-phase softmax per step: phase A turns S^T into P^T (the exponentials)
+// and releases dV(i) and S^T(i+1); phase B turns dP^T into dS^T while the
+// tensor pipe runs dV(i) / S^T(i+1), then releases dK(i) and dP^T(i+1).
+// P stays packed in registers between the phases (R1 is overwritten by
+// S^T(i+1) as soon as dV(i) has read it).  Two softmax warpgroups split the
+// 128 query columns; both read before either packs over the shared lanes.
 template <int D>
 struct DkvCfg {
   static constexpr int PANELS = D / 64;
   static constexpr int KV_BYTES = 128 * D * 2;             // resident K (or V) tile
-  static constexpr int QT_BYTES = kStep * D * 2;           // one Q (or dO) step tile
-  static constexpr int SLOT = ((2 * QT_BYTES + 512 + 1023) / 1024) * 1024;
-  static constexpr int STAGES = D == 128 ? 4 : 6;
-  static constexpr int NBAR = 1 + 2 * STAGES + 2 + 2 + 1;
+  static constexpr int QT_BYTES = 128 * D * 2;             // one Q (or dO) 128-row step tile
+  static constexpr int SLOT = ((2 * QT_BYTES + 1024 + 1023) / 1024) * 1024;
+  static constexpr int STAGES = D == 128 ? 2 : 4;
+  static constexpr int NBAR = 1 + 2 * STAGES + 5;
   static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
-  static constexpr int DV_COL = 256, DK_COL = 256 + D;
+  static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
 };
 
 template <int D>
@@ -94,14 +107,16 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   uint64_t* kv_full = bars;
   uint64_t* qd_full = bars + 1;
   uint64_t* qd_empty = qd_full + C::STAGES;
-  uint64_t* st_full = qd_empty + C::STAGES;   // [2]
-  uint64_t* pds_full = st_full + 2;           // [2]
-  uint64_t* dkv_done = pds_full + 2;
+  uint64_t* s_full = qd_empty + C::STAGES;    // S^T(i) in R1
+  uint64_t* p_ready = s_full + 1;             // P^T(i) packed in R1 (256 arrivals)
+  uint64_t* dp_full = p_ready + 1;            // dP^T(i) in R2
+  uint64_t* ds_ready = dp_full + 1;           // dS^T(i) packed in R2 (256 arrivals)
+  uint64_t* dkv_done = ds_ready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * 128, g = blockIdx.y;
-  const int nsteps = p.G * p.tq64;
+  const int nsteps = p.G * p.tpq;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -109,10 +124,10 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&st_full[b], 1);
-      mbar_init(&pds_full[b], 256);
-    }
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 256);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 256);
     mbar_init(dkv_done, 1);
     fence_barrier_init();
   }
@@ -137,120 +152,152 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       for (int i = 0; i < nsteps; ++i) {
         const int s = i % C::STAGES, u = i / C::STAGES;
         if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
-        const int h = g * p.G + i / p.tq64, r0 = (i % p.tq64) * kStep;
+        const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
         uint8_t* slot = sSlot + s * C::SLOT;
-        mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 512);
+        mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 1024);
         for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_3d(slot + pn * kStep * 128, &tmQ, &qd_full[s], pn * 64, r0, h);
-          tma_load_3d(slot + C::QT_BYTES + pn * kStep * 128, &tmG, &qd_full[s], pn * 64, r0, h);
+          tma_load_3d(slot + pn * 128 * 128, &tmQ, &qd_full[s], pn * 64, r0, h);
+          tma_load_3d(slot + C::QT_BYTES + pn * 128 * 128, &tmG, &qd_full[s], pn * 64, r0, h);
         }
         const size_t off = (size_t)h * p.rows_pad + r0;
-        bulk_load(slot + 2 * C::QT_BYTES, p.Lp + off, 256, &qd_full[s]);
-        bulk_load(slot + 2 * C::QT_BYTES + 256, p.Dp + off, 256, &qd_full[s]);
+        bulk_load(slot + 2 * C::QT_BYTES, p.Lp + off, 512, &qd_full[s]);
+        bulk_load(slot + 2 * C::QT_BYTES + 512, p.Dp + off, 512, &qd_full[s]);
       }
     }
   } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    {   // converged warp; one elected lane issues (see lvx_fwd_sm100.cu)
-      constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
-      constexpr uint32_t idKV = idesc_bf16(128, D, false, true);
-      const uint64_t dk0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
-      const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
-      const uint64_t ds0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);            // K-major Q / dO
-      const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), kStep * 128, 1024);  // MN-major Q / dO
-      mbar_wait(kv_full, 0);
-      tc_fence_after();
-      for (int i = 0; i <= nsteps; ++i) {
-        if (i < nsteps) {
-          const int s = i % C::STAGES, b = i & 1;
-          mbar_wait(&qd_full[s], (i / C::STAGES) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t qd = ds0 + ((s * C::SLOT) >> 4), gd = qd + (C::QT_BYTES >> 4);
+    // ------------------------------------------- MMA issuer (converged warp)
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idKV = idesc_bf16(128, D, false, true);
+    const uint64_t dk0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
+    const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
+    const uint64_t ds0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);        // K-major Q / dO
+    const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), 128 * 128, 1024);  // MN-major Q / dO
+    auto qslot = [&](int i) { return (uint64_t)(((i % C::STAGES) * C::SLOT) >> 4); };
+    auto issue_st = [&](int i, uint64_t a0, uint32_t col, uint32_t xoff, uint64_t* bar) {
+      // col R1: S^T = K Q^T ; col R2: dP^T = V dO^T   (M=128 kv, N=128 q, K=D)
+      if (elect_one()) {
+        const uint64_t b = ds0 + qslot(i) + (xoff >> 4);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t ko = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
-              const uint32_t qo = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
-              mma_bf16_ss(tmem + b * 128, dk0 + ko, qd + qo, idS, kk > 0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t ko = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
-              const uint32_t qo = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
-              mma_bf16_ss(tmem + b * 128 + 64, dv0 + ko, gd + qo, idS, kk > 0);
-            }
-            mma_commit(&st_full[b]);
-          }
-          __syncwarp();
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t o = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+          mma_bf16_ss(tmem + col, a0 + o, b + o, idS, kk > 0);
         }
-        if (i > 0) {
-          const int ii = i - 1, s = ii % C::STAGES, b = ii & 1;
-          mbar_wait(&pds_full[b], (ii >> 1) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t qm = dm0 + ((s * C::SLOT) >> 4), gm = qm + (C::QT_BYTES >> 4);
-#pragma unroll
-            for (int kk = 0; kk < kStep / 16; ++kk)   // dV += P^T dO
-              mma_bf16_ts(tmem + C::DV_COL, tmem + b * 128 + kk * 8, gm + ((kk * 16 * 128) >> 4),
-                          idKV, (ii > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-            for (int kk = 0; kk < kStep / 16; ++kk)   // dK += dS^T Q
-              mma_bf16_ts(tmem + C::DK_COL, tmem + b * 128 + 64 + kk * 8,
-                          qm + ((kk * 16 * 128) >> 4), idKV, (ii > 0 || kk > 0) ? 1u : 0u);
-            mma_commit(&qd_empty[s]);
-          }
-          __syncwarp();
-        }
+        mma_commit(bar);
       }
-      if (elect_one()) mma_commit(dkv_done);
       __syncwarp();
+    };
+    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t xoff) {
+      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0)
+      if (elect_one()) {
+        const uint64_t b = dm0 + qslot(i) + (xoff >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          mma_bf16_ts(tmem + acc_col, tmem + a_col + kk * 8, b + ((kk * 16 * 128) >> 4), idKV,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    tc_fence_after();
+    mbar_wait(&qd_full[0], 0);
+    tc_fence_after();
+    issue_st(0, dk0, C::R1, 0, s_full);
+    issue_st(0, dv0, C::R2, C::QT_BYTES, dp_full);
+    for (int i = 0; i < nsteps; ++i) {
+      const uint32_t ph = i & 1;
+      mbar_wait(p_ready, ph);
+      tc_fence_after();
+      issue_acc(i, C::DV_COL, C::R1, C::QT_BYTES);            // dV(i)
+      if (i + 1 < nsteps) {
+        mbar_wait(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
+        tc_fence_after();
+        issue_st(i + 1, dk0, C::R1, 0, s_full);               // S^T(i+1) after dV(i) read R1
+      }
+      mbar_wait(ds_ready, ph);
+      tc_fence_after();
+      issue_acc(i, C::DK_COL, C::R2, 0);                      // dK(i)
+      if (elect_one()) mma_commit(&qd_empty[i % C::STAGES]);
+      __syncwarp();
+      if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::QT_BYTES, dp_full);   // dP^T(i+1)
     }
+    if (elect_one()) mma_commit(dkv_done);
+    __syncwarp();
   } else {
-    // ------------------------------- softmax: kv row per thread, 32 of the 64
-    // query columns per warpgroup (wg), so two warps share each TMEM lane quarter
-    const int wg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    // -------------- softmax: kv row per thread, 64 of the 128 query columns per wg
+    const int wg = warp >> 2, q4 = warp & 3;
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     for (int i = 0; i < nsteps; ++i) {
-      const int s = i % C::STAGES, b = i & 1;
-      mbar_wait(&st_full[b], (i >> 1) & 1);
+      const int s = i % C::STAGES;
+      const uint32_t ph = i & 1;
+      const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 256;
+      // phase A: P^T = exp2(S^T * c - Lp[q]), 32 columns at a time
+      mbar_wait(s_full, ph);
       tc_fence_after();
-      uint32_t sv[32], gv[32];
-      tmem_ld32(tl + b * 128 + wg * 32, sv);
-      tmem_ld32(tl + b * 128 + 64 + wg * 32, gv);
-      const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 128;
-      float lp[32], dp[32];
+      uint32_t pp[32];
 #pragma unroll
-      for (int c = 0; c < 32; c += 4) {
-        const float4 a = ld_shared_f4(lds + c * 4);
-        const float4 e = ld_shared_f4(lds + 256 + c * 4);
-        lp[c] = a.x; lp[c + 1] = a.y; lp[c + 2] = a.z; lp[c + 3] = a.w;
-        dp[c] = e.x; dp[c + 1] = e.y; dp[c + 2] = e.z; dp[c + 3] = e.w;
-      }
-      tmem_wait_ld();
-      // both warpgroups must have read S^T / dP^T before either packs its
-      // bf16 half over them: warpgroup 1's packed columns [16, 32) lie inside
-      // warpgroup 0's input columns [0, 32) (the same TMEM lanes)
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      uint32_t pp[16], dd[16];
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sv[32];
+        tmem_ld32(tl + C::R1 + wg * 64 + hh * 32, sv);
+        tmem_wait_ld();
+        if (p.debug == 1) {
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lp[e]));
-        const float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lp[e + 1]));
-        pp[e / 2] = pack_bf16(p0, p1);
-        dd[e / 2] = pack_bf16(p0 * (__uint_as_float(gv[e]) - dp[e]),
-                              p1 * (__uint_as_float(gv[e + 1]) - dp[e + 1]));
+          for (int e = 0; e < 16; ++e) pp[hh * 16 + e] = sv[2 * e];
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 32; c4 += 4) {
+            const float4 l4 = ld_shared_f4(lds + (hh * 32 + c4) * 4);
+            // phase A is MUFU-bound (16K exp2 per step): 1 in 4 on the FMA pipe
+            const float p0 = ex2(fmaf(__uint_as_float(sv[c4]), p.scale_log2, -l4.x));
+            const float p1 = ex2(fmaf(__uint_as_float(sv[c4 + 1]), p.scale_log2, -l4.y));
+            const float p2 = ex2(fmaf(__uint_as_float(sv[c4 + 2]), p.scale_log2, -l4.z));
+            const float p3 = ex2_poly(fmaf(__uint_as_float(sv[c4 + 3]), p.scale_log2, -l4.w));
+            pp[hh * 16 + c4 / 2] = pack_bf16(p0, p1);
+            pp[hh * 16 + c4 / 2 + 1] = pack_bf16(p2, p3);
+          }
+        }
       }
-      tmem_st16(tl + b * 128 + wg * 16, pp);        // P^T over S^T
-      tmem_st16(tl + b * 128 + 64 + wg * 16, dd);   // dS^T over dP^T
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // both wgs read R1 before packing
+      tmem_st32(tl + C::R1 + wg * 32, pp);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&pds_full[b]);
+      mbar_arrive(p_ready);
+      // phase B: dS^T = P^T (dP^T - D[q])
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      uint32_t dd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t gv[32];
+        tmem_ld32(tl + C::R2 + wg * 64 + hh * 32, gv);
+        tmem_wait_ld();
+        if (p.debug == 1) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 32; c4 += 4) {
+            const float4 d4 = ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);
+            const uint32_t a = pp[hh * 16 + c4 / 2], b = pp[hh * 16 + c4 / 2 + 1];
+            const float p0 = __uint_as_float(a << 16), p1 = __uint_as_float(a & 0xFFFF0000u);
+            const float p2 = __uint_as_float(b << 16), p3 = __uint_as_float(b & 0xFFFF0000u);
+            dd[hh * 16 + c4 / 2] = pack_bf16(p0 * (__uint_as_float(gv[c4]) - d4.x),
+                                             p1 * (__uint_as_float(gv[c4 + 1]) - d4.y));
+            dd[hh * 16 + c4 / 2 + 1] = pack_bf16(p2 * (__uint_as_float(gv[c4 + 2]) - d4.z),
+                                                 p3 * (__uint_as_float(gv[c4 + 3]) - d4.w));
+          }
+        }
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");   // both wgs read R2 before packing
+      tmem_st32(tl + C::R2 + wg * 32, dd);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_ready);
     }
     // epilogue: warpgroup 0 drains dV, warpgroup 1 drains scale * dK, into the
     // fp32 accumulators (one read-modify-write when accumulating)
     mbar_wait(dkv_done, 0);
     tc_fence_after();
-    const int row = n0 + r;
+    const int row = n0 + q4 * 32 + lane;
     const bool valid = row < p.rows_kv;
     const uint32_t col = wg ? C::DK_COL : C::DV_COL;
     const float mul = wg ? p.scale : 1.f;
@@ -285,16 +332,26 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 }
 
 // ================================================================ dQ kernel
+// Q-parallel, one 128-row query tile per CTA, split over the KV block in
+// 128-row steps.  Q and dO are copied once into TMEM so that all three MMAs
+// read A from TMEM (TS) and SMEM holds only a 3-stage K/V ring.  TMEM:
+//   [0,128) S(j)   [128,256) dP(j), then dS(j) packed bf16   [256,256+D) dQ
+//   [384,448) Q    [448,512) dO          (bf16 pairs; D = 128)
+// Two softmax warpgroups split the 128 kv columns of a step.  Phase A turns
+// S into P (kept packed in registers) and releases S(j+1); phase B turns dP
+// into dS over dP and releases dQ(j) -> dP(j+1) (tensor-pipe order).
 template <int D>
 struct DqCfg {
   static constexpr int PANELS = D / 64;
   static constexpr int Q_BYTES = 128 * D * 2;
-  static constexpr int KVT_BYTES = kStep * D * 2;
-  static constexpr int SLOT = 2 * KVT_BYTES;
+  static constexpr int KVT_BYTES = 128 * D * 2;
+  static constexpr int SLOT = 2 * KVT_BYTES;             // K | V, also Q | dO staging
   static constexpr int STAGES = D == 128 ? 3 : 6;
-  static constexpr int NBAR = 1 + 2 * STAGES + 8 + 1;
-  static constexpr int SMEM = 1024 + 4 * Q_BYTES + STAGES * SLOT + NBAR * 8 + 16;
-  static constexpr int DQ_COL = 256;
+  static constexpr int NBAR = 2 + 2 * STAGES + 6;
+  static constexpr int SMEM = 1024 + STAGES * SLOT + NBAR * 8 + 16;
+  static constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384,
+                       G_COL = 384 + D / 2;
+  static constexpr int QSLOT = STAGES - 1;                  // where Q / dO are staged
 };
 
 template <int D>
@@ -306,46 +363,36 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u = smem_u32(smem_raw);
   uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
-  uint8_t* sQ = sm;                       // [2] tiles
-  uint8_t* sG = sQ + 2 * C::Q_BYTES;      // [2] dO tiles
-  uint8_t* sKV = sG + 2 * C::Q_BYTES;     // STAGES x (K | V)
+  uint8_t* sKV = sm;                          // STAGES x (K | V)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::SLOT);
-  uint64_t* qd_full = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* qd_full = bars;                   // Q / dO staged in slot QSLOT
+  uint64_t* q_ready = bars + 1;               // Q / dO copied into TMEM (256)
+  uint64_t* kv_full = bars + 2;
   uint64_t* kv_empty = kv_full + C::STAGES;
-  uint64_t* s_full = kv_empty + C::STAGES;   // [2] S_t(j) in TMEM
-  uint64_t* s_read = s_full + 2;             // [2] softmax has read S_t(j)
-  uint64_t* dp_full = s_read + 2;            // [2] dP_t(j) in TMEM
-  uint64_t* ds_full = dp_full + 2;           // [2] dS_t(j) written over dP_t
-  uint64_t* dq_done = ds_full + 2;
+  uint64_t* s_full = kv_empty + C::STAGES;    // S(j) in TMEM
+  uint64_t* s_read = s_full + 1;              // softmax has read S(j) (256)
+  uint64_t* dp_full = s_read + 1;             // dP(j) in TMEM
+  uint64_t* ds_full = dp_full + 1;            // dS(j) packed over dP (256)
+  uint64_t* dq_done = ds_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
+  const int tt = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
   const int kv_t0 = split * p.tiles_per_split;
   const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
-  bool active[2];
-  int qh[2], row0[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int tt = 2 * pair + t;
-    active[t] = tt < p.G * p.tpq;
-    qh[t] = g * p.G + tt / p.tpq;
-    row0[t] = (tt % p.tpq) * 128;
-  }
+  const int qh = g * p.G + tt / p.tpq, row0 = (tt % p.tpq) * 128;
 
   if (threadIdx.x == 0) {
     mbar_init(qd_full, 1);
+    mbar_init(q_ready, 256);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&s_read[t], 128);
-      mbar_init(&dp_full[t], 1);
-      mbar_init(&ds_full[t], 128);
-    }
+    mbar_init(s_full, 1);
+    mbar_init(s_read, 256);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 256);
     mbar_init(dq_done, 1);
     fence_barrier_init();
   }
@@ -361,176 +408,183 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmG);
-      mbar_arrive_expect_tx(qd_full, (active[0] + active[1]) * 2 * C::Q_BYTES);
-      for (int t = 0; t < 2; ++t)
-        if (active[t])
-          for (int pn = 0; pn < C::PANELS; ++pn) {
-            tma_load_3d(sQ + t * C::Q_BYTES + pn * 128 * 128, &tmQ, qd_full, pn * 64, row0[t],
-                        qh[t]);
-            tma_load_3d(sG + t * C::Q_BYTES + pn * 128 * 128, &tmG, qd_full, pn * 64, row0[t],
-                        qh[t]);
-          }
+      uint8_t* qs = sKV + C::QSLOT * C::SLOT;
+      mbar_arrive_expect_tx(qd_full, 2 * C::Q_BYTES);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma_load_3d(qs + pn * 128 * 128, &tmQ, qd_full, pn * 64, row0, qh);
+        tma_load_3d(qs + C::Q_BYTES + pn * 128 * 128, &tmG, qd_full, pn * 64, row0, qh);
+      }
       for (int j = 0; j < nt; ++j) {
         const int s = j % C::STAGES, u = j / C::STAGES;
         if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
+        else if (s == C::QSLOT) mbar_wait(q_ready, 0);   // Q / dO have left this slot
         uint8_t* slot = sKV + s * C::SLOT;
         mbar_arrive_expect_tx(&kv_full[s], C::SLOT);
-        const int kr = (kv_t0 + j) * kStep;
+        const int kr = (kv_t0 + j) * 128;
         for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_3d(slot + pn * kStep * 128, &tmK, &kv_full[s], pn * 64, kr, g);
-          tma_load_3d(slot + C::KVT_BYTES + pn * kStep * 128, &tmV, &kv_full[s], pn * 64, kr, g);
+          tma_load_3d(slot + pn * 128 * 128, &tmK, &kv_full[s], pn * 64, kr, g);
+          tma_load_3d(slot + C::KVT_BYTES + pn * 128 * 128, &tmV, &kv_full[s], pn * 64, kr, g);
         }
       }
     }
   } else if (warp == 9) {
-    {   // converged warp; one elected lane issues
-      constexpr uint32_t idS = idesc_bf16(128, kStep, false, false);
-      constexpr uint32_t idQ = idesc_bf16(128, D, false, true);
-      const uint64_t dq0 = umma_desc_sw128(smem_u32(sQ), 0, 1024);
-      const uint64_t dg0 = umma_desc_sw128(smem_u32(sG), 0, 1024);
-      const uint64_t dkv0 = umma_desc_sw128(smem_u32(sKV), 0, 1024);           // K-major K / V
-      const uint64_t dkm0 = umma_desc_sw128(smem_u32(sKV), kStep * 128, 1024); // MN-major K
-      mbar_wait(qd_full, 0);
-      tc_fence_after();
-      // Per query tile t the tensor pipe sees
-      //   S_t(j+1) [after softmax read S_t(j)]  ...  dQ_t(j) [dS over dP_t] -> dP_t(j+1)
-      // so the exponentials of step j+1 overlap dQ_t(j); only dS = P(dP - D)
-      // sits between dP_t(j) and dQ_t(j).
-      auto issue_s = [&](int t, int j) {
-        if (elect_one()) {
-          const uint64_t a = dq0 + ((t * C::Q_BYTES) >> 4);
-          const uint64_t b = dkv0 + (((j % C::STAGES) * C::SLOT) >> 4);
+    // ------------------------------------------- MMA issuer (converged warp)
+    constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idQ = idesc_bf16(128, D, false, true);
+    const uint64_t dkv0 = umma_desc_sw128(smem_u32(sKV), 0, 1024);          // K-major K / V
+    const uint64_t dkm0 = umma_desc_sw128(smem_u32(sKV), 128 * 128, 1024);  // MN-major K
+    auto kslot = [&](int j) { return (uint64_t)(((j % C::STAGES) * C::SLOT) >> 4); };
+    auto issue_sdp = [&](int j, uint32_t a_col, uint32_t col, uint32_t boff, uint64_t* bar) {
+      if (elect_one()) {   // S = Q K^T / dP = dO V^T, A (Q / dO) from TMEM
+        const uint64_t b = dkv0 + kslot(j) + (boff >> 4);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t qo = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
-            const uint32_t ko = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
-            mma_bf16_ss(tmem + t * 128, a + qo, b + ko, idS, kk > 0);
-          }
-          mma_commit(&s_full[t]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t o = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+          mma_bf16_ts(tmem + col, tmem + a_col + kk * 8, b + o, idS, kk > 0);
         }
-        __syncwarp();
-      };
-      auto issue_dp = [&](int t, int j) {
-        if (elect_one()) {
-          const uint64_t a = dg0 + ((t * C::Q_BYTES) >> 4);
-          const uint64_t b = dkv0 + (((j % C::STAGES) * C::SLOT + C::KVT_BYTES) >> 4);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t qo = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
-            const uint32_t ko = ((kk >> 2) * (kStep * 128) + (kk & 3) * 32) >> 4;
-            mma_bf16_ss(tmem + t * 128 + 64, a + qo, b + ko, idS, kk > 0);
-          }
-          mma_commit(&dp_full[t]);
-        }
-        __syncwarp();
-      };
-      auto issue_dq = [&](int t, int j) {
-        if (elect_one()) {
-          const uint64_t b = dkm0 + (((j % C::STAGES) * C::SLOT) >> 4);
-#pragma unroll
-          for (int kk = 0; kk < kStep / 16; ++kk)   // dQ += dS K (A = dS in TMEM over dP_t)
-            mma_bf16_ts(tmem + C::DQ_COL + t * D, tmem + t * 128 + 64 + kk * 8,
-                        b + ((kk * 16 * 128) >> 4), idQ, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        __syncwarp();
-      };
-      auto wait_kv = [&](int j) {
-        mbar_wait(&kv_full[j % C::STAGES], (j / C::STAGES) & 1);
-        tc_fence_after();
-      };
-      wait_kv(0);
-      for (int t = 0; t < 2; ++t)
-        if (active[t]) {
-          issue_s(t, 0);
-          issue_dp(t, 0);
-        }
-      for (int j = 0; j < nt; ++j) {
-        if (j + 1 < nt) {
-          wait_kv(j + 1);
-          for (int t = 0; t < 2; ++t) {
-            if (!active[t]) continue;
-            mbar_wait(&s_read[t], j & 1);
-            tc_fence_after();
-            issue_s(t, j + 1);
-          }
-        }
-        for (int t = 0; t < 2; ++t) {
-          if (!active[t]) continue;
-          mbar_wait(&ds_full[t], j & 1);
-          tc_fence_after();
-          issue_dq(t, j);
-          if (j + 1 < nt) issue_dp(t, j + 1);
-        }
-        if (elect_one()) mma_commit(&kv_empty[j % C::STAGES]);
-        __syncwarp();
+        mma_commit(bar);
       }
-      if (elect_one()) mma_commit(dq_done);
       __syncwarp();
-    }
-  } else {
-    // ------------------------------------------ softmax (query row per thread)
-    const int t = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
-    if (active[t]) {
-      const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-      const int row = row0[t] + r;
-      const size_t prow = (size_t)qh[t] * p.rows_pad + row;
-      const float lrow = p.Lp[prow], drow = p.Dp[prow];
-      for (int j = 0; j < nt; ++j) {
-        const int nvalid = min(kStep, p.rows_kv - (kv_t0 + j) * kStep);
-        // phase A: P = exp2(S*c - Lp) as soon as S_t(j) lands; S_t is then free
-        mbar_wait(&s_full[t], j & 1);
-        tc_fence_after();
-        float pv[64];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t sv[32];
-          tmem_ld32(tl + t * 128 + hh * 32, sv);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow));
-            pv[hh * 32 + e] = (hh * 32 + e < nvalid) ? x : 0.f;
-          }
-          if (hh == 1) {
-            tc_fence_before();
-            mbar_arrive(&s_read[t]);
-          }
-        }
-        // phase B: dS = P (dP - D), bf16 pairs over dP_t
-        mbar_wait(&dp_full[t], j & 1);
-        tc_fence_after();
-        uint32_t dd[32];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t gv[32];
-          tmem_ld32(tl + t * 128 + 64 + hh * 32, gv);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; e += 2)
-            dd[hh * 16 + e / 2] = pack_bf16(pv[hh * 32 + e] * (__uint_as_float(gv[e]) - drow),
-                                            pv[hh * 32 + e + 1] * (__uint_as_float(gv[e + 1]) - drow));
-        }
-        tmem_st32(tl + t * 128 + 64, dd);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&ds_full[t]);
-      }
-      mbar_wait(dq_done, 0);
+    };
+    auto wait_kv = [&](int j) {
+      mbar_wait(&kv_full[j % C::STAGES], (j / C::STAGES) & 1);
       tc_fence_after();
-      const bool valid = row < p.rows_q;
-      float* dst = p.ws_dq + (((size_t)split * p.hq + qh[t]) * p.rows_q + row) * D;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tl + C::DQ_COL + t * D + c * 32, v);
-        tmem_wait_ld();
-        if (valid) {
+    };
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    wait_kv(0);
+    issue_sdp(0, C::Q_COL, C::S_COL, 0, s_full);
+    issue_sdp(0, C::G_COL, C::DP_COL, C::KVT_BYTES, dp_full);
+    for (int j = 0; j < nt; ++j) {
+      const uint32_t ph = j & 1;
+      if (j + 1 < nt) {
+        wait_kv(j + 1);
+        mbar_wait(s_read, ph);
+        tc_fence_after();
+        issue_sdp(j + 1, C::Q_COL, C::S_COL, 0, s_full);            // S(j+1)
+      }
+      mbar_wait(ds_full, ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t b = dkm0 + kslot(j);
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + e) =
-                make_float4(__uint_as_float(v[e]) * p.scale, __uint_as_float(v[e + 1]) * p.scale,
-                            __uint_as_float(v[e + 2]) * p.scale, __uint_as_float(v[e + 3]) * p.scale);
+        for (int kk = 0; kk < 128 / 16; ++kk)   // dQ += dS K (A = dS packed over dP)
+          mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + kk * 8, b + ((kk * 16 * 128) >> 4),
+                      idQ, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&kv_empty[j % C::STAGES]);
+      }
+      __syncwarp();
+      if (j + 1 < nt) issue_sdp(j + 1, C::G_COL, C::DP_COL, C::KVT_BYTES, dp_full);   // dP(j+1)
+    }
+    if (elect_one()) mma_commit(dq_done);
+    __syncwarp();
+  } else {
+    // ------------- softmax: query row per thread, 64 of the 128 kv columns per wg
+    const int wg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    {   // stage Q (wg 0) / dO (wg 1) rows into TMEM as bf16 pairs (A operands)
+      mbar_wait(qd_full, 0);
+      const uint32_t base = smem_u32(sKV + C::QSLOT * C::SLOT + wg * C::Q_BYTES) + r * 128;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {      // one 64-column (128 B) panel per chunk
+        uint32_t v[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {          // 16-byte chunks, 128B swizzle
+          uint32_t a, b2, c2, d2;
+          const uint32_t addr = base + c * 128 * 128 + ((q ^ (r & 7)) << 4);
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(a), "=r"(b2), "=r"(c2), "=r"(d2) : "r"(addr));
+          v[q * 4] = a; v[q * 4 + 1] = b2; v[q * 4 + 2] = c2; v[q * 4 + 3] = d2;
         }
+        tmem_st32(tl + (wg ? C::G_COL : C::Q_COL) + c * 32, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(q_ready);
+    }
+    const int row = row0 + r;
+    const size_t prow = (size_t)qh * p.rows_pad + row;
+    const float lrow = p.Lp[prow], drow = p.Dp[prow];
+    for (int j = 0; j < nt; ++j) {
+      const uint32_t ph = j & 1;
+      const int nvalid = min(128, p.rows_kv - (kv_t0 + j) * 128) - wg * 64;
+      // phase A: P = exp2(S*c - Lp), packed in registers; S is then free
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      uint32_t pp[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sv[32];
+        tmem_ld32(tl + C::S_COL + wg * 64 + hh * 32, sv);
+        tmem_wait_ld();
+        if (p.debug == 1) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pp[hh * 16 + e] = sv[2 * e];
+          continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const int c = hh * 32 + e;
+          float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow));
+          float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lrow));
+          float p2 = ex2(fmaf(__uint_as_float(sv[e + 2]), p.scale_log2, -lrow));
+          float p3 = ex2_poly(fmaf(__uint_as_float(sv[e + 3]), p.scale_log2, -lrow));
+          if (nvalid < 64) {
+            p0 = c < nvalid ? p0 : 0.f;
+            p1 = c + 1 < nvalid ? p1 : 0.f;
+            p2 = c + 2 < nvalid ? p2 : 0.f;
+            p3 = c + 3 < nvalid ? p3 : 0.f;
+          }
+          pp[c / 2] = pack_bf16(p0, p1);
+          pp[c / 2 + 1] = pack_bf16(p2, p3);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(s_read);
+      // phase B: dS = P (dP - D), packed over dP
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      uint32_t dd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t gv[32];
+        tmem_ld32(tl + C::DP_COL + wg * 64 + hh * 32, gv);
+        tmem_wait_ld();
+        if (p.debug == 1) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
+          continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const uint32_t a = pp[(hh * 32 + e) / 2];
+          const float p0 = __uint_as_float(a << 16), p1 = __uint_as_float(a & 0xFFFF0000u);
+          dd[(hh * 32 + e) / 2] = pack_bf16(p0 * (__uint_as_float(gv[e]) - drow),
+                                            p1 * (__uint_as_float(gv[e + 1]) - drow));
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // both wgs read dP before packing
+      tmem_st32(tl + C::DP_COL + wg * 32, dd);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    // epilogue: warpgroup w drains dQ columns [w*D/2, (w+1)*D/2) of its rows
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    const bool valid = row < p.rows_q;
+    float* dst = p.ws_dq + (((size_t)split * p.hq + qh) * p.rows_q + row) * D;
+#pragma unroll 1
+    for (int c = wg * (D / 64); c < (wg + 1) * (D / 64); ++c) {
+      uint32_t v[32];
+      tmem_ld32(tl + C::DQ_COL + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(dst + c * 32 + e) =
+              make_float4(__uint_as_float(v[e]) * p.scale, __uint_as_float(v[e + 1]) * p.scale,
+                          __uint_as_float(v[e + 2]) * p.scale, __uint_as_float(v[e + 3]) * p.scale);
       }
     }
   }
@@ -592,13 +646,13 @@ BwdPlan plan_bwd(const lvx_view* q, const lvx_view* k) {
   pl.tq64 = (int)ceil_div(q->rows, kStep);
   pl.tpq = (int)ceil_div(q->rows, 128);
   pl.rows_pad = pl.tpq * 128;
-  pl.pairs = (int)ceil_div((int64_t)G * pl.tpq, 2);
-  pl.n_tiles = (int)ceil_div(k->rows, kStep);
+  pl.pairs = G * pl.tpq;                       // one 128-row query tile per dQ CTA
+  pl.n_tiles = (int)ceil_div(k->rows, 128);
   const int64_t units0 = (int64_t)pl.pairs * k->heads;
   const int sms = device_sms();
   int best = 1;
   double best_score = -1.0;
-  const int max_s = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.n_tiles / 4));
+  const int max_s = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.n_tiles / 2));
   for (int s = 1; s <= max_s; ++s) {
     const int tps = (int)ceil_div(pl.n_tiles, s);
     const int real_s = (int)ceil_div(pl.n_tiles, tps);
@@ -637,6 +691,8 @@ void fill_params(BwdParams& p, const BwdPlan& pl, const lvx_view* q, const lvx_v
   p.splits = pl.splits;
   p.scale = (float)scale;
   p.scale_log2 = (float)(scale * 1.4426950408889634);
+  const char* dbg = getenv("LVX_BWD_DEBUG");
+  p.debug = dbg ? atoi(dbg) : 0;
   char* w = static_cast<char*>(ws);
   const size_t lp_bytes = align256((size_t)p.hq * p.rows_pad * 4);
   p.Lp = reinterpret_cast<float*>(w);
@@ -660,8 +716,8 @@ template <int D>
 int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
                BwdParams p, const lvx_view* dk, const lvx_view* dvv, int accumulate,
                cudaStream_t st) {
-  CUtensorMap mq64, mg64, mk128, mv128;
-  if (!make_tma_3d(&mq64, q, kStep) || !make_tma_3d(&mg64, dO, kStep) ||
+  CUtensorMap mq128, mg128, mk128, mv128;
+  if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
       !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
     return LVX_ECUDA;
   static bool attr = false;
@@ -679,7 +735,7 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.dv_rs = dvv->row_stride;
   p.accumulate = accumulate;
   bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 320,
-                      DkvCfg<D>::SMEM, st>>>(mq64, mk128, mv128, mg64, p);
+                      DkvCfg<D>::SMEM, st>>>(mq128, mk128, mv128, mg128, p);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
@@ -687,9 +743,9 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
 template <int D>
 int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
               const BwdParams& p, const BwdPlan& pl, cudaStream_t st) {
-  CUtensorMap mq128, mg128, mk64, mv64;
+  CUtensorMap mq128, mg128, mk128, mv128;
   if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
-      !make_tma_3d(&mk64, k, kStep) || !make_tma_3d(&mv64, v, kStep))
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
     return LVX_ECUDA;
   static bool attr = false;
   if (!attr) {
@@ -699,7 +755,7 @@ int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx
     attr = true;
   }
   bwd_dq_kernel<D><<<dim3(pl.pairs, pl.splits, (unsigned)k->heads), 320, DqCfg<D>::SMEM, st>>>(
-      mq128, mk64, mv64, mg128, p);
+      mq128, mk128, mv128, mg128, p);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }

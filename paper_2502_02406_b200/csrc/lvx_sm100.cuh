@@ -216,7 +216,9 @@ __device__ __forceinline__ float ex2(float x) {
 // round-to-nearest split x = j + f, f in [-0.5, 0.5], degree-3 minimax of 2^f
 // (max relative error 7.5e-5, far below bf16 rounding of P), exponent add.
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
+  // clamp at -126: p(0) = 0.99993 has exponent 126, so j >= -126 keeps the
+  // biased exponent >= 0 (x = -inf, e.g. padded rows with L = +inf, -> ~1e-38)
+  x = fmaxf(x, -126.f);
   const float t = x + 12582912.f;          // 1.5 * 2^23
   const float j = t - 12582912.f;
   const float f = x - j;
