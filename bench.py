@@ -191,6 +191,10 @@ def native_arm(args):
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
+        # the ring hop's NCCL kernel becomes ready exactly when the next
+        # attention grid launches; high-priority NCCL streams let it take the
+        # first SM that frees instead of queueing behind the whole grid
+        os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     from paper_2502_02406_b200 import build

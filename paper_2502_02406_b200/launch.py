@@ -29,6 +29,7 @@ def _worker(rank, n, port, args, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         torch.cuda.set_device(rank)
+        os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
         dist.init_process_group("nccl", rank=rank, world_size=n,
                                 device_id=torch.device("cuda", rank))
         from .strategies import run_distributed
