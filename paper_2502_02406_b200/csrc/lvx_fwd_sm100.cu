@@ -40,7 +40,7 @@ using namespace sm100;
 
 constexpr int kBM = 128;   // query rows per tile (TMEM lanes)
 constexpr int kBN = 128;   // kv rows per tile
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <int D>
@@ -62,6 +62,7 @@ struct FwdParams {
   int tiles_per_split;
   int splits;
   float scale_log2;     // scale * log2(e)
+  int variant;          // LVX_FWD_VARIANT (tuning only): 1 = stub exp math, 2 = always two-pass
   float* ws_o;          // [splits][hq][rows_q][D]
   float* ws_l;          // [splits][hq][rows_q]
 };
@@ -117,9 +118,12 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
+  // Registers move from warpgroup 2 (TMA + MMA issue) to the softmax
+  // warpgroups, which hold a packed P tile plus two S chunks in flight.  Each
+  // role resizes inside its own branch so ptxas sizes each region separately.
   if (warp == 8) {
     // ------------------------------------------------------------ producer
+    reg_dealloc<56>();
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
@@ -144,6 +148,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    reg_dealloc<56>();
     // Tensor-pipe order per KV tile j and query tile t:
     //   ... PV_t(j-1) -> QK_t(j) -> [softmax_t(j) writes P over S_t] -> PV_t(j) -> QK_t(j+1)
     // tcgen05.mma executes in issue order, so QK_t(j+1) overwrites S_t/P_t only
@@ -212,8 +217,11 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         if (j + 1 < nt) release(2 * j + 2);         // K_{j+1} consumed
       }
     }
+  } else if (warp >= 10) {
+    reg_dealloc<56>();   // idle warps of warpgroup 2
   } else {
     // ------------------------------------------------------------ softmax
+    reg_alloc<224>();
     const int t = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     if (active[t]) {
       const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
@@ -223,62 +231,116 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         tc_fence_after();
         const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
         const uint32_t sa = tl + C::S_COL0 + t * kBN;
-        // pass 1 over TMEM: row max (log2 domain)
-        float mx = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t sv[32];
-          tmem_ld32(sa + c * 32, sv);
-          tmem_wait_ld();
-          if (nvalid == kBN) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
-          }
-        }
-        mx *= p.scale_log2;
-        const bool need = mx > m_used + kRescaleThreshold;
-        const float alpha = need ? ex2(m_used - mx) : 1.f;
-        if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            const uint32_t oa = tl + C::O_COL0 + t * D + c * 32;
-            tmem_ld32(oa, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st32(oa, ov);
-          }
-        }
-        if (need) {
-          l *= alpha;
-          m_used = mx;
-        }
-        // pass 2: P = exp2(S*c - m) -> bf16 pairs written over S_t (chunk c of
-        // S is read before packed columns [16c, 16c+16) are overwritten)
+        // Single pass (j > 0): exponentiate against the current reference max
+        // m_used while tracking the row max.  The four S chunks are loaded
+        // in two round trips; P stays packed in registers until the warp knows no
+        // row grew past m_used + threshold, so S is still intact in TMEM for
+        // the two-pass path below when one did (rare after the first tiles).
+        bool done = false;
         float rs = 0.f;
+        if (j > 0 && p.variant == 0) {
+          uint32_t pk[4][16];
+          float xmc[4], rsc[4];   // per-chunk partials: four short dependency chains
+          auto chunk = [&](const uint32_t (&sv)[32], int c) {
+            float xm = -INFINITY, rs = 0.f;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t sv[32], pk[16];
-          tmem_ld32(sa + c * 32, sv);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int col = c * 32 + e;
-            float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used));
-            float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used));
-            if (nvalid < kBN) {
-              p0 = col < nvalid ? p0 : 0.f;
-              p1 = col + 1 < nvalid ? p1 : 0.f;
+            for (int e = 0; e < 32; e += 2) {
+              const int col = c * 32 + e;
+              float x0 = fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used);
+              float x1 = fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used);
+              if (nvalid < kBN) {
+                x0 = col < nvalid ? x0 : -INFINITY;
+                x1 = col + 1 < nvalid ? x1 : -INFINITY;
+              }
+              xm = fmaxf(xm, fmaxf(x0, x1));
+              const float p0 = ex2(x0), p1 = ex2(x1);
+              rs += p0 + p1;
+              pk[c][e / 2] = pack_bf16(p0, p1);
             }
-            rs += p0 + p1;
-            pk[e / 2] = pack_bf16(p0, p1);
+            xmc[c] = xm;
+            rsc[c] = rs;
+          };
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip (register cap 168)
+            uint32_t s0[32], s1[32];
+            tmem_ld32(sa + h * 64, s0);
+            tmem_ld32(sa + h * 64 + 32, s1);
+            tmem_wait_ld();
+            chunk(s0, 2 * h);
+            chunk(s1, 2 * h + 1);
           }
-          tmem_st16(sa + c * 16, pk);
+          rs = (rsc[0] + rsc[1]) + (rsc[2] + rsc[3]);
+          const float xm = fmaxf(fmaxf(xmc[0], xmc[1]), fmaxf(xmc[2], xmc[3]));
+          if (!__any_sync(0xffffffffu, xm > kRescaleThreshold)) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_st16(sa + c * 16, pk[c]);
+            done = true;
+          } else {
+            rs = 0.f;
+          }
+        }
+        if (!done) {
+          // pass 1 over TMEM: row max (log2 domain)
+          float mx = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t sv[32];
+            tmem_ld32(sa + c * 32, sv);
+            tmem_wait_ld();
+            if (nvalid == kBN) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
+            }
+          }
+          mx *= p.scale_log2;
+          const bool need = mx > m_used + kRescaleThreshold;
+          const float alpha = need ? ex2(m_used - mx) : 1.f;
+          if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t ov[32];
+              const uint32_t oa = tl + C::O_COL0 + t * D + c * 32;
+              tmem_ld32(oa, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st32(oa, ov);
+            }
+          }
+          if (need) {
+            l *= alpha;
+            m_used = mx;
+          }
+          // pass 2: P = exp2(S*c - m) -> bf16 pairs written over S_t (chunk c of
+          // S is read before packed columns [16c, 16c+16) are overwritten)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t sv[32], pk[16];
+            tmem_ld32(sa + c * 32, sv);
+            tmem_wait_ld();
+            if (p.variant == 1) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pk[e] = sv[2 * e];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const int col = c * 32 + e;
+                float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used));
+                float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used));
+                if (nvalid < kBN) {
+                  p0 = col < nvalid ? p0 : 0.f;
+                  p1 = col + 1 < nvalid ? p1 : 0.f;
+                }
+                rs += p0 + p1;
+                pk[e / 2] = pack_bf16(p0, p1);
+              }
+            }
+            tmem_st16(sa + c * 16, pk);
+          }
         }
         tmem_wait_st();
         l += rs;
@@ -492,6 +554,8 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
   p.tiles_per_split = pl.tiles_per_split;
   p.splits = pl.splits;
   p.scale_log2 = (float)(scale * 1.4426950408889634);
+  const char* var = getenv("LVX_FWD_VARIANT");
+  p.variant = var ? atoi(var) : 0;
   const size_t n = (size_t)q->heads * q->rows;
   p.ws_o = static_cast<float*>(ws);
   p.ws_l = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.splits * n * D * 4));
