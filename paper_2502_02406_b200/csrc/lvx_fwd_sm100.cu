@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "lvx_common.cuh"
 #include "lvx_sm100.cuh"
@@ -42,6 +43,8 @@ constexpr int kBM = 128;   // query rows per tile (TMEM lanes)
 constexpr int kBN = 128;   // kv rows per tile
 constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
+constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
 
 template <int D>
 struct FwdCfg {
@@ -62,7 +65,8 @@ struct FwdParams {
   int tiles_per_split;
   int splits;
   float scale_log2;     // scale * log2(e)
-  int variant;          // LVX_FWD_VARIANT (tuning only): 1 = stub exp math, 2 = always two-pass
+  int variant;          // LVX_FWD_VARIANT (tuning only): 1 = stub exp math, 2 = always two-pass,
+                        // 10 = no polynomial exp2
   float* ws_o;          // [splits][hq][rows_q][D]
   float* ws_l;          // [splits][hq][rows_q]
 };
@@ -232,51 +236,72 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
         const uint32_t sa = tl + C::S_COL0 + t * kBN;
         // Single pass (j > 0): exponentiate against the current reference max
-        // m_used while tracking the row max.  The four S chunks are loaded
-        // in two round trips; P stays packed in registers until the warp knows no
-        // row grew past m_used + threshold, so S is still intact in TMEM for
-        // the two-pass path below when one did (rare after the first tiles).
-        bool done = false;
+        // m_used without looking for the row max first.  The row sum bounds
+        // every element, so if no row's sum exceeds 2^kFastLog2 no P element
+        // does either and P is final.  P stays packed in registers until the
+        // warp knows that, so S is still intact in TMEM for the two-pass path
+        // below when a row's scores grew (rare after the first tiles; that
+        // path then moves m_used to the exact row max).  Packed FFMA2/FADD2
+        // halve the FMA-pipe issue per element.
+        bool done = false, fast_failed = false;
         float rs = 0.f;
-        if (j > 0 && p.variant == 0) {
+        if (j > 0 && p.variant != 1 && p.variant != 2) {
           uint32_t pk[4][16];
-          float xmc[4], rsc[4];   // per-chunk partials: four short dependency chains
-          auto chunk = [&](const uint32_t (&sv)[32], int c) {
-            float xm = -INFINITY, rs = 0.f;
+          float2 rsc[4];
+          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+          const float2 nm2 = make_float2(-m_used, -m_used);
+          // full and ragged tiles are separate instantiations: otherwise the
+          // column mask is if-converted into two selects per element everywhere
+          auto pass = [&](auto masked, auto poly) {
+            auto chunk = [&](const uint32_t (&sv)[32], int c) {
+              float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const int col = c * 32 + e;
-              float x0 = fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used);
-              float x1 = fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used);
-              if (nvalid < kBN) {
-                x0 = col < nvalid ? x0 : -INFINITY;
-                x1 = col + 1 < nvalid ? x1 : -INFINITY;
+              for (int e = 0; e < 32; e += 2) {
+                float2 x = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])),
+                                 sc2, nm2);
+                if constexpr (decltype(masked)::value) {
+                  const int col = c * 32 + e;
+                  x.x = col < nvalid ? x.x : -INFINITY;
+                  x.y = col + 1 < nvalid ? x.y : -INFINITY;
+                }
+                // decltype(poly)::value of every 8 pairs take exp2 on the FMA
+                // pipe: MUFU.EX2 alone would set the pace (2 x 128 per
+                // sub-partition per KV tile ~ the tile's MMA time)
+                const float2 pp = ((e / 2) % 8) < decltype(poly)::value
+                                      ? ex2_poly2(x)
+                                      : make_float2(ex2(x.x), ex2(x.y));
+                acc = fadd2(acc, pp);
+                pk[c][e / 2] = pack_bf16(pp.x, pp.y);
               }
-              xm = fmaxf(xm, fmaxf(x0, x1));
-              const float p0 = ex2(x0), p1 = ex2(x1);
-              rs += p0 + p1;
-              pk[c][e / 2] = pack_bf16(p0, p1);
-            }
-            xmc[c] = xm;
-            rsc[c] = rs;
-          };
+              rsc[c] = acc;
+            };
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip (register cap 168)
-            uint32_t s0[32], s1[32];
-            tmem_ld32(sa + h * 64, s0);
-            tmem_ld32(sa + h * 64 + 32, s1);
-            tmem_wait_ld();
-            chunk(s0, 2 * h);
-            chunk(s1, 2 * h + 1);
-          }
-          rs = (rsc[0] + rsc[1]) + (rsc[2] + rsc[3]);
-          const float xm = fmaxf(fmaxf(xmc[0], xmc[1]), fmaxf(xmc[2], xmc[3]));
-          if (!__any_sync(0xffffffffu, xm > kRescaleThreshold)) {
+            for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip
+              uint32_t s0[32], s1[32];
+              tmem_ld32(sa + h * 64, s0);
+              tmem_ld32(sa + h * 64 + 32, s1);
+              tmem_wait_ld();
+              chunk(s0, 2 * h);
+              chunk(s1, 2 * h + 1);
+            }
+          };
+          using I = std::integral_constant<int, 0>;
+          if (nvalid < kBN)
+            pass(std::true_type{}, I{});
+          else if (p.variant == 0)
+            pass(std::false_type{}, std::integral_constant<int, kPolyPairs>{});
+          else
+            pass(std::false_type{}, I{});
+          const float2 r2 = fadd2(fadd2(rsc[0], rsc[1]), fadd2(rsc[2], rsc[3]));
+          rs = r2.x + r2.y;
+          // !(rs <= bound) also catches inf / NaN sums
+          if (!__any_sync(0xffffffffu, !(rs <= kFastBound))) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_st16(sa + c * 16, pk[c]);
             done = true;
           } else {
             rs = 0.f;
+            fast_failed = true;
           }
         }
         if (!done) {
@@ -297,7 +322,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             }
           }
           mx *= p.scale_log2;
-          const bool need = mx > m_used + kRescaleThreshold;
+          const bool need = mx > m_used + (fast_failed ? 0.f : kRescaleThreshold);
           const float alpha = need ? ex2(m_used - mx) : 1.f;
           if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
 #pragma unroll 1

@@ -138,6 +138,28 @@ __device__ __forceinline__ void tmem_wait_st() {
 }
 
 // 32 lanes x 32 consecutive 32-bit columns; thread t gets lane (base+t).
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes per issue slot.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("{\n .reg .b64 a, b, c;\n mov.b64 a, {%1,%2};\n mov.b64 b, {%3,%4};\n"
+      " mov.b64 c, {%5,%6};\n fma.rn.f32x2 %0, a, b, c;\n}"
+      : "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("{\n .reg .b64 a, b;\n mov.b64 a, {%1,%2};\n mov.b64 b, {%3,%4};\n"
+      " add.rn.f32x2 %0, a, b;\n}"
+      : "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
 // Warpgroup register reallocation (all four warps of a warpgroup execute one).
 template <int N>
 __device__ __forceinline__ void reg_alloc() {
@@ -236,6 +258,23 @@ __device__ __forceinline__ float ex2_poly(float x) {
                        0.9999280713f);
   const int ji = __float_as_int(t) - 0x4B400000;
   return __int_as_float(__float_as_int(p) + (ji << 23));
+}
+
+// ex2_poly on a pair with packed FFMA2/FADD2 (10 issue slots per pair, no MUFU).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 mg = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, mg);
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.0551716531f, 0.0551716531f), f,
+                   make_float2(0.2426111615f, 0.2426111615f));
+  p = ffma2(p, f, make_float2(0.6932609919f, 0.6932609919f));
+  p = ffma2(p, f, make_float2(0.9999280713f, 0.9999280713f));
+  // bits(t) = 0x4B400000 + j and 0x4B400000 << 23 == 0 (mod 2^32)
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {

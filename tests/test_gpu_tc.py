@@ -64,6 +64,25 @@ def test_tc_forward_sharp_scores_rescale():
     assert eo <= TOL_BF16 and el <= TOL_BF16
 
 
+@pytest.mark.parametrize("growth", [0.5, 4.0])
+def test_tc_forward_growing_scores_fallback(growth):
+    # K rows scaled up tile by tile: the row max rises on every KV tile, so the
+    # single-pass softmax must reject its P (row sum over bound) and redo the
+    # tile through the two-pass path with an O rescale
+    import paper_2502_02406_b200 as lvx
+    (q, k, v, _), _ = bf16_inputs(2, 1, 200, 1500, 128, seed=21, q_scale=2.0)
+    ramp = 1.0 + growth * torch.arange(1500, device="cuda", dtype=torch.float32) / 128.0
+    k = (k.float() * ramp[None, :, None]).to(torch.bfloat16)
+    Q, K, V = (t.double().cpu().numpy() for t in (q, k, v))
+    st = lvx.blockwise_attention(q, k, v)
+    O, L = orc.blockwise_attention(Q, K, V)
+    eo = orc.max_norm_error(st.O.cpu().numpy(), O)
+    el = orc.max_norm_error(st.L.cpu().numpy(), L)
+    assert np.isfinite(st.O.cpu().numpy()).all()
+    print(f"\nTC fwd growing x{growth}: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
 def test_tc_forward_prior_merge_and_split_combine():
     import paper_2502_02406_b200 as lvx
     from paper_2502_02406_b200 import kernels as Kn
