@@ -9,6 +9,7 @@ the exported symbols.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
@@ -46,10 +47,12 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
-        raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_2502_02406_b200.build`"
+    # LVX_B200_LIB: an alternate build of the same library (same-box A/B tooling)
+    path = Path(os.environ.get("LVX_B200_LIB") or LIB_PATH)
+    if not path.exists():
+        raise RuntimeError(f"{path} not built: run `python -m paper_2502_02406_b200.build`"
                            " (there is no CPU fallback)")
-    lib = ctypes.CDLL(str(LIB_PATH))
+    lib = ctypes.CDLL(str(path))
     P = ctypes.POINTER(LvxView)
     vp, sz, dbl, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double, ctypes.c_int
     proto = {

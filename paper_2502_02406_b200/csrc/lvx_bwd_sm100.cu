@@ -8,21 +8,23 @@
 // atomic stream of 64 KB per (KV tile, Q tile) pair would need ~7 TB/s of L2
 // reductions at full tensor rate):
 //   bwd_dkv_kernel  KV-parallel.  One CTA owns a 128-row KV tile; dK, dV
-//                   accumulate in TMEM over every 64-row query step of the
+//                   accumulate in TMEM over every 128-row query step of the
 //                   GQA group (kernels.py:258-262 accumulate over rounds on
 //                   top of this in fp32 HBM accumulators).
 //                   MMAs: S^T = K Q^T, dP^T = V dO^T (SS); dV += P^T dO,
 //                   dK += dS^T Q (TS: P^T / dS^T live in TMEM as bf16, written
 //                   over the S^T / dP^T columns they came from).
-//   bwd_dq_kernel   Q-parallel, two 128-row query tiles per CTA sharing each
-//                   64-row K/V tile, split over the KV block.  S = Q K^T,
-//                   dP = dO V^T (SS); dQ += dS K (TS, dS in TMEM).
-// Softmax statistics enter pre-scaled: Lp = L log2(e) (+inf on padding rows,
-// so P = 0 there) and D, packed by bwd_prep_kernel into 16-byte aligned rows.
+//   bwd_dq_kernel   Q-parallel, one 128-row query tile per CTA (Q, dO copied
+//                   into TMEM), 128-row K/V steps, split over the KV block.
+//                   S = Q K^T, dP = dO V^T, dQ += dS K (all TS).
+// Softmax statistics enter pre-scaled and negated, nL = -L log2(e) (-inf on
+// padding rows, so P = 0 there) and nD = -D, packed by bwd_prep_kernel into
+// 16-byte aligned rows, so the element math is FFMA2 / FADD2 / FMUL2 pairs.
 #include <cuda.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "lvx_common.cuh"
 #include "lvx_sm100.cuh"
@@ -34,6 +36,7 @@ using namespace sm100;
 
 constexpr int kStep = 64;      // q rows per step (dkv kernel) / kv rows per step (dq kernel)
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kPolyPairs = 3;   // of every 8 column pairs, exp2 by polynomial (FMA pipe)
 
 // ------------------------------------------------------------------- prep
 __global__ void bwd_prep_kernel(View3<const float> L, View3<const float> Dv, int hq, int rows,
@@ -42,10 +45,10 @@ __global__ void bwd_prep_kernel(View3<const float> L, View3<const float> Dv, int
   if (idx >= (int64_t)hq * rows_pad) return;
   const int h = (int)(idx / rows_pad), r = (int)(idx % rows_pad);
   if (r < rows) {
-    Lp[idx] = *L.at(h, r) * kLog2e;
-    Dp[idx] = *Dv.at(h, r);
+    Lp[idx] = -*L.at(h, r) * kLog2e;
+    Dp[idx] = -*Dv.at(h, r);
   } else {
-    Lp[idx] = INFINITY;
+    Lp[idx] = -INFINITY;
     Dp[idx] = 0.f;
   }
 }
@@ -226,11 +229,12 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     // -------------- softmax: kv row per thread, 64 of the 128 query columns per wg
     const int wg = warp >> 2, q4 = warp & 3;
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     for (int i = 0; i < nsteps; ++i) {
       const int s = i % C::STAGES;
       const uint32_t ph = i & 1;
       const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 256;
-      // phase A: P^T = exp2(S^T * c - Lp[q]), 32 columns at a time
+      // phase A: P^T = exp2(S^T * c + nL[q]), 32 columns at a time
       mbar_wait(s_full, ph);
       tc_fence_after();
       uint32_t pp[32];
@@ -245,14 +249,15 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         } else {
 #pragma unroll
           for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 l4 = ld_shared_f4(lds + (hh * 32 + c4) * 4);
-            // phase A is MUFU-bound (16K exp2 per step): 1 in 4 on the FMA pipe
-            const float p0 = ex2(fmaf(__uint_as_float(sv[c4]), p.scale_log2, -l4.x));
-            const float p1 = ex2(fmaf(__uint_as_float(sv[c4 + 1]), p.scale_log2, -l4.y));
-            const float p2 = ex2(fmaf(__uint_as_float(sv[c4 + 2]), p.scale_log2, -l4.z));
-            const float p3 = ex2_poly(fmaf(__uint_as_float(sv[c4 + 3]), p.scale_log2, -l4.w));
-            pp[hh * 16 + c4 / 2] = pack_bf16(p0, p1);
-            pp[hh * 16 + c4 / 2 + 1] = pack_bf16(p2, p3);
+            const float4 l4 = ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
+            const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
+            const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
+            const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
+            const float2 p0 = (pi % 8) < kPolyPairs ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
+            const float2 p1 = ((pi + 1) % 8) < kPolyPairs ? ex2_poly2(x1)
+                                                          : make_float2(ex2(x1.x), ex2(x1.y));
+            pp[pi] = pack_bf16(p0.x, p0.y);
+            pp[pi + 1] = pack_bf16(p1.x, p1.y);
           }
         }
       }
@@ -261,7 +266,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
-      // phase B: dS^T = P^T (dP^T - D[q])
+      // phase B: dS^T = P^T (dP^T + nD[q])
       mbar_wait(dp_full, ph);
       tc_fence_after();
       uint32_t dd[32];
@@ -276,14 +281,14 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         } else {
 #pragma unroll
           for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 d4 = ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);
-            const uint32_t a = pp[hh * 16 + c4 / 2], b = pp[hh * 16 + c4 / 2 + 1];
-            const float p0 = __uint_as_float(a << 16), p1 = __uint_as_float(a & 0xFFFF0000u);
-            const float p2 = __uint_as_float(b << 16), p3 = __uint_as_float(b & 0xFFFF0000u);
-            dd[hh * 16 + c4 / 2] = pack_bf16(p0 * (__uint_as_float(gv[c4]) - d4.x),
-                                             p1 * (__uint_as_float(gv[c4 + 1]) - d4.y));
-            dd[hh * 16 + c4 / 2 + 1] = pack_bf16(p2 * (__uint_as_float(gv[c4 + 2]) - d4.z),
-                                                 p3 * (__uint_as_float(gv[c4 + 3]) - d4.w));
+            const float4 d4 = ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
+            const int pi = (hh * 32 + c4) / 2;
+            const float2 t0 = fadd2(u2f2(gv[c4], gv[c4 + 1]), make_float2(d4.x, d4.y));
+            const float2 t1 = fadd2(u2f2(gv[c4 + 2], gv[c4 + 3]), make_float2(d4.z, d4.w));
+            const float2 r0 = fmul2(unpack_bf16(pp[pi]), t0);
+            const float2 r1 = fmul2(unpack_bf16(pp[pi + 1]), t1);
+            dd[pi] = pack_bf16(r0.x, r0.y);
+            dd[pi + 1] = pack_bf16(r1.x, r1.y);
           }
         }
       }
@@ -504,11 +509,13 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     const int row = row0 + r;
     const size_t prow = (size_t)qh * p.rows_pad + row;
-    const float lrow = p.Lp[prow], drow = p.Dp[prow];
+    const float2 nl2 = make_float2(p.Lp[prow], p.Lp[prow]);   // -L log2 e
+    const float2 nd2 = make_float2(p.Dp[prow], p.Dp[prow]);   // -D
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     for (int j = 0; j < nt; ++j) {
       const uint32_t ph = j & 1;
       const int nvalid = min(128, p.rows_kv - (kv_t0 + j) * 128) - wg * 64;
-      // phase A: P = exp2(S*c - Lp), packed in registers; S is then free
+      // phase A: P = exp2(S*c + nL), packed in registers; S is then free
       mbar_wait(s_full, ph);
       tc_fence_after();
       uint32_t pp[32];
@@ -522,26 +529,31 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           for (int e = 0; e < 16; ++e) pp[hh * 16 + e] = sv[2 * e];
           continue;
         }
+        // full and ragged KV steps are separate instantiations (otherwise the
+        // column mask is if-converted into selects on every element)
+        auto pa = [&](auto masked) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const int c = hh * 32 + e;
-          float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -lrow));
-          float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -lrow));
-          float p2 = ex2(fmaf(__uint_as_float(sv[e + 2]), p.scale_log2, -lrow));
-          float p3 = ex2_poly(fmaf(__uint_as_float(sv[e + 3]), p.scale_log2, -lrow));
-          if (nvalid < 64) {
-            p0 = c < nvalid ? p0 : 0.f;
-            p1 = c + 1 < nvalid ? p1 : 0.f;
-            p2 = c + 2 < nvalid ? p2 : 0.f;
-            p3 = c + 3 < nvalid ? p3 : 0.f;
+          for (int e = 0; e < 32; e += 2) {
+            const int c = hh * 32 + e;
+            float2 x = ffma2(u2f2(sv[e], sv[e + 1]), sc2, nl2);
+            if constexpr (decltype(masked)::value) {
+              x.x = c < nvalid ? x.x : -INFINITY;
+              x.y = c + 1 < nvalid ? x.y : -INFINITY;
+            }
+            const float2 pq = ((c / 2) % 8) < kPolyPairs && !decltype(masked)::value
+                                  ? ex2_poly2(x)
+                                  : make_float2(ex2(x.x), ex2(x.y));
+            pp[c / 2] = pack_bf16(pq.x, pq.y);
           }
-          pp[c / 2] = pack_bf16(p0, p1);
-          pp[c / 2 + 1] = pack_bf16(p2, p3);
-        }
+        };
+        if (nvalid < 64)
+          pa(std::true_type{});
+        else
+          pa(std::false_type{});
       }
       tc_fence_before();
       mbar_arrive(s_read);
-      // phase B: dS = P (dP - D), packed over dP
+      // phase B: dS = P (dP + nD), packed over dP
       mbar_wait(dp_full, ph);
       tc_fence_after();
       uint32_t dd[32];
@@ -557,10 +569,9 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const uint32_t a = pp[(hh * 32 + e) / 2];
-          const float p0 = __uint_as_float(a << 16), p1 = __uint_as_float(a & 0xFFFF0000u);
-          dd[(hh * 32 + e) / 2] = pack_bf16(p0 * (__uint_as_float(gv[e]) - drow),
-                                            p1 * (__uint_as_float(gv[e + 1]) - drow));
+          const int pi = (hh * 32 + e) / 2;
+          const float2 r2 = fmul2(unpack_bf16(pp[pi]), fadd2(u2f2(gv[e], gv[e + 1]), nd2));
+          dd[pi] = pack_bf16(r2.x, r2.y);
         }
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");   // both wgs read dP before packing
