@@ -518,7 +518,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // phase A: P = exp2(S*c + nL), packed in registers; S is then free
       mbar_wait(s_full, ph);
       tc_fence_after();
-      uint32_t pp[32];
+      float2 pf[32];   // P in fp32 until phase B (only dS feeds an MMA here)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t sv[32];
@@ -526,7 +526,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tmem_wait_ld();
         if (p.debug == 1) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pp[hh * 16 + e] = sv[2 * e];
+          for (int e = 0; e < 16; ++e) pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
           continue;
         }
         // full and ragged KV steps are separate instantiations (otherwise the
@@ -543,7 +543,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             const float2 pq = ((c / 2) % 8) < kPolyPairs && !decltype(masked)::value
                                   ? ex2_poly2(x)
                                   : make_float2(ex2(x.x), ex2(x.y));
-            pp[c / 2] = pack_bf16(pq.x, pq.y);
+            pf[c / 2] = pq;
           }
         };
         if (nvalid < 64)
@@ -570,7 +570,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const int pi = (hh * 32 + e) / 2;
-          const float2 r2 = fmul2(unpack_bf16(pp[pi]), fadd2(u2f2(gv[e], gv[e + 1]), nd2));
+          const float2 r2 = fmul2(pf[pi], fadd2(u2f2(gv[e], gv[e + 1]), nd2));
           dd[pi] = pack_bf16(r2.x, r2.y);
         }
       }
