@@ -492,6 +492,22 @@ bool make_tma_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
   return r == CUDA_SUCCESS;
 }
 
+bool make_tma_f32_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t rs = (uint64_t)v->row_stride * 4;
+  uint64_t hs = (uint64_t)v->head_stride * 4;
+  if (v->heads <= 1) hs = rs * (uint64_t)(v->rows > 0 ? v->rows : 1);
+  cuuint64_t dims[3] = {(cuuint64_t)v->d, (cuuint64_t)v->rows, (cuuint64_t)v->heads};
+  cuuint64_t strides[2] = {rs, hs};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, v->data, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int device_sms() {
   static int sms = 0;
   if (!sms) {

@@ -81,6 +81,27 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// shared -> global tensor store / reduce-add (bulk-group completion)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
+                   "l"(reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, const void* src, int c0,
+                                                  int c1, int c2) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::
+          "l"(reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -175,6 +196,17 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
 }
 __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
+}
+
+// Named barriers over the two softmax warpgroups (256 threads): producers of
+// a hand-off arrive without waiting, consumers sync.
+template <int ID>
+__device__ __forceinline__ void named_arrive() {
+  asm volatile("bar.arrive %0, 256;" ::"n"(ID) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync %0, 256;" ::"n"(ID) : "memory");
 }
 
 // Warpgroup register reallocation (all four warps of a warpgroup execute one).
@@ -311,6 +343,8 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 
 // host helpers shared by the sm100 kernels (lvx_fwd_sm100.cu)
 bool make_tma_3d(CUtensorMap* m, const lvx_view* v, int box_rows);
+// fp32 [heads, rows, d] view -> 3-D map with a (32, box_rows, 1) box, 128B swizzle
+bool make_tma_f32_3d(CUtensorMap* m, const lvx_view* v, int box_rows);
 int device_sms();
 bool is_sm100();
 bool tma_view_ok(const lvx_view* v);
