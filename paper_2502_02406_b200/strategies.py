@@ -201,9 +201,25 @@ def _dev_copy(t: torch.Tensor, buf: torch.Tensor) -> torch.Tensor:
 # LV-XAttn query rotation
 # ---------------------------------------------------------------------------
 
+@dataclass
+class KVStream:
+    """K/V rows of the local block arriving / leaving in chunks (the host
+    pipeline, ``host_pipeline.py``).  ``bounds`` are row ranges covering the
+    block.  ``wait_chunk(c)`` makes the compute stream wait until chunk c is
+    resident (forward round 0 consumes chunks as they land; later rounds and
+    the backward find the whole block resident).  ``dkv_done(c, dk, dv)`` is
+    called once chunk c's dK / dV are final (the batched dK/dV pass runs per
+    chunk), so they can leave while the next chunk computes."""
+
+    bounds: list
+    wait_chunk: object = None
+    dkv_done: object = None
+
+
 def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                 scale: float, tile_rows: int = DEFAULT_TILE_ROWS,
-                trace: RoundTrace | None = None) -> AttentionState:
+                trace: RoundTrace | None = None,
+                kv_stream: KVStream | None = None) -> AttentionState:
     """Query-rotation forward for one rank; collective over all n
     (strategies.py:175-231).  Round r: ship the state finished last round
     (block i-r+1; round 0 ships the empty state) plus Q of block i-r to the
@@ -236,12 +252,29 @@ def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block
             o_r, l_r, q_r = o_s, l_s, q_cur
         t0 = ops.event() if trace is not None else None
         hop, sent = ctx.shift([o_s, l_s, q_cur], [o_r, l_r, q_r], ["O", "L", "Q"])
-        ws = ops.fwd_workspace(q_cur, k_block)
-        ops.fwd_partial(q_cur, k_block, v_block, scale, ws)
-        t1 = ops.event() if trace is not None else None
-        hop.wait()
-        t2 = ops.event() if trace is not None else None
-        ops.fwd_finish(q_cur, k_block, ws, o_r, l_r, o_r, l_r)   # merge(recv, delta)
+        if r == 0 and kv_stream is not None and len(kv_stream.bounds) > 1:
+            # K/V still streaming in: one partial + merge per resident chunk
+            for c, (a, b) in enumerate(kv_stream.bounds):
+                if kv_stream.wait_chunk is not None:
+                    kv_stream.wait_chunk(c)
+                kc, vc = k_block[:, a:b], v_block[:, a:b]
+                ws = ops.fwd_workspace(q_cur, kc)
+                ops.fwd_partial(q_cur, kc, vc, scale, ws)
+                if c == 0:
+                    t1 = ops.event() if trace is not None else None
+                    hop.wait()
+                    t2 = ops.event() if trace is not None else None
+                ops.fwd_finish(q_cur, kc, ws, o_r, l_r, o_r, l_r)
+        else:
+            if kv_stream is not None and kv_stream.wait_chunk is not None:
+                for c in range(len(kv_stream.bounds)):
+                    kv_stream.wait_chunk(c)
+            ws = ops.fwd_workspace(q_cur, k_block)
+            ops.fwd_partial(q_cur, k_block, v_block, scale, ws)
+            t1 = ops.event() if trace is not None else None
+            hop.wait()
+            t2 = ops.event() if trace is not None else None
+            ops.fwd_finish(q_cur, k_block, ws, o_r, l_r, o_r, l_r)   # merge(recv, delta)
         if trace is not None:
             t3 = ops.event()
             trace._add_timed(ops, t0, t1, t2, sent)
@@ -269,7 +302,7 @@ def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block
 
 def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                  state: AttentionState, do_block, scale: float,
-                 trace: RoundTrace | None = None):
+                 trace: RoundTrace | None = None, kv_stream: KVStream | None = None):
     """Query-rotation backward (strategies.py:234-276): the tuple
     (Q, dO, L, D, dQ) of every block travels once around the ring and every
     rank adds its K/V block's contribution; the last dQ hop is the
@@ -312,6 +345,15 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     l_j = _dev_copy(state.L, Lb.view(cur, qs[i]))
     d_j = Db.view(cur, qs[i])
     ops.row_stats(state.O, do_block, d_j)             # strategies.py:247
+    dk = torch.empty(k_block.shape, dtype=sd, device=dev)
+    dv = torch.empty(v_block.shape, dtype=sd, device=dev)
+    early_dkv = n == 1 and kv_stream is not None and kv_stream.dkv_done is not None
+    if early_dkv:   # n = 1: the rows are all local, so dK/dV first and their chunks
+        # leave the GPU while the dQ kernel runs
+        t4 = ops.event() if trace is not None else None
+        _dkv_chunks(ops, kv_stream, q_j, k_block, v_block, l_j, d_j, do_j, scale, dk, dv)
+        if trace is not None:
+            trace.section("dkv_kernel", ops, t4, ops.event())
     dq_prev = None
     blk = i
     for r in range(n):
@@ -370,13 +412,24 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
         hop.wait()
         if trace is not None:
             trace.epilogue_bytes_by_class = epi
-    dk = torch.empty(k_block.shape, dtype=sd, device=dev)
-    dv = torch.empty(v_block.shape, dtype=sd, device=dev)
-    t4 = ops.event() if trace is not None else None
-    ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
-    if trace is not None:
-        trace.section("dkv_kernel", ops, t4, ops.event())
+    if not early_dkv:
+        t4 = ops.event() if trace is not None else None
+        if kv_stream is not None and kv_stream.dkv_done is not None:
+            _dkv_chunks(ops, kv_stream, Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv)
+        else:
+            ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
+        if trace is not None:
+            trace.section("dkv_kernel", ops, t4, ops.event())
     return dq_out, dk, dv
+
+
+def _dkv_chunks(ops, kv_stream: KVStream, q, k_block, v_block, L, D, g, scale, dk, dv):
+    """The batched dK/dV pass per KV chunk (each chunk's rows are independent)."""
+    for c, (a, b) in enumerate(kv_stream.bounds):
+        dkc, dvc = dk[:, a:b], dv[:, a:b]
+        ops.bwd_dkv(q, k_block[:, a:b], v_block[:, a:b], L, D, g, scale, dkc, dvc,
+                    accumulate=False)
+        kv_stream.dkv_done(c, dkc, dvc)
 
 
 # ---------------------------------------------------------------------------

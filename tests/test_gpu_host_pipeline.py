@@ -1,0 +1,96 @@
+"""HostLayerPipeline (host-resident inputs, chunked H2D / D2H, prefetch) vs the
+oracle and vs the device-resident LV-XAttn path.
+
+Tolerance: bf16 outputs against the f64 oracle on the same bf16-rounded
+inputs, max-normalised error <= 1e-2 (as tests/test_gpu_tc.py).  Steps that
+run the same chunked schedule must agree bit for bit whether or not their
+inputs were prefetched."""
+import pytest
+import torch
+
+from oracle import lvx_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_02406_b200 import build
+    build.build()
+
+
+def _host_inputs(hq, hkv, sq, skv, d, seed):
+    Q, K, V, dO = orc.make_inputs(sq, skv, hq, d, seed, hkv=hkv)
+    return [torch.from_numpy(t).to(torch.bfloat16).pin_memory() for t in (Q, K, V, dO)]
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipeline_steps_vs_oracle(chunks):
+    from paper_2502_02406_b200.comm import DeviceContext
+    from paper_2502_02406_b200.host_pipeline import HostLayerPipeline, HostStep
+    from paper_2502_02406_b200.kernels import default_scale
+    from paper_2502_02406_b200.strategies import ShardSpec
+    hq, hkv, sq, skv, d = 4, 2, 200, 3000, 128
+    ctx = DeviceContext(0, 1)
+    shards = ShardSpec.balanced(sq, skv, 1)
+    scale = default_scale(d)
+    steps = [HostStep.allocate(*_host_inputs(hq, hkv, sq, skv, d, seed)) for seed in (1, 2, 3)]
+    HostLayerPipeline(ctx, shards, scale, chunks=chunks, prefetch=True).run(steps)
+    for seed, st in zip((1, 2, 3), steps):
+        Q, K, V, dO = (t.double().numpy() for t in (st.q, st.k, st.v, st.do))
+        O, L = orc.dense_attention(Q, K, V)
+        dQ, dK, dV = orc.dense_attention_backward(Q, K, V, O, L, dO)
+        errs = {"O": orc.max_norm_error(st.o.double().numpy(), O),
+                "L": orc.max_norm_error(st.l.double().numpy(), L),
+                "dQ": orc.max_norm_error(st.dq.double().numpy(), dQ),
+                "dK": orc.max_norm_error(st.dk.double().numpy(), dK),
+                "dV": orc.max_norm_error(st.dv.double().numpy(), dV)}
+        print(f"\nhost pipeline chunks={chunks} seed={seed}: {errs}")
+        assert max(errs.values()) <= TOL, errs
+
+
+def test_pipeline_prefetch_bit_identical():
+    """The same inputs run unprefetched (first step) and prefetched (later
+    steps, both slots) give identical bytes; prefetch off gives them too."""
+    from paper_2502_02406_b200.comm import DeviceContext
+    from paper_2502_02406_b200.host_pipeline import HostLayerPipeline, HostStep
+    from paper_2502_02406_b200.kernels import default_scale
+    from paper_2502_02406_b200.strategies import ShardSpec
+    hq, hkv, sq, skv, d = 8, 2, 130, 2500, 64
+    ctx = DeviceContext(0, 1)
+    shards = ShardSpec.balanced(sq, skv, 1)
+    ins = _host_inputs(hq, hkv, sq, skv, d, 7)
+    steps = [HostStep.allocate(*ins) for _ in range(3)]
+    HostLayerPipeline(ctx, shards, default_scale(d), chunks=4).run(steps)
+    alone = HostStep.allocate(*ins)
+    HostLayerPipeline(ctx, shards, default_scale(d), chunks=4, prefetch=False).run([alone])
+    for st in steps:
+        for name in ("o", "l", "dq", "dk", "dv"):
+            assert torch.equal(getattr(st, name), getattr(alone, name)), name
+
+
+def test_pipeline_matches_device_path():
+    """Chunked H2D / chunked dK/dV vs the device-resident strategies.  Not bit
+    identical: round 0 merges per-chunk partial states, so L (and through
+    P = exp(S - L) every gradient) differs in the last bits; within 5e-3."""
+    from paper_2502_02406_b200.comm import DeviceContext
+    from paper_2502_02406_b200.host_pipeline import HostLayerPipeline, HostStep
+    from paper_2502_02406_b200.kernels import default_scale
+    from paper_2502_02406_b200.strategies import ShardSpec, lvx_backward, lvx_forward
+    hq, hkv, sq, skv, d = 4, 4, 256, 4096, 128
+    ctx = DeviceContext(0, 1)
+    shards = ShardSpec.balanced(sq, skv, 1)
+    scale = default_scale(d)
+    ins = _host_inputs(hq, hkv, sq, skv, d, 11)
+    st = HostStep.allocate(*ins)
+    HostLayerPipeline(ctx, shards, scale, chunks=4).run([st])
+    q, k, v, g = (t.cuda() for t in ins)
+    state = lvx_forward(ctx, shards, q, k, v, scale)
+    dq, dk, dv = lvx_backward(ctx, shards, q, k, v, state, g, scale)
+    torch.cuda.synchronize()
+    for host, dev_t in ((st.o, state.O), (st.l, state.L), (st.dq, dq), (st.dk, dk), (st.dv, dv)):
+        err = orc.max_norm_error(host.double().numpy(), dev_t.double().cpu().numpy())
+        assert err <= 5e-3, err

@@ -149,3 +149,63 @@ def test_gloo_cross_attention_recompute_matches_reference(golden_mllm_ca, policy
                  (go, "gwo")):
         assert orc.max_norm_error(a, g[f"{pol}_{b}"]) <= 1e-12, b
     assert flops == int(g[f"{pol}_flops"])
+
+
+def _stream_worker(rank, n, port, q):
+    """lvx fwd+bwd with K/V streamed in 3 chunks (KVStream) vs the resident
+    call on the same rank: identical up to the chunked merge (f64)."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=n)
+        from paper_2502_02406_b200.comm import DeviceContext
+        from paper_2502_02406_b200.strategies import (KVStream, ShardSpec, lvx_backward,
+                                                      lvx_forward)
+        from tests.oracle_ops import OracleOps
+        Q, K, V, dO = (torch.from_numpy(t) for t in orc.make_inputs(96, 301, 4, 16, 5, hkv=2))
+        shards = ShardSpec.balanced(96, 301, n)
+        ctx = DeviceContext(rank, n, group=dist.group.WORLD, device=torch.device("cpu"),
+                            ops=OracleOps())
+        (qa, qb), (ka, kb) = shards.q_ranges[rank], shards.kv_ranges[rank]
+        q_i, do_i = Q[:, qa:qb].contiguous(), dO[:, qa:qb].contiguous()
+        k_i, v_i = K[:, ka:kb].contiguous(), V[:, ka:kb].contiguous()
+        scale = 0.25
+        st0 = lvx_forward(ctx, shards, q_i, k_i, v_i, scale)
+        g0 = lvx_backward(ctx, shards, q_i, k_i, v_i, st0, do_i, scale)
+        rows = k_i.shape[1]
+        bounds = [(0, rows // 3), (rows // 3, 2 * rows // 3), (2 * rows // 3, rows)]
+        waited, done = [], []
+        kvs = KVStream(bounds=bounds, wait_chunk=waited.append,
+                       dkv_done=lambda c, dk, dv: done.append((c, dk.clone(), dv.clone())))
+        st1 = lvx_forward(ctx, shards, q_i, k_i, v_i, scale, kv_stream=kvs)
+        g1 = lvx_backward(ctx, shards, q_i, k_i, v_i, st1, do_i, scale, kv_stream=kvs)
+        errs = [orc.max_norm_error(a.numpy(), b.numpy())
+                for a, b in ((st1.O, st0.O), (st1.L, st0.L), (g1[0], g0[0]), (g1[1], g0[1]),
+                             (g1[2], g0[2]))]
+        chunks_ok = [c for c, _, _ in done] == [0, 1, 2] and all(
+            torch.equal(dk, g1[1][:, a:b]) and torch.equal(dv, g1[2][:, a:b])
+            for (c, dk, dv), (a, b) in zip(done, bounds))
+        if rank == 0:
+            q.put(("ok", errs, waited[:3], chunks_ok))
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        import traceback
+        q.put(("err", rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_gloo_lvx_kv_stream_chunks(n):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _port()
+    ps = [ctx.Process(target=_stream_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in ps:
+        p.start()
+    msg = q.get()
+    for p in ps:
+        p.join(timeout=120)
+    assert msg[0] == "ok", msg
+    _, errs, waited, chunks_ok = msg
+    assert max(errs) <= 1e-12, errs
+    assert waited == [0, 1, 2]
+    assert chunks_ok
