@@ -301,8 +301,18 @@ def native_arm(args):
     kflops, kdur = kernels[kname]
     burst, sust, hbm, pk_kind = peaks()
     achieved = kflops / kdur / 1e12
+    traffic, traffic_src = None, None
+    tj = ROOT / "profiles" / "r01b_traffic.json"
+    if world == 1 and args.strategy == "lvx" and args.skv == CFG["s_kv"] and tj.exists():
+        # ncu DRAM bytes per launch of this kernel at this exact launch shape
+        rec = json.loads(tj.read_text())["per_launch"].get(kname)
+        if rec:
+            traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+            traffic_src = {"file": "profiles/r01b_traffic.json", "read": rec["dram_bytes_read"],
+                           "write": rec["dram_bytes_write"], "algorithmic": rec["algorithmic_bytes"]}
     roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": sust,
-                "unit": "TFLOP/s", "frac": achieved / sust, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / sust, "traffic": traffic,
+                "traffic_detail": traffic_src,
                 "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
                 "frac_of_burst": achieved / burst, "frac_of_nominal_2250": achieved / 2250.0,
                 "per_launch_ms": kdur * 1e3,
