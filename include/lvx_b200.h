@@ -155,6 +155,33 @@ int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream);
 /* dst = src converted (F32/F64/BF16 <-> F32/F64/BF16), strided views. */
 int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
 
+/* ---- projections (SURVEY.md §8(b) lvx_kv_recompute / lvx_project_bwd) --
+ * Plain GEMMs on cuBLAS (bf16 in / fp32 accumulate; f32 without TF32; f64).
+ * Row-major matrices; strides in elements; all operands one dtype.  These
+ * entry points keep one cuBLAS handle per device (created on first use,
+ * calls serialised by a mutex) and use cuBLAS's own workspace. */
+typedef struct lvx_matrix {
+  void* data;
+  int64_t rows, cols, row_stride;
+  int32_t dtype, _pad;
+} lvx_matrix;
+
+/* project (kernels.py:227-235): out[h] = x [S, e] @ w[:, h*d:(h+1)*d] for every
+ * head of the [heads, S, d] view out.  out->head_stride == d (heads are column
+ * blocks of one [S, heads*d] matrix) is one GEMM; any other head stride one
+ * strided-batched GEMM. */
+int lvx_project(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* out, void* stream);
+/* project_backward (kernels.py:238-254): dx = dout_flat w^T, dw = x^T dout_flat
+ * for dout a [heads, S, d] view (the flat [S, heads*d] matrix is never copied). */
+int lvx_project_bwd(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* dout,
+                    const lvx_matrix* dx, const lvx_matrix* dw, void* stream);
+/* The MLLM K/V recompute from the shared visual tokens (mllm.py:296-300,
+ * :358-360): k = project(y, w_k), v = project(y, w_v).  When w_v follows w_k in
+ * one [e, 2*hkv*d] weight and v_out follows k_out in one [S, 2*hkv*d] output
+ * (head_stride == d) it is ONE GEMM y @ [W_K | W_V]. */
+int lvx_kv_recompute(const lvx_matrix* y, const lvx_matrix* w_k, const lvx_matrix* w_v,
+                     const lvx_view* k_out, const lvx_view* v_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

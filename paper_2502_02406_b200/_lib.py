@@ -23,12 +23,19 @@ EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eli
            "lvx_blockwise_fwd", "lvx_fwd_partial", "lvx_fwd_finish", "lvx_merge_states",
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
            "lvx_fill_empty_state", "lvx_convert", "lvx_bwd_workspace", "lvx_bwd_dq_partial",
-           "lvx_bwd_dq_finish", "lvx_bwd_dkv")
+           "lvx_bwd_dq_finish", "lvx_bwd_dkv", "lvx_project", "lvx_project_bwd",
+           "lvx_kv_recompute")
 
 
 class LvxView(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("heads", ctypes.c_int64), ("rows", ctypes.c_int64),
                 ("d", ctypes.c_int64), ("head_stride", ctypes.c_int64),
+                ("row_stride", ctypes.c_int64), ("dtype", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+
+class LvxMatrix(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
                 ("row_stride", ctypes.c_int64), ("dtype", ctypes.c_int32),
                 ("_pad", ctypes.c_int32)]
 
@@ -54,6 +61,7 @@ def load() -> ctypes.CDLL:
                            " (there is no CPU fallback)")
     lib = ctypes.CDLL(str(path))
     P = ctypes.POINTER(LvxView)
+    M = ctypes.POINTER(LvxMatrix)
     vp, sz, dbl, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double, ctypes.c_int
     proto = {
         "lvx_abi_version": (i32, []),
@@ -74,6 +82,9 @@ def load() -> ctypes.CDLL:
         "lvx_bwd_dq_finish": (i32, [P, P, P, i32, vp, sz, vp]),
         "lvx_bwd_dkv": (i32, [P, P, P, P, P, P, dbl, P, P, i32, vp, sz, vp]),
         "lvx_convert": (i32, [P, P, vp]),
+        "lvx_project": (i32, [M, M, P, vp]),
+        "lvx_project_bwd": (i32, [M, M, P, M, M, vp]),
+        "lvx_kv_recompute": (i32, [M, M, M, P, P, vp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
@@ -105,6 +116,16 @@ def view(t: torch.Tensor | None):
     else:
         raise ValueError(f"expected a [heads, rows, d] tensor, got shape {tuple(t.shape)}")
     return ctypes.byref(v)
+
+
+def matrix(t: torch.Tensor):
+    """Row-major [rows, cols] matrix (unit column stride) -> pointer to LvxMatrix."""
+    if t.dim() != 2:
+        raise ValueError(f"expected a 2-D matrix, got shape {tuple(t.shape)}")
+    if t.numel() and t.shape[1] > 1 and t.stride(1) != 1:
+        raise ValueError("matrix columns must be contiguous")
+    rs = t.stride(0) if t.shape[0] > 1 else max(t.shape[1], 1)
+    return ctypes.byref(LvxMatrix(t.data_ptr(), t.shape[0], t.shape[1], rs, lvx_dtype(t), 0))
 
 
 def check(fn: str, status: int) -> None:

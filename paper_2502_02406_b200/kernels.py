@@ -360,9 +360,40 @@ def project(x, W, heads: int):
         raise ValueError(f"weight cols {W.shape[1]} not divisible by heads {heads}")
     (xt, kind), (wt, _) = _to_dev(x), _to_dev(W)
     dt = _common_dtype(xt, wt)
-    flat = xt.to(dt) @ wt.to(dt)
-    out = flat.view(xt.shape[0], heads, -1).transpose(0, 1).contiguous()
+    xt, wt = _rows_contig(xt.to(dt)), _rows_contig(wt.to(dt))
+    out = torch.empty((heads, xt.shape[0], wt.shape[1] // heads), dtype=dt, device=xt.device)
+    project_into(xt, wt, out)
     return _back(out, kind)
+
+
+def _rows_contig(t: torch.Tensor) -> torch.Tensor:
+    return t if (t.dim() != 2 or t.numel() == 0 or t.shape[1] <= 1 or t.stride(1) == 1) \
+        else t.contiguous()
+
+
+def project_into(x: torch.Tensor, W: torch.Tensor, out: torch.Tensor) -> None:
+    """out[h] = x @ W[:, h*d:(h+1)*d] for a [heads, S, d] device view (lvx_project;
+    one GEMM when the heads are column blocks of one [S, heads*d] matrix)."""
+    _lib.check("lvx_project", _lib.load().lvx_project(
+        _lib.matrix(x), _lib.matrix(W), _lib.view(out), _lib.stream_ptr(x.device)))
+
+
+def kv_recompute(y: torch.Tensor, w_k: torch.Tensor, w_v: torch.Tensor, k_out: torch.Tensor,
+                 v_out: torch.Tensor) -> None:
+    """K, V of the MLLM recompute from the shared visual tokens (mllm.py:296-300,
+    :358-360) into [hkv, S, d] device views (lvx_kv_recompute)."""
+    _lib.check("lvx_kv_recompute", _lib.load().lvx_kv_recompute(
+        _lib.matrix(y), _lib.matrix(w_k), _lib.matrix(w_v), _lib.view(k_out), _lib.view(v_out),
+        _lib.stream_ptr(y.device)))
+
+
+def project_backward_into(x: torch.Tensor, W: torch.Tensor, d_out: torch.Tensor,
+                          dx: torch.Tensor, dw: torch.Tensor) -> None:
+    """dx = dOut_flat W^T, dw = x^T dOut_flat for a [heads, S, d] device view
+    d_out (lvx_project_bwd, no flattening copy)."""
+    _lib.check("lvx_project_bwd", _lib.load().lvx_project_bwd(
+        _lib.matrix(x), _lib.matrix(W), _lib.view(d_out), _lib.matrix(dx), _lib.matrix(dw),
+        _lib.stream_ptr(x.device)))
 
 
 def project_backward(x, W, dOut):
@@ -374,5 +405,10 @@ def project_backward(x, W, dOut):
                          f"{tuple(x.shape)} and weight {tuple(W.shape)}")
     (xt, kind), (wt, _), (gt, _) = _to_dev(x), _to_dev(W), _to_dev(dOut)
     dt = _common_dtype(xt, wt)
-    g = gt.to(dt).transpose(0, 1).reshape(xt.shape[0], W.shape[1])
-    return _back(g @ wt.to(dt).T, kind), _back(xt.to(dt).T @ g, kind)
+    xt, wt, gt = _rows_contig(xt.to(dt)), _rows_contig(wt.to(dt)), gt.to(dt)
+    if gt.numel() and gt.shape[2] > 1 and gt.stride(2) != 1:
+        gt = gt.contiguous()
+    dx = torch.empty(xt.shape, dtype=dt, device=xt.device)
+    dw = torch.empty(wt.shape, dtype=dt, device=xt.device)
+    project_backward_into(xt, wt, gt, dx, dw)
+    return _back(dx, kind), _back(dw, kind)

@@ -17,9 +17,10 @@ the weights are replicated.  Every projection is row-local, so:
             partial sums over the rank's rows and are all-reduced (the
             reference is single-worker, so this collective is new).
 
-The projection GEMMs run on cuBLAS through torch (plain library GEMMs);
-fusing the K/V recompute into the attention kernels' producer is the next
-step.  ``OpCounter`` counts forward-direction projection FLOP
+The projection GEMMs run on cuBLAS behind the C ABI (``lvx_kv_recompute``,
+``lvx_project_bwd``; plain library GEMMs, heads folded into the GEMM strides);
+the output projection W_O stays a torch matmul.  Fusing the K/V recompute into
+the attention kernels' producer is the next step.  ``OpCounter`` counts forward-direction projection FLOP
 done inside the backward, like ``src/mllm.py:242-253``.
 """
 from __future__ import annotations
@@ -31,7 +32,7 @@ import torch
 import torch.distributed as dist
 
 from .comm import DeviceContext
-from .kernels import AttentionState, default_scale
+from .kernels import AttentionState, default_scale, kv_recompute, project_backward_into
 from .strategies import (ShardSpec, lvx_backward, lvx_forward, ring_backward, ring_forward)
 
 
@@ -104,10 +105,14 @@ def _flat(t: torch.Tensor) -> torch.Tensor:
 
 
 def project_kv(y: torch.Tensor, w: CrossAttentionWeights):
-    """K/V from the visual tokens with ONE GEMM y [S, e] @ [W_K | W_V]."""
-    kv = y @ w.kv_weight()
+    """K/V from the visual tokens with ONE GEMM y [S, e] @ [W_K | W_V]
+    (``lvx_kv_recompute``); K and V are zero-copy head views of its output."""
     hkd = w.hkv * w.d
-    return _heads(kv[:, :hkd], w.hkv), _heads(kv[:, hkd:], w.hkv)
+    wkv = w.kv_weight()
+    kv = torch.empty((y.shape[0], 2 * hkd), dtype=y.dtype, device=y.device)
+    k, v = _heads(kv[:, :hkd], w.hkv), _heads(kv[:, hkd:], w.hkv)
+    kv_recompute(y, wkv[:, :hkd], wkv[:, hkd:], k, v)
+    return k, v
 
 
 def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: torch.Tensor,
@@ -151,11 +156,15 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     dq, dk, dv = bwd(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
     del k, v
     dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
-    d_x = g_i + dq @ w.w_q.T
-    g_wq = saved.x.T @ dq
+    d_x = torch.empty_like(g_i)
+    g_wq = torch.empty_like(w.w_q)
+    project_backward_into(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
+    d_x += g_i
     dkv = torch.cat([dk, dv], dim=1)
-    d_y = dkv @ w.kv_weight().T
-    g_wkv = y_i.T @ dkv
+    wkv = w.kv_weight()
+    d_y = torch.empty_like(y_i)
+    g_wkv = torch.empty_like(wkv)
+    project_backward_into(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
     hkd = w.hkv * w.d
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
     if ctx.n > 1:

@@ -1,0 +1,89 @@
+"""Projection entry points (lvx_project / lvx_project_bwd / lvx_kv_recompute,
+cuBLAS behind the C ABI) vs the reference's golden vectors and vs torch.
+
+Tolerances: f64 1e-12 and f32 1e-5 max-normalised against the reference's own
+outputs (tests/golden/golden_kernels.npz: kernels.py:227-254 run in this
+container); bf16 layouts against a torch fp32 matmul of the same bf16 inputs,
+1e-2."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import lvx_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_02406_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("dt,tol", [(np.float64, 1e-12), (np.float32, 1e-5)])
+def test_project_vs_reference(golden_kernels, dt, tol):
+    from paper_2502_02406_b200 import kernels as K
+    g = golden_kernels
+    x, W, gr = (g[k].astype(dt) for k in ("proj_x", "proj_W", "proj_g"))
+    out = K.project(x, W, 2)
+    dx, dw = K.project_backward(x, W, gr)
+    assert out.dtype == dt and dx.dtype == dt
+    assert orc.max_norm_error(out, g["proj_out"]) <= tol
+    assert orc.max_norm_error(dx, g["proj_dX"]) <= tol
+    assert orc.max_norm_error(dw, g["proj_dW"]) <= tol
+
+
+def _bf(*shape, seed):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.rand(*shape, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16)
+
+
+def _err(a, b):
+    return orc.max_norm_error(a.double().cpu().numpy(), b.double().cpu().numpy())
+
+
+@pytest.mark.parametrize("interleaved", [True, False])
+def test_project_head_layouts_bf16(interleaved):
+    """One GEMM into column blocks of [S, h*d] vs strided-batched GEMM into a
+    contiguous [h, S, d] output; project_bwd with flat vs per-head dOut."""
+    from paper_2502_02406_b200 import kernels as K
+    S, e, h, d = 300, 256, 4, 64
+    x, W = _bf(S, e, seed=1), _bf(e, h * d, seed=2)
+    if interleaved:
+        out = torch.empty(S, h * d, dtype=torch.bfloat16, device="cuda").view(S, h, d).transpose(0, 1)
+    else:
+        out = torch.empty(h, S, d, dtype=torch.bfloat16, device="cuda")
+    K.project_into(x, W, out)
+    ref = (x.float() @ W.float()).view(S, h, d).transpose(0, 1)
+    assert _err(out, ref) <= 1e-2
+    g = _bf(h, S, d, seed=3)
+    if interleaved:
+        g = g.transpose(0, 1).contiguous().transpose(0, 1)   # [h, S, d] view, head stride d
+    dx = torch.empty_like(x)
+    dw = torch.empty_like(W)
+    K.project_backward_into(x, W, g, dx, dw)
+    gf = g.float().transpose(0, 1).reshape(S, h * d)
+    assert _err(dx, gf @ W.float().T) <= 1e-2
+    assert _err(dw, x.float().T @ gf) <= 1e-2
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_kv_recompute_bf16(fused):
+    from paper_2502_02406_b200 import kernels as K
+    S, e, hkv, d = 513, 384, 2, 128
+    y = _bf(S, e, seed=4)
+    wkv = _bf(e, 2 * hkv * d, seed=5)
+    wk, wv = (wkv[:, :hkv * d], wkv[:, hkv * d:]) if fused else \
+        (wkv[:, :hkv * d].contiguous(), wkv[:, hkv * d:].contiguous())
+    if fused:
+        kv = torch.empty(S, 2 * hkv * d, dtype=torch.bfloat16, device="cuda")
+        k = kv[:, :hkv * d].view(S, hkv, d).transpose(0, 1)
+        v = kv[:, hkv * d:].view(S, hkv, d).transpose(0, 1)
+    else:
+        k = torch.empty(hkv, S, d, dtype=torch.bfloat16, device="cuda")
+        v = torch.empty(hkv, S, d, dtype=torch.bfloat16, device="cuda")
+    K.kv_recompute(y, wk, wv, k, v)
+    ref = (y.float() @ wkv.float()).view(S, 2 * hkv, d).transpose(0, 1)
+    assert _err(k, ref[:hkv]) <= 1e-2 and _err(v, ref[hkv:]) <= 1e-2
