@@ -63,6 +63,18 @@ class CudaOps:
                       ws=self.bwd_workspace(q, k, slot=2))
 
     # -- device timing (CUDA events on the compute stream) -----------------
+    def kv_recompute(self, y, w_k, w_v, k_out, v_out) -> None:
+        """k_out / v_out ([hkv, S, d] views) = project(y, W_K / W_V) (lvx_kv_recompute)."""
+        if y.shape[0]:
+            K.kv_recompute(y, w_k, w_v, k_out, v_out)
+        else:
+            k_out.zero_()
+            v_out.zero_()
+
+    def project_backward(self, x, W, d_out, dx, dw) -> None:
+        """dx = dOut_flat W^T, dw = x^T dOut_flat for a [heads, S, d] view (lvx_project_bwd)."""
+        K.project_backward_into(x, W, d_out, dx, dw)
+
     @staticmethod
     def event():
         e = torch.cuda.Event(enable_timing=True)

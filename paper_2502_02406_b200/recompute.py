@@ -32,7 +32,7 @@ import torch
 import torch.distributed as dist
 
 from .comm import DeviceContext
-from .kernels import AttentionState, default_scale, kv_recompute, project_backward_into
+from .kernels import AttentionState, default_scale
 from .strategies import (ShardSpec, lvx_backward, lvx_forward, ring_backward, ring_forward)
 
 
@@ -104,14 +104,14 @@ def _flat(t: torch.Tensor) -> torch.Tensor:
     return t.transpose(0, 1).reshape(s, h * d)
 
 
-def project_kv(y: torch.Tensor, w: CrossAttentionWeights):
+def project_kv(ctx: DeviceContext, y: torch.Tensor, w: CrossAttentionWeights):
     """K/V from the visual tokens with ONE GEMM y [S, e] @ [W_K | W_V]
     (``lvx_kv_recompute``); K and V are zero-copy head views of its output."""
     hkd = w.hkv * w.d
     wkv = w.kv_weight()
     kv = torch.empty((y.shape[0], 2 * hkd), dtype=y.dtype, device=y.device)
     k, v = _heads(kv[:, :hkd], w.hkv), _heads(kv[:, hkd:], w.hkv)
-    kv_recompute(y, wkv[:, :hkd], wkv[:, hkd:], k, v)
+    ctx.ops.kv_recompute(y, wkv[:, :hkd], wkv[:, hkd:], k, v)
     return k, v
 
 
@@ -122,7 +122,7 @@ def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: to
     policy = ActivationPolicy(policy)
     scale = default_scale(w.d) if scale is None else scale
     q = _heads(x_i @ w.w_q, w.hq)
-    k, v = project_kv(y_i, w)
+    k, v = project_kv(ctx, y_i, w)
     fwd = lvx_forward if strategy == "lvx" else ring_forward
     st = fwd(ctx, shards, q, k, v, scale)
     saved = SavedCA(policy=policy, x=x_i, state=st,
@@ -148,7 +148,7 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     if saved.policy is ActivationPolicy.STORE_KV:
         k, v = saved.kv
     else:   # the MLLM-specific recompute from the one shared y
-        k, v = project_kv(y_i, w)
+        k, v = project_kv(ctx, y_i, w)
         if counter is not None:
             counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
             counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
@@ -158,13 +158,13 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
     d_x = torch.empty_like(g_i)
     g_wq = torch.empty_like(w.w_q)
-    project_backward_into(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
+    ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
     d_x += g_i
     dkv = torch.cat([dk, dv], dim=1)
     wkv = w.kv_weight()
     d_y = torch.empty_like(y_i)
     g_wkv = torch.empty_like(wkv)
-    project_backward_into(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
+    ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
     hkd = w.hkv * w.d
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
     if ctx.n > 1:

@@ -4,8 +4,9 @@ Run in the build container (the only place ``/root/reference`` exists):
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
 
-Writes ``tests/golden/golden_kernels.npz``, ``golden_strategies.npz`` and
-``golden_c1.npz``.  The GPU box never reads ``/root/reference``; it only
+Writes ``tests/golden/golden_kernels.npz``, ``golden_strategies.npz``,
+``golden_c1.npz``, ``golden_mllm_ca.npz`` and ``golden_mllm_stack.npz``
+(``--only mllm``: just the last).  The GPU box never reads ``/root/reference``; it only
 reads these committed fixtures.  Inputs come from the reference's own
 ``seeded_random_tensor`` (Philox) and are stored alongside the outputs.
 """
@@ -144,5 +145,59 @@ def main() -> None:
         print(f, (OUT / f).stat().st_size, "bytes")
 
 
+def make_mllm_stack() -> None:
+    """Full toy-MLLM stack: several LM blocks with CA
+    layers sharing one y, both policies, ledgers, measured activation bytes
+    and max_frames_under_budget answers -> golden_mllm_stack.npz."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import json
+    from dataclasses import replace as _replace
+    from lvxattn.mllm import (TOY_CONFIG, ActivationPolicy, ModelParams, OpCounter,
+                              ToyMllmConfig, analytic_ledger, max_frames_under_budget,
+                              measured_activation_bytes, mllm_backward, mllm_forward)
+    from lvxattn.tensorio import seeded_random_tensor as srt
+    cfg = ToyMllmConfig(num_lm_blocks=5, ca_positions=(0, 2, 3), d_embed=16, h=2, d=8,
+                        frames=3, tokens_per_frame=11, s_q=10, dtype="f64")
+    params = ModelParams.init_random(cfg, seed=5)
+    x0 = srt(71, (cfg.s_q, cfg.d_embed))
+    y = srt(72, (cfg.s_kv, cfg.d_embed))
+    gout = srt(73, (cfg.s_q, cfg.d_embed))
+    out = {"config": np.array(json.dumps(cfg.as_dict())), "x0": x0, "y": y, "g": gout}
+    for pos, p in params.ca.items():
+        for n in ("w_q", "w_k", "w_v", "w_o"):
+            out[f"p_ca{pos}_{n}"] = getattr(p, n)
+    for i, p in enumerate(params.lm):
+        out[f"p_lm{i}_w1"], out[f"p_lm{i}_w2"] = p.w1, p.w2
+    for pol in (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV):
+        o, saved, ledger = mllm_forward(x0, y, params, cfg, pol)
+        cnt = OpCounter()
+        gr = mllm_backward(gout, saved, y, params, cfg, pol, counter=cnt)
+        t = pol.value
+        out[f"{t}_out"], out[f"{t}_dx0"], out[f"{t}_dy"] = o, gr.d_x0, gr.d_y
+        for pos, gp in gr.ca.items():
+            for n in ("w_q", "w_k", "w_v", "w_o"):
+                out[f"{t}_g_ca{pos}_{n}"] = getattr(gp, n)
+        for i, gp in enumerate(gr.lm):
+            out[f"{t}_g_lm{i}_w1"], out[f"{t}_g_lm{i}_w2"] = gp.w1, gp.w2
+        out[f"{t}_flops"] = np.array(cnt.projection_flops)
+        out[f"{t}_ledger"] = np.array(json.dumps(ledger.as_dict()))
+        out[f"{t}_measured"] = np.array(json.dumps(measured_activation_bytes(saved)))
+    # ledgers and frame budgets of the shipped TOY_CONFIG and a bf16-sized variant
+    budgets = [1 << 20, 5 << 20, 64 << 20, 1 << 30]
+    for name, c in (("toy", TOY_CONFIG), ("toy_f32_many", _replace(TOY_CONFIG, frames=256))):
+        for pol in (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV):
+            out[f"{name}_{pol.value}_ledger"] = np.array(json.dumps(analytic_ledger(c, pol).as_dict()))
+            out[f"{name}_{pol.value}_frames"] = np.array(
+                [max_frames_under_budget(c, pol, b) for b in budgets])
+    out["budgets"] = np.array(budgets)
+    np.savez_compressed(OUT / "golden_mllm_stack.npz", **out)
+    print("golden_mllm_stack.npz", (OUT / "golden_mllm_stack.npz").stat().st_size, "bytes")
+
+
 if __name__ == "__main__":
-    main()
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "mllm":
+        make_mllm_stack()
+    else:
+        main()
+        make_mllm_stack()

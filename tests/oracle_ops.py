@@ -104,6 +104,16 @@ class OracleOps:
             dk.copy_(gk)
             dv.copy_(gv)
 
+    def kv_recompute(self, y, w_k, w_v, k_out, v_out):
+        h = k_out.shape[0]
+        for w, out in ((w_k, k_out), (w_v, v_out)):
+            out.copy_(torch.from_numpy(orc.project(_np(y), _np(w), h)).to(out.dtype))
+
+    def project_backward(self, x, W, d_out, dx, dw):
+        gx, gw = orc.project_backward(_np(x), _np(W), _np(d_out))
+        dx.copy_(torch.from_numpy(np.asarray(gx)).to(dx.dtype))
+        dw.copy_(torch.from_numpy(np.asarray(gw)).to(dw.dtype))
+
     @staticmethod
     def event():
         return time.perf_counter()

@@ -128,3 +128,54 @@ def test_ca_block_matches_reference_mllm(golden_mllm_ca):
     # the recompute policy does exactly two extra y projections (mllm.py:358-363)
     s_kv = g["y"].shape[0]
     assert int(g["recompute_flops"]) - int(g["store_flops"]) == 2 * 2 * s_kv * e * h * d
+
+
+def _stack_golden():
+    import json
+    from tests.conftest import GOLDEN
+    g = dict(np.load(GOLDEN / "golden_mllm_stack.npz"))
+    cfg = json.loads(str(g["config"]))
+    ca = {p: tuple(g[f"p_ca{p}_{n}"] for n in ("w_q", "w_k", "w_v", "w_o"))
+          for p in cfg["ca_positions"]}
+    lm = [(g[f"p_lm{i}_w1"], g[f"p_lm{i}_w2"]) for i in range(cfg["num_lm_blocks"])]
+    return g, cfg, ca, lm
+
+
+@pytest.mark.parametrize("policy", ["store", "recompute"])
+def test_mllm_stack_matches_reference(policy):
+    """The oracle's toy-MLLM stack (mllm.py:274-371) vs the reference's own
+    forward/backward on a 5-block, 3-CA-layer f64 model."""
+    g, cfg, ca, lm = _stack_golden()
+    out, saved = orc.mllm_stack_forward(g["x0"], g["y"], ca, lm, cfg["ca_positions"], cfg["h"],
+                                        store_kv=policy == "store")
+    assert orc.max_norm_error(out, g[f"{policy}_out"]) <= 1e-12
+    dx0, dy, cag, lmg = orc.mllm_stack_backward(g["g"], saved, g["y"], ca, lm,
+                                                cfg["ca_positions"], cfg["h"])
+    assert orc.max_norm_error(dx0, g[f"{policy}_dx0"]) <= 1e-12
+    assert orc.max_norm_error(dy, g[f"{policy}_dy"]) <= 1e-12
+    for p, gw in cag.items():
+        for n, arr in zip(("w_q", "w_k", "w_v", "w_o"), gw):
+            assert orc.max_norm_error(arr, g[f"{policy}_g_ca{p}_{n}"]) <= 1e-12
+    for i, (g1, g2) in enumerate(lmg):
+        assert orc.max_norm_error(g1, g[f"{policy}_g_lm{i}_w1"]) <= 1e-12
+        assert orc.max_norm_error(g2, g[f"{policy}_g_lm{i}_w2"]) <= 1e-12
+
+
+def test_mllm_ledger_and_frames_match_reference():
+    import json
+    g, cfg, _, _ = _stack_golden()
+    toy = dict(num_lm_blocks=8, num_ca_layers=4, d_embed=128, h=2, d=64, s_q=64)   # TOY_CONFIG
+    for name, frames in (("toy", 16), ("toy_f32_many", 256)):
+        for pol in ("store", "recompute"):
+            led = orc.analytic_ledger(**toy, s_kv=frames * 729, store_kv=pol == "store", b=4)
+            assert led == json.loads(str(g[f"{name}_{pol}_ledger"])), (name, pol)
+            got = [orc.max_frames_under_budget(
+                lambda f, p=pol: orc.analytic_ledger(**toy, s_kv=f * 729, store_kv=p == "store",
+                                                     b=4)["peak_total"], int(bud))
+                   for bud in g["budgets"]]
+            assert got == list(g[f"{name}_{pol}_frames"]), (name, pol, got)
+    for pol in ("store", "recompute"):
+        led = orc.analytic_ledger(cfg["num_lm_blocks"], len(cfg["ca_positions"]), cfg["d_embed"],
+                                  cfg["h"], cfg["d"], cfg["s_q"],
+                                  cfg["frames"] * cfg["tokens_per_frame"], pol == "store", b=8)
+        assert led == json.loads(str(g[f"{pol}_ledger"]))
