@@ -6,7 +6,7 @@ Run in the build container (the only place ``/root/reference`` exists):
 
 Writes ``tests/golden/golden_kernels.npz``, ``golden_strategies.npz``,
 ``golden_c1.npz``, ``golden_mllm_ca.npz`` and ``golden_mllm_stack.npz``
-(``--only mllm``: just the last).  The GPU box never reads ``/root/reference``; it only
+and ``golden_analytics.json`` (``--only mllm`` / ``--only analytics``: one of them).  The GPU box never reads ``/root/reference``; it only
 reads these committed fixtures.  Inputs come from the reference's own
 ``seeded_random_tensor`` (Philox) and are stored alongside the outputs.
 """
@@ -195,9 +195,44 @@ def make_mllm_stack() -> None:
     print("golden_mllm_stack.npz", (OUT / "golden_mllm_stack.npz").stat().st_size, "bytes")
 
 
+def make_analytics() -> None:
+    """The reference's cost model (analytics.py) on a grid of workloads and the
+    shipped presets -> golden_analytics.json (§8(f) next 3)."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import json
+    from lvxattn import analytics as A
+    hw = A.HardwareSpec(1665.5e12, 900e9)
+    cases = [(2048, 1 << 20, 32, 128, 8, 2), (5514, 1 << 18, 28, 128, 4, 2), (1024, 524288, 8, 64, 8, 2),
+             (128, 4096, 8, 64, 2, 4), (7, 0, 2, 4, 3, 8), (1000, 1000, 4, 16, 1, 4)]
+    out = {"hw": [hw.gpu_flops, hw.net_bandwidth], "cases": []}
+    for (sq, skv, h, d, n, b) in cases:
+        w = A.WorkloadSpec(s_q=sq, s_kv=skv, h=h, d=d, n=n, elem_bytes=b)
+        out["cases"].append({
+            "w": [sq, skv, h, d, n, b],
+            "round_times": {k: v.as_dict() for k, v in A.round_times(w, hw).items()},
+            "speedup": A.speedup(w, hw), "closed_form": A.speedup_closed_form(w, hw),
+            "regime": A.classify_regime(w, hw).as_dict(),
+            "volume_report": A.volume_report(w) if sq and skv else None})
+    out["memory"] = A.memory_cross_attention(2048, 1 << 20, 4096, 2)
+    out["video"] = [vars(A.workload_from_video(m, 600, 1, 512, 8)) for m in sorted(A.TOKENS_PER_FRAME)]
+    out["presets"] = {k: {"w": vars(p.workload), "d_model": p.d_model}
+                      for k, p in A.PRESETS.items()}
+    grid = A.grid_values(256, 65536, 5)
+    out["grid"] = grid
+    out["sweep_csv"] = A.format_sweep_csv(A.sweep(grid, A.grid_values(1 << 16, 1 << 24, 4), hw,
+                                                  32, 128, 8, 2))
+    (OUT / "golden_analytics.json").write_text(json.dumps(out, indent=0, sort_keys=True))
+    print("golden_analytics.json", (OUT / "golden_analytics.json").stat().st_size, "bytes")
+
+
 if __name__ == "__main__":
-    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "mllm":
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
+    if only == "mllm":
         make_mllm_stack()
+    elif only == "analytics":
+        make_analytics()
     else:
         main()
         make_mllm_stack()
+        make_analytics()
