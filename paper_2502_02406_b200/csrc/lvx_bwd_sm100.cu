@@ -68,7 +68,7 @@ struct BwdParams {
   float* ws_dq;       // [splits][hq][rows_q][D]
   int debug;          // LVX_BWD_DEBUG (profiling only): 1 = skip exp / dS math,
                       // 2 = also skip Q/dO reloads (dkv), 3 = skip reloads only,
-                      // 4 = skip the dK/dV drain
+                      // 4 = skip the dK/dV drain, 5 = no nL/nD shared loads (dkv)
 };
 
 // ============================================================ dK / dV kernel
@@ -167,7 +167,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
         const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
         uint8_t* slot = sSlot + s * C::SLOT;
-        if (p.debug >= 2 && u > 0) {   // profiling only: no reload latency (stale data)
+        if ((p.debug == 2 || p.debug == 3) && u > 0) {   // profiling: no reloads (stale data)
           mbar_arrive(&qd_full[s]);
           continue;
         }
@@ -276,7 +276,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         } else {
 #pragma unroll
           for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 l4 = ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
+            const float4 l4 = p.debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
+                                           : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
             const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
             const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
             const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
@@ -318,7 +319,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         } else {
 #pragma unroll
           for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 d4 = ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
+            const float4 d4 = p.debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                           : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
             const int pi = (hh * 32 + c4) / 2;
             const float2 t0 = fadd2(u2f2(gv[c4], gv[c4 + 1]), make_float2(d4.x, d4.y));
             const float2 t1 = fadd2(u2f2(gv[c4 + 2], gv[c4 + 3]), make_float2(d4.z, d4.w));
