@@ -37,6 +37,7 @@ using namespace sm100;
 constexpr int kStep = 64;      // q rows per step (dkv kernel) / kv rows per step (dq kernel)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kPolyPairs = 3;   // of every 8 column pairs, exp2 by polynomial (FMA pipe)
+constexpr int kPolyPairsDkv = 2; // the same for the dK/dV kernel's phase A
 
 // ------------------------------------------------------------------- prep
 __global__ void bwd_prep_kernel(View3<const float> L, View3<const float> Dv, int hq, int rows,
@@ -281,8 +282,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
             const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
             const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
-            const float2 p0 = (pi % 8) < kPolyPairs ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
-            const float2 p1 = ((pi + 1) % 8) < kPolyPairs ? ex2_poly2(x1)
+            const float2 p0 = (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
+            const float2 p1 = ((pi + 1) % 8) < kPolyPairsDkv ? ex2_poly2(x1)
                                                           : make_float2(ex2(x1.x), ex2(x1.y));
             pp[pi] = pack_bf16(p0.x, p0.y);
             pp[pi + 1] = pack_bf16(p1.x, p1.y);
