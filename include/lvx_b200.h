@@ -144,6 +144,10 @@ int lvx_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
                        double scale, void* workspace, size_t workspace_bytes, void* stream);
 int lvx_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq_acc,
                       int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+/* lvx_bwd_dkv: dk_acc / dv_acc in the state dtype (accumulate 0 or 1), or -- for
+ * BF16 inputs with accumulate == 0 -- in BF16, written straight from the
+ * tensor-core epilogue (the reference's output-dtype convention); BF16 outputs
+ * on shapes the tensor-core kernel does not take return LVX_EUNSUPPORTED. */
 int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v,
                 const lvx_view* l, const lvx_view* dd, const lvx_view* d_o, double scale,
                 const lvx_view* dk_acc, const lvx_view* dv_acc, int accumulate,

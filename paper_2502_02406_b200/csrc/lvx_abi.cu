@@ -239,11 +239,17 @@ int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const l
                 const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, void* stream) {
   int s = check_bwd_inputs(q, k, v, L, D, dO);
   if (s) return s;
-  const int sd = state_dtype(q->dtype);
+  // dK / dV in the state dtype (any mode) or, overwriting, in the bf16 input
+  // dtype straight from the tensor-core epilogue
+  const bool in_dtype = q->dtype == LVX_BF16 && dk && dv && dk->dtype == LVX_BF16 &&
+                        dv->dtype == LVX_BF16;
+  const int sd = in_dtype ? LVX_BF16 : state_dtype(q->dtype);
   if ((s = check_acc(dk, k, sd)) || (s = check_acc(dv, k, sd))) return s;
+  if (in_dtype && accumulate) return LVX_EDTYPE;
   if (ws_bytes < lvx_bwd_workspace(q, k)) return LVX_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k->heads * k->rows == 0) return LVX_OK;
+  if (in_dtype && !use_tc_bwd(q, k, v, dO, dk, dv)) return LVX_EUNSUPPORTED;
   if (use_tc_bwd(q, k, v, dO, dk, dv))
     return tc_bwd_dkv(q, k, v, L, D, dO, scale, dk, dv, accumulate, ws, ws_bytes, st);
   if (q->heads * q->rows == 0) {

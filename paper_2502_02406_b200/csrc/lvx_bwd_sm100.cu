@@ -64,7 +64,8 @@ struct BwdParams {
   const float* Lp;    // [hq][rows_pad]
   const float* Dp;
   int accumulate;     // dK / dV: TMA reduce-add into the fp32 accumulators (else store)
-  float* dk_ptr; float* dv_ptr;   // fp32 outputs [hkv][rows_kv][D] (strided)
+  void* dk_ptr; void* dv_ptr;     // outputs [hkv][rows_kv][D] (strided): fp32, or bf16
+  int out_bf16;                   //   when overwriting in the input dtype
   int64_t dk_hs, dk_rs, dv_hs, dv_rs;
   float* ws_dq;       // [splits][hq][rows_q][D]
   int debug;          // LVX_BWD_DEBUG (profiling only): 1 = skip exp / dS math,
@@ -368,10 +369,31 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (!p.accumulate && p.debug != 4) {   // 4: profiling, no drain
+    if (!p.accumulate && p.out_bf16 && p.debug != 4) {
+      // overwrite in bf16: each 8-lane group packs 64 columns of one row (two
+      // staged 32-column chunks) into one full 128-byte line
+      __nv_bfloat16* base = static_cast<__nv_bfloat16*>(wg ? p.dk_ptr : p.dv_ptr);
+      const int64_t hs = wg ? p.dk_hs : p.dv_hs, rs = wg ? p.dk_rs : p.dv_rs;
+#pragma unroll 1
+      for (int cp = 0; cp < D / 64; ++cp) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3), q8 = lane & 7;
+          const int c = cp * 2 + (q8 >> 2), qq = (q8 & 3) * 2;
+          const uint32_t rb = smem_u32(stage + c * 4096) + rr * 128;
+          const float4 a = ld_shared_f4(rb + ((qq ^ (rr & 7)) << 4));
+          const float4 b = ld_shared_f4(rb + (((qq + 1) ^ (rr & 7)) << 4));
+          const int grow = n0 + q4 * 32 + rr;
+          if (grow < p.rows_kv)
+            *reinterpret_cast<uint4*>(base + g * hs + (int64_t)grow * rs + cp * 64 + q8 * 8) =
+                make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
+                           pack_bf16(b.z, b.w));
+        }
+      }
+    } else if (!p.accumulate && p.debug != 4) {   // 4: profiling, no drain
       // overwrite: each 8-lane group stores one full 128-byte row segment
       // (STG.128, whole lines); measured ~5 % faster than TMA tensor stores here
-      float* base = (wg ? p.dk_ptr : p.dv_ptr);
+      float* base = static_cast<float*>(wg ? p.dk_ptr : p.dv_ptr);
       const int64_t hs = wg ? p.dk_hs : p.dv_hs, rs = wg ? p.dk_rs : p.dv_rs;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
@@ -758,6 +780,12 @@ bool f32_rows_ok(const lvx_view* v) {
          v->row_stride % 4 == 0 && (v->heads <= 1 || v->head_stride % 4 == 0);
 }
 
+// bf16 outputs (dK / dV overwritten in the input dtype): 16-byte aligned rows
+bool bf16_rows_ok(const lvx_view* v) {
+  return v->dtype == LVX_BF16 && (reinterpret_cast<uintptr_t>(v->data) & 15) == 0 &&
+         v->row_stride % 8 == 0 && (v->heads <= 1 || v->head_stride % 8 == 0);
+}
+
 void fill_params(BwdParams& p, const BwdPlan& pl, const lvx_view* q, const lvx_view* k,
                  double scale, void* ws) {
   p.hq = (int)q->heads;
@@ -798,10 +826,11 @@ template <int D>
 int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
                BwdParams p, const lvx_view* dk, const lvx_view* dvv, int accumulate,
                cudaStream_t st) {
-  CUtensorMap mq128, mg128, mk128, mv128, mdk, mdv;
+  CUtensorMap mq128, mg128, mk128, mv128, mdk{}, mdv{};
   if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
-      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128) ||
-      !make_tma_f32_3d(&mdk, dk, 32) || !make_tma_f32_3d(&mdv, dvv, 32))
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
+    return LVX_ECUDA;
+  if (accumulate && (!make_tma_f32_3d(&mdk, dk, 32) || !make_tma_f32_3d(&mdv, dvv, 32)))
     return LVX_ECUDA;
   static bool attr = false;
   if (!attr) {
@@ -811,8 +840,9 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
     attr = true;
   }
   p.accumulate = accumulate;
-  p.dk_ptr = static_cast<float*>(dk->data);
-  p.dv_ptr = static_cast<float*>(dvv->data);
+  p.dk_ptr = dk->data;
+  p.dv_ptr = dvv->data;
+  p.out_bf16 = dk->dtype == LVX_BF16;
   p.dk_hs = dk->head_stride;
   p.dk_rs = dk->row_stride;
   p.dv_hs = dvv->head_stride;
@@ -854,7 +884,8 @@ bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
 }
 
 bool tc_bwd_outputs_ok(const lvx_view* dO, const lvx_view* a, const lvx_view* b) {
-  return tma_view_ok(dO) && (!a || f32_rows_ok(a)) && (!b || f32_rows_ok(b));
+  auto ok = [](const lvx_view* x) { return !x || f32_rows_ok(x) || bf16_rows_ok(x); };
+  return tma_view_ok(dO) && ok(a) && ok(b);
 }
 
 size_t tc_bwd_workspace(const lvx_view* q, const lvx_view* k) {
@@ -905,8 +936,8 @@ int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   if (k->rows == 0) return LVX_OK;
   if (q->rows == 0) {
     if (accumulate) return LVX_OK;
-    int s = fill_zero_f32(dk, st);
-    return s ? s : fill_zero_f32(dv, st);
+    int s = fill_empty_zero(dk, st);
+    return s ? s : fill_empty_zero(dv, st);
   }
   if (ws_bytes < tc_bwd_workspace(q, k)) return LVX_EWORKSPACE;
   const BwdPlan pl = plan_bwd(q, k);

@@ -511,6 +511,9 @@ int fill_empty_zero(const lvx_view* a, cudaStream_t st) {
     zero_state_kernel<float><<<ceil_div(total, threads), threads, 0, st>>>(make_view<float>(a));
   else if (a->dtype == LVX_F64)
     zero_state_kernel<double><<<ceil_div(total, threads), threads, 0, st>>>(make_view<double>(a));
+  else if (a->dtype == LVX_BF16)
+    zero_state_kernel<__nv_bfloat16><<<ceil_div(total, threads), threads, 0, st>>>(
+        make_view<__nv_bfloat16>(a));
   else
     return LVX_EDTYPE;
   return launch_status();

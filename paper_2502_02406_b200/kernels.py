@@ -297,10 +297,21 @@ def bwd_dkv(q, k, v, L, D, d_o, scale: float, dk, dv, accumulate: bool = True,
     """dk/dv (+)= contributions of every query row in q."""
     if ws is None:
         ws = workspace(bwd_ws_bytes(q, k), q.device, slot=2)
-    _lib.check("lvx_bwd_dkv", _lib.load().lvx_bwd_dkv(
+    st = _lib.load().lvx_bwd_dkv(
         _lib.view(q), _lib.view(k), _lib.view(v), _lib.view(L), _lib.view(D), _lib.view(d_o),
         float(scale), _lib.view(dk), _lib.view(dv), int(bool(accumulate)), ws.data_ptr(),
-        ws.numel(), _lib.stream_ptr(q.device)))
+        ws.numel(), _lib.stream_ptr(q.device))
+    sd = state_dtype(q.dtype)
+    if st == -4 and dk.dtype != sd and not accumulate:
+        # bf16 outputs on a shape the tensor-core kernel does not take: the
+        # exact SIMT kernels write the state dtype, converted on the device
+        tk, tv = torch.empty(dk.shape, dtype=sd, device=dk.device), \
+            torch.empty(dv.shape, dtype=sd, device=dv.device)
+        bwd_dkv(q, k, v, L, D, d_o, scale, tk, tv, False, ws)
+        dk.copy_(tk)
+        dv.copy_(tv)
+        return
+    _lib.check("lvx_bwd_dkv", st)
 
 
 def bwd_ws_bytes(q, k) -> int:

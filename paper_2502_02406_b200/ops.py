@@ -21,6 +21,12 @@ class CudaOps:
     def state_dtype(dt: torch.dtype) -> torch.dtype:
         return K.state_dtype(dt)
 
+    @staticmethod
+    def grad_dtype(dt: torch.dtype) -> torch.dtype:
+        """Gradients come back in the input dtype (the reference's convention);
+        dK/dV are written in it directly by the tensor-core epilogue."""
+        return dt
+
     def fwd_workspace(self, q: torch.Tensor, k: torch.Tensor) -> torch.Tensor:
         return K.workspace(K.fwd_workspace_bytes(q, k), q.device, slot=0)
 

@@ -306,7 +306,9 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     """Query-rotation backward (strategies.py:234-276): the tuple
     (Q, dO, L, D, dQ) of every block travels once around the ring and every
     rank adds its K/V block's contribution; the last dQ hop is the
-    homecoming.  Returns (dQ_i, dK_i, dV_i) in the state dtype.
+    homecoming.  Returns (dQ_i, dK_i, dV_i) in the input dtype (the
+    reference's convention): everything is computed and carried in the fp32
+    state dtype and the batched dK/dV pass writes bf16 gradients directly.
 
     B200 schedule (same messages and bytes per rank as the reference; see
     DESIGN.md §5):
@@ -345,8 +347,9 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     l_j = _dev_copy(state.L, Lb.view(cur, qs[i]))
     d_j = Db.view(cur, qs[i])
     ops.row_stats(state.O, do_block, d_j)             # strategies.py:247
-    dk = torch.empty(k_block.shape, dtype=sd, device=dev)
-    dv = torch.empty(v_block.shape, dtype=sd, device=dev)
+    gd = _grad_dtype(ops, q_block.dtype)
+    dk = torch.empty(k_block.shape, dtype=gd, device=dev)   # written once, in gd
+    dv = torch.empty(v_block.shape, dtype=gd, device=dev)
     early_dkv = n == 1 and kv_stream is not None and kv_stream.dkv_done is not None
     if early_dkv:   # n = 1: the rows are all local, so dK/dV first and their chunks
         # leave the GPU while the dQ kernel runs
@@ -420,7 +423,11 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
             ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
         if trace is not None:
             trace.section("dkv_kernel", ops, t4, ops.event())
-    return dq_out, dk, dv
+    return dq_out.to(gd), dk, dv
+
+
+def _grad_dtype(ops, dt):
+    return ops.grad_dtype(dt) if hasattr(ops, "grad_dtype") else ops.state_dtype(dt)
 
 
 def _dkv_chunks(ops, kv_stream: KVStream, q, k_block, v_block, L, D, g, scale, dk, dv):
@@ -540,7 +547,8 @@ def ring_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_blo
     _expect(blk, (i + 1) % n, f"worker {i} backward epilogue")
     if trace is not None:
         trace.epilogue_bytes_by_class = epi
-    return dq, dk, dv
+    gd = _grad_dtype(ctx.ops, q_block.dtype)
+    return dq.to(gd), dk.to(gd), dv.to(gd)
 
 
 # ---------------------------------------------------------------------------
@@ -658,8 +666,10 @@ def head_parallel_backward(ctx: DeviceContext, shards: ShardSpec, saved, do_bloc
                                            "grad_scatter": sum(s_sent.values())})
         trace.section("bwd_kernel", ops, t1, t2)
         trace.section("all_to_all", ops, t0, t1)
-    return (torch.cat([b[0] for b in back], dim=0), torch.cat([b[1] for b in back], dim=0),
-            torch.cat([b[2] for b in back], dim=0))
+    gd = _grad_dtype(ops, do_block.dtype)
+    return (torch.cat([b[0] for b in back], dim=0).to(gd),
+            torch.cat([b[1] for b in back], dim=0).to(gd),
+            torch.cat([b[2] for b in back], dim=0).to(gd))
 
 
 # ---------------------------------------------------------------------------

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--shape", default="c2round")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--bf16-grads", action="store_true", help="dK/dV in bf16 (the lvx path)")
     a = ap.parse_args()
     from paper_2502_02406_b200 import kernels as K
     hq, hkv, sq, skv, d = SHAPES[a.shape]
@@ -68,13 +69,16 @@ def main():
         dq = torch.zeros(hq, sq, d, device=dev)
         dk = torch.zeros(hkv, skv, d, device=dev)
         dv = torch.zeros(hkv, skv, d, device=dev)
+        gdt = torch.bfloat16 if a.bf16_grads else torch.float32
+        dkg = torch.zeros(hkv, skv, d, device=dev, dtype=gdt)
+        dvg = torch.zeros(hkv, skv, d, device=dev, dtype=gdt)
         bf = 10.0 * sq * skv * hq * d
         ms3 = t(lambda: K.bwd_accumulate(q, k, v, L, D, g, scale, dq, dk, dv))
         res["bwd_ms"] = ms3
         res["bwd_tflops"] = bf / ms3 / 1e9
         res["bwd_frac_of_peak"] = res["bwd_tflops"] / peaks["bf16_tflops"]
         wsb = K.workspace(K.bwd_ws_bytes(q, k), dev, slot=3)
-        res["bwd_dkv_ms"] = t(lambda: K.bwd_dkv(q, k, v, L, D, g, scale, dk, dv, False, ws=wsb))
+        res["bwd_dkv_ms"] = t(lambda: K.bwd_dkv(q, k, v, L, D, g, scale, dkg, dvg, False, ws=wsb))
         res["bwd_dq_ms"] = t(lambda: (K.bwd_dq_partial(q, k, v, L, D, g, scale, wsb),
                                       K.bwd_dq_finish(q, k, wsb, dq, True)))
         # tensor work actually issued: dkv 4 GEMMs, dq 3 GEMMs of 2*sq*skv*hq*d each
