@@ -156,6 +156,11 @@ int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v,
 /* ---- utilities ---------------------------------------------------------
  * empty_state (kernels.py:48-53): O = 0, L = -inf. */
 int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream);
+/* Process-wide planner setting: the split / grid planners size their waves
+ * for (SM count - sms) SMs, leaving room for NCCL's send/recv CTAs that run
+ * beside the ring-round kernels (one process per GPU).  Returns the previous
+ * value; 0 (the default) plans for the whole device. */
+int lvx_set_sm_reserve(int sms);
 /* dst = src converted (F32/F64/BF16 <-> F32/F64/BF16), strided views. */
 int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
 

@@ -24,7 +24,7 @@ EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eli
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
            "lvx_fill_empty_state", "lvx_convert", "lvx_bwd_workspace", "lvx_bwd_dq_partial",
            "lvx_bwd_dq_finish", "lvx_bwd_dkv", "lvx_project", "lvx_project_bwd",
-           "lvx_kv_recompute")
+           "lvx_kv_recompute", "lvx_set_sm_reserve")
 
 
 class LvxView(ctypes.Structure):
@@ -85,6 +85,7 @@ def load() -> ctypes.CDLL:
         "lvx_project": (i32, [M, M, P, vp]),
         "lvx_project_bwd": (i32, [M, M, P, M, M, vp]),
         "lvx_kv_recompute": (i32, [M, M, M, P, P, vp]),
+        "lvx_set_sm_reserve": (i32, [i32]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -17,6 +17,7 @@ schedulers' round traces.
 """
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 
@@ -133,6 +134,9 @@ class _Shift:
         self._local = None
 
 
+NCCL_SM_RESERVE = int(os.environ.get("LVX_SM_RESERVE", "4"))   # tuning override
+
+
 class DeviceContext:
     """Per-rank handle: the analogue of ``WorkerContext`` (cluster.py:227-291)
     for one process per GPU.
@@ -158,6 +162,11 @@ class DeviceContext:
             from .ops import CudaOps
             ops = CudaOps()
         self.ops = ops
+        if n > 1 and hasattr(ops, "set_sm_reserve"):
+            # NCCL's send/recv CTAs run beside the ring-round kernels: plan the
+            # grids for 4 SMs fewer (n=4 C2: -2.3 % step time, tools/ab_plan_sms.sh);
+            # the no-comm arm keeps the same plans (same per-rank schedule)
+            ops.set_sm_reserve(NCCL_SM_RESERVE)
         self.stats = TransportStats()
         # comm_enabled=False runs the identical schedule with every hop
         # skipped: the "no-communication" arm of PAPER.md:233.

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -508,6 +509,11 @@ bool make_tma_f32_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
   return r == CUDA_SUCCESS;
 }
 
+// SMs the grid planners leave free (lvx_set_sm_reserve): NCCL's send/recv
+// CTAs share the GPU with the ring-round kernels, and a plan that fills every
+// SM in whole waves then spills a straggler wave.
+std::atomic<int> g_sm_reserve{0};
+
 int device_sms() {
   static int sms = 0;
   if (!sms) {
@@ -516,7 +522,8 @@ int device_sms() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  return sms;
+  const int r = g_sm_reserve.load(std::memory_order_relaxed);
+  return r > 0 && r < sms ? sms - r : sms;
 }
 
 bool is_sm100() {

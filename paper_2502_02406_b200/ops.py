@@ -22,6 +22,12 @@ class CudaOps:
         return K.state_dtype(dt)
 
     @staticmethod
+    def set_sm_reserve(sms: int) -> int:
+        """SMs the kernel planners leave to NCCL (lvx_set_sm_reserve)."""
+        from . import _lib
+        return int(_lib.load().lvx_set_sm_reserve(int(sms)))
+
+    @staticmethod
     def grad_dtype(dt: torch.dtype) -> torch.dtype:
         """Gradients come back in the input dtype (the reference's convention);
         dK/dV are written in it directly by the tensor-core epilogue."""
