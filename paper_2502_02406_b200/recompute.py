@@ -115,13 +115,53 @@ def project_kv(ctx: DeviceContext, y: torch.Tensor, w: CrossAttentionWeights):
     return k, v
 
 
+# RECOMPUTE_KV at n = 1 projects, attends and merges K/V in chunks of this many
+# visual rows, so the layer never holds more than one chunk's K/V (the
+# reference materialises the whole layer's K/V, mllm.py:294-295, :358-360).
+KV_CHUNK_ROWS = 1 << 17
+
+
+def _row_chunks(rows: int, chunk: int):
+    return [(a, min(a + chunk, rows)) for a in range(0, rows, chunk)]
+
+
+def _chunked(ctx: DeviceContext, policy: ActivationPolicy, strategy: str, y_rows: int,
+             kv_chunk_rows: int | None) -> bool:
+    return (kv_chunk_rows is not None and ctx.n == 1 and strategy == "lvx" and
+            policy is ActivationPolicy.RECOMPUTE_KV and y_rows > kv_chunk_rows)
+
+
+def _attend_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, scale: float,
+                    chunk: int) -> AttentionState:
+    """n = 1 forward over K/V chunks: partial + fused LSE merge per chunk."""
+    ops = ctx.ops
+    sd = ops.state_dtype(q.dtype)
+    O = torch.empty(q.shape, dtype=sd, device=q.device)
+    L = torch.empty(q.shape[:2], dtype=sd, device=q.device)
+    ops.fill_empty(O, L)
+    for a, b in _row_chunks(y.shape[0], chunk):
+        k, v = project_kv(ctx, y[a:b], w)
+        ws = ops.fwd_workspace(q, k)
+        ops.fwd_partial(q, k, v, scale, ws)
+        ops.fwd_finish(q, k, ws, O, L, O, L)
+        del k, v      # the allocator hands the chunk buffer to the next chunk
+    return AttentionState(O=O, L=L)
+
+
 def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: torch.Tensor,
                w: CrossAttentionWeights, policy: ActivationPolicy = ActivationPolicy.RECOMPUTE_KV,
-               scale: float | None = None, strategy: str = "lvx"):
+               scale: float | None = None, strategy: str = "lvx",
+               kv_chunk_rows: int | None = KV_CHUNK_ROWS):
     """Returns (out_i = x_i + flat(O_i) W_O, saved)."""
     policy = ActivationPolicy(policy)
     scale = default_scale(w.d) if scale is None else scale
     q = _heads(x_i @ w.w_q, w.hq)
+    if _chunked(ctx, policy, strategy, y_i.shape[0], kv_chunk_rows):
+        st = _attend_chunked(ctx, q, y_i, w, scale, kv_chunk_rows)
+        saved = SavedCA(policy=policy, x=x_i, state=st, kv=None)
+        saved.extras["kv_chunk_rows"] = kv_chunk_rows
+        out = x_i + _flat(st.O.to(x_i.dtype)) @ w.w_o
+        return out, saved
     k, v = project_kv(ctx, y_i, w)
     fwd = lvx_forward if strategy == "lvx" else ring_forward
     st = fwd(ctx, shards, q, k, v, scale)
@@ -145,32 +185,69 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     q = _heads(saved.x @ w.w_q, w.hq)
     if counter is not None:
         counter.add(saved.x.shape[0], w.w_q.shape[0], w.w_q.shape[1])
-    if saved.policy is ActivationPolicy.STORE_KV:
-        k, v = saved.kv
-    else:   # the MLLM-specific recompute from the one shared y
-        k, v = project_kv(ctx, y_i, w)
+    hkd = w.hkv * w.d
+    wkv = w.kv_weight()
+    chunk = saved.extras.get("kv_chunk_rows")
+    if chunk:   # n = 1 RECOMPUTE in K/V chunks (see _attend_chunked)
         if counter is not None:
             counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
             counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
-    bwd = lvx_backward if strategy == "lvx" else ring_backward
-    dq, dk, dv = bwd(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
-    del k, v
-    dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
+        dq, d_y, g_wkv = _backward_chunked(ctx, q, y_i, w, wkv, saved.state,
+                                           d_o.to(q.dtype), scale, chunk)
+        dq = _flat(dq.to(dt))
+    else:
+        if saved.policy is ActivationPolicy.STORE_KV:
+            k, v = saved.kv
+        else:   # the MLLM-specific recompute from the one shared y
+            k, v = project_kv(ctx, y_i, w)
+            if counter is not None:
+                counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
+                counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
+        bwd = lvx_backward if strategy == "lvx" else ring_backward
+        dq, dk, dv = bwd(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
+        del k, v
+        dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
+        dkv = torch.cat([dk, dv], dim=1)
+        d_y = torch.empty_like(y_i)
+        g_wkv = torch.empty_like(wkv)
+        ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
     d_x = torch.empty_like(g_i)
     g_wq = torch.empty_like(w.w_q)
     ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
     d_x += g_i
-    dkv = torch.cat([dk, dv], dim=1)
-    wkv = w.kv_weight()
-    d_y = torch.empty_like(y_i)
-    g_wkv = torch.empty_like(wkv)
-    ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
-    hkd = w.hkv * w.d
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
     if ctx.n > 1:
         for t in (g_wq, g_wk, g_wv, g_wo):
             dist.all_reduce(t, group=group if group is not None else ctx.group)
     return CrossAttentionGrads(d_x=d_x, d_y=d_y, w_q=g_wq, w_k=g_wk, w_v=g_wv, w_o=g_wo)
+
+
+def _backward_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, wkv, state,
+                      d_o, scale: float, chunk: int):
+    """n = 1 backward over K/V chunks: per chunk re-project K/V, add its dQ
+    contribution (fp32, in place), compute its dK/dV and fold them into the
+    chunk's d_y rows and the K/V weight gradient.  Returns (dQ, d_y, g_wkv)."""
+    ops = ctx.ops
+    sd = ops.state_dtype(q.dtype)
+    D = torch.empty(state.L.shape, dtype=sd, device=q.device)
+    ops.row_stats(state.O, d_o, D)
+    dq = torch.empty(q.shape, dtype=sd, device=q.device)
+    d_y = torch.empty_like(y)
+    g_wkv = torch.zeros(wkv.shape, dtype=sd, device=y.device)
+    part = torch.empty_like(wkv)
+    hkd = w.hkv * w.d
+    for c, (a, b) in enumerate(_row_chunks(y.shape[0], chunk)):
+        k, v = project_kv(ctx, y[a:b], w)
+        ws = ops.bwd_workspace(q, k)
+        ops.bwd_dq_partial(q, k, v, state.L, D, d_o, scale, ws)
+        ops.bwd_dq_finish(q, k, ws, dq, accumulate=c > 0)
+        dkv = torch.empty((b - a, 2 * hkd), dtype=y.dtype, device=y.device)
+        ops.bwd_dkv(q, k, v, state.L, D, d_o, scale, _heads(dkv[:, :hkd], w.hkv),
+                    _heads(dkv[:, hkd:], w.hkv), accumulate=False)
+        del k, v
+        ops.project_backward(y[a:b], wkv, _heads(dkv, 2 * w.hkv), d_y[a:b], part)
+        g_wkv += part
+    return dq, d_y, g_wkv.to(wkv.dtype)
 
 
 def activation_bytes(saved: SavedCA) -> int:

@@ -26,6 +26,10 @@ class OracleOps:
     def state_dtype(dt):
         return torch.float64 if dt == torch.float64 else torch.float32
 
+    @staticmethod
+    def grad_dtype(dt):
+        return OracleOps.state_dtype(dt)
+
     def fwd_workspace(self, q, k):
         return {}
 

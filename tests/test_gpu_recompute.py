@@ -68,3 +68,52 @@ def test_recompute_layer_vs_oracle():
              ("w_k", gr.w_k, rk), ("w_v", gr.w_v, rv), ("w_o", gr.w_o, rwo))}
     print("\nrecompute CA layer bf16 vs f64 oracle:", errs)
     assert max(errs.values()) <= 3e-2   # bf16 projections + bf16 attention operands
+
+
+def test_chunked_recompute_matches_unchunked():
+    """n = 1 RECOMPUTE_KV in K/V chunks (3 chunks + a ragged tail) vs the
+    one-shot layer: same outputs and gradients up to the chunked merge /
+    fp32 dQ accumulation order, i.e. bf16 rounding flips (max-normalised
+    1e-2 as the other bf16 tests; one bf16 ulp near the max is ~7e-3), same
+    recompute FLOP."""
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200.recompute import ActivationPolicy, OpCounter, ca_backward, ca_forward
+    w, x, y, g, _ = _setup()
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
+    res, ops = {}, {}
+    for chunk in (None, 200):
+        out, saved = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, kv_chunk_rows=chunk)
+        cnt = OpCounter()
+        gr = ca_backward(ctx, sh, g, saved, y, w, counter=cnt)
+        res[chunk] = [out, gr.d_x, gr.d_y, gr.w_q, gr.w_k, gr.w_v, gr.w_o]
+        ops[chunk] = cnt.projection_flops
+    for a, b in zip(res[None], res[200]):
+        err = orc.max_norm_error(b.double().cpu().numpy(), a.double().cpu().numpy())
+        assert err <= 1e-2, err
+    assert ops[None] == ops[200]
+
+
+def test_chunked_recompute_bounds_kv_transient():
+    """The forward's peak allocation under chunked recompute stays below the
+    one-shot layer's by about the full K/V minus one chunk."""
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200.recompute import ActivationPolicy, ca_forward
+    w, x, _, _, _ = _setup(e=256, hq=4, hkv=2, d=64, sq=128, skv=64)
+    y = (torch.rand(65536, 256, device="cuda") * 2 - 1).bfloat16()
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
+    peaks = {}
+    for chunk in (None, 8192):
+        ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, kv_chunk_rows=chunk)  # warm-up
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        out, saved = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, kv_chunk_rows=chunk)
+        torch.cuda.synchronize()
+        peaks[chunk] = torch.cuda.max_memory_allocated() - base
+        del out, saved
+    full_kv = 2 * 65536 * w.hkv * w.d * 2
+    chunk_kv = 2 * 8192 * w.hkv * w.d * 2
+    assert peaks[None] - peaks[8192] >= 0.9 * (full_kv - chunk_kv), (peaks, full_kv)
