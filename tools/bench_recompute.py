@@ -1,6 +1,7 @@
 """K/V recompute overhead of one cross-attention layer (§3.2, the
 "< 8 %" claim) on one B200: ca_forward + ca_backward under STORE_KV vs
-RECOMPUTE_KV, bf16, CUDA-event timed, and the activation bytes each keeps.
+RECOMPUTE_KV, bf16, CUDA-event timed in 5 interleaved rounds (median; clocks
+drift under the power cap), and the activation bytes each keeps.
 
     python tools/bench_recompute.py [--preset flamingo|llama] [--iters N]
 """
@@ -38,22 +39,38 @@ def main():
     ctx = lvx.DeviceContext(0, 1)
     sh = lvx.ShardSpec.balanced(sq, skv, 1)
     out = {"preset": a.preset, "dims": [e, hq, hkv, d, sq, skv]}
-    for pol in (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV):
-        def step():
-            o, saved = ca_forward(ctx, sh, x, y, w, pol)
-            ca_backward(ctx, sh, go, saved, y, w)
-            return saved
+    pols = (ActivationPolicy.STORE_KV, ActivationPolicy.RECOMPUTE_KV)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    times = {p: {"fwd": [], "bwd": [], "step": []} for p in pols}
+    saved_of = {}
+    for p in pols:   # warm-up both
         for _ in range(2):
-            saved = step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.iters):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        out[pol.value] = {"ms": e0.elapsed_time(e1) / a.iters,
-                          "activation_bytes": activation_bytes(saved)}
+            o, sv = ca_forward(ctx, sh, x, y, w, p)
+            ca_backward(ctx, sh, go, sv, y, w)
+    torch.cuda.synchronize()
+    # interleaved rounds (clocks drift under the power cap): median per policy
+    for _ in range(5):
+        for p in pols:
+            tf = tb = 0.0
+            for _ in range(a.iters):
+                e0, e1, e2 = ev(), ev(), ev()
+                e0.record()
+                o, sv = ca_forward(ctx, sh, x, y, w, p)
+                e1.record()
+                ca_backward(ctx, sh, go, sv, y, w)
+                e2.record()
+                torch.cuda.synchronize()
+                tf += e0.elapsed_time(e1)
+                tb += e1.elapsed_time(e2)
+                saved_of[p] = sv
+            times[p]["fwd"].append(tf / a.iters)
+            times[p]["bwd"].append(tb / a.iters)
+            times[p]["step"].append((tf + tb) / a.iters)
+    med = lambda xs: sorted(xs)[len(xs) // 2]  # noqa: E731
+    for p in pols:
+        out[p.value] = {"ms": med(times[p]["step"]), "fwd_ms": med(times[p]["fwd"]),
+                        "bwd_ms": med(times[p]["bwd"]),
+                        "activation_bytes": activation_bytes(saved_of[p])}
     out["recompute_overhead"] = out["recompute"]["ms"] / out["store"]["ms"] - 1.0
     out["activation_saving_bytes"] = out["store"]["activation_bytes"] - \
         out["recompute"]["activation_bytes"]
