@@ -234,3 +234,33 @@ def test_tc_kernels_bit_deterministic(shape):
         else:
             for a, b in zip(cur, base):
                 assert torch.equal(a, b)
+
+
+def _random_shapes(n=12, seed=2502):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        hkv = int(rng.choice([1, 2, 3, 4, 8]))
+        hq = hkv * int(rng.choice([1, 2, 4, 8]))
+        out.append((hq, hkv, int(rng.integers(1, 300)), int(rng.integers(1, 2600)),
+                    int(rng.choice([64, 128]))))
+    return out
+
+
+@pytest.mark.parametrize("shape", _random_shapes())
+def test_tc_random_shapes_fwd_bwd_vs_oracle(shape):
+    """Seeded random GQA shapes (ragged rows, tiny and single-row blocks) through
+    the bf16 tensor-core path: the full LV-XAttn layer at n = 1 (forward, dQ
+    and the batched bf16 dK/dV pass) against the f64 oracle, 1e-2."""
+    import paper_2502_02406_b200 as lvx
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(hq, hkv, sq, skv, d, seed=sum(shape))
+    ctx = lvx.DeviceContext(0, 1)
+    st, (dq, dk, dv), _, _ = lvx.run_rank("lvx", ctx, lvx.ShardSpec.balanced(sq, skv, 1),
+                                          q, k, v, g)
+    O, L = orc.dense_attention(Q, K, V)
+    dQ, dK, dV = orc.dense_attention_backward(Q, K, V, O, L, G)
+    got = {"O": st.O, "L": st.L, "dQ": dq, "dK": dk, "dV": dv}
+    errs = {n: orc.max_norm_error(t.double().cpu().numpy(), ref)
+            for (n, t), ref in zip(got.items(), (O, L, dQ, dK, dV))}
+    assert max(errs.values()) <= TOL_BF16, (shape, errs)

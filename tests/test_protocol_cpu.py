@@ -209,3 +209,24 @@ def test_gloo_lvx_kv_stream_chunks(n):
     assert max(errs) <= 1e-12, errs
     assert waited == [0, 1, 2]
     assert chunks_ok
+
+
+def test_gloo_n8_protocols_vs_oracle_simulation():
+    """The rank count of the driver's largest scaling run (n = 8) over gloo:
+    lvx / ring / head-parallel forward + backward with uneven shards (13 query
+    rows) and empty ones (5 query rows: three ranks hold none) against the
+    oracle's rank-by-rank simulation of the reference schedule (f64, 1e-12),
+    per-rank byte counters included for the ring protocols."""
+    cases = []
+    for sq, skv, seed in ((13, 37, 81), (5, 19, 82)):
+        Q, K, V, dO = orc.make_inputs(sq, skv, 8, 4, seed)
+        for strategy in ("lvx", "ring", "head"):
+            cases.append((strategy, Q, K, V, dO))
+    outs = run_group(8, cases)
+    for (strategy, Q, K, V, dO), (O, L, dQ, dK, dV, fb, bb, sb, rounds) in zip(cases, outs):
+        sim = orc.simulate(strategy, Q, K, V, dO, n=8)
+        for name, arr in (("O", O), ("L", L), ("dQ", dQ), ("dK", dK), ("dV", dV)):
+            assert orc.max_norm_error(arr, getattr(sim, name)) <= 1e-12, (strategy, Q.shape, name)
+        if strategy != "head":
+            assert fb == list(sim.fwd_bytes), (strategy, fb, sim.fwd_bytes)
+            assert bb == list(sim.bwd_bytes), (strategy, bb, sim.bwd_bytes)
