@@ -268,7 +268,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
                 // decltype(poly)::value of every 8 pairs take exp2 on the FMA
                 // pipe: MUFU.EX2 alone would set the pace (2 x 128 per
                 // sub-partition per KV tile ~ the tile's MMA time)
-                const float2 pp = ((e / 2) % 8) < decltype(poly)::value
+                const float2 pp = ((((c * 16 + e / 2) * 3) % 8) < decltype(poly)::value)
                                       ? ex2_poly2(x)
                                       : make_float2(ex2(x.x), ex2(x.y));
                 acc = fadd2(acc, pp);
