@@ -629,7 +629,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
               x.x = c < nvalid ? x.x : -INFINITY;
               x.y = c + 1 < nvalid ? x.y : -INFINITY;
             }
-            const float2 pq = ((c / 2) % 8) < kPolyPairs && !decltype(masked)::value
+            const float2 pq = (((c / 2) * 3) % 8) < kPolyPairs && !decltype(masked)::value
                                   ? ex2_poly2(x)
                                   : make_float2(ex2(x.x), ex2(x.y));
             pf[c / 2] = pq;
