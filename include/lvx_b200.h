@@ -22,7 +22,10 @@
  *     F32/BF16 inputs and F64 for F64 inputs.
  *   - Every call is asynchronous on the caller's cudaStream_t, never
  *     synchronises the host, allocates nothing (scratch comes from the
- *     caller's workspace) and keeps no global mutable state.
+ *     caller's workspace) and keeps no global mutable state -- except two
+ *     documented process-wide items: the planner's SM reserve
+ *     (lvx_set_sm_reserve) and the cached per-device cuBLAS handle of the
+ *     three projection calls (which also use cuBLAS's own workspace).
  *   - Return value: LVX_OK (0) or a negative lvx_status.  The Python shim
  *     maps LVX_EINVAL/LVX_EDTYPE to ValueError with the reference messages
  *     (kernels.py:62-73) and LVX_ECUDA to RuntimeError.
