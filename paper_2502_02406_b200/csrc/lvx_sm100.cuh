@@ -110,15 +110,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// shared -> global tensor store / reduce-add (bulk-group completion)
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1,
-                                             int c2, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint"
-      " [%0, {%2, %3, %4}], [%1], %5;" ::"l"(reinterpret_cast<uint64_t>(m)),
-      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
-      : "memory");
-}
+// shared -> global tensor reduce-add (bulk-group completion)
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, const void* src, int c0,
                                                   int c1, int c2, uint64_t policy) {
   asm volatile(
@@ -220,9 +212,6 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   float2 r;
   asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
   return r;
-}
-__device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
-  return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
 }
 __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
@@ -326,20 +315,12 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x on the FMA pipe (offloads the MUFU unit, which bounds softmax on B200):
 // round-to-nearest split x = j + f, f in [-0.5, 0.5], degree-3 minimax of 2^f
 // (max relative error 7.5e-5, far below bf16 rounding of P), exponent add.
-__device__ __forceinline__ float ex2_poly(float x) {
-  // clamp at -126: p(0) = 0.99993 has exponent 126, so j >= -126 keeps the
-  // biased exponent >= 0 (x = -inf, e.g. padded rows with L = +inf, -> ~1e-38)
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;          // 1.5 * 2^23
-  const float j = t - 12582912.f;
-  const float f = x - j;
-  const float p = fmaf(fmaf(fmaf(0.0551716531f, f, 0.2426111615f), f, 0.6932609919f), f,
-                       0.9999280713f);
-  const int ji = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (ji << 23));
-}
 
-// ex2_poly on a pair with packed FFMA2/FADD2 (10 issue slots per pair, no MUFU).
+// exp2 on a pair on the FMA pipe (packed FFMA2/FADD2, 10 issue slots per pair, no
+// MUFU): x = j + f, j = round(x), f in [-0.5, 0.5]; 2^f by a degree-3 minimax
+// polynomial (rel. error 7.5e-5, below bf16's 2^-9); 2^j added to the exponent
+// bits.  Clamped at -126: p(0) = 0.99993 has exponent 126, so j >= -126 keeps the
+// biased exponent >= 0 (x = -inf, e.g. padded rows, gives ~1e-38, not garbage).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
