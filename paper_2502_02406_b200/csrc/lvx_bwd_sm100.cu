@@ -909,13 +909,16 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.dk_rs = dk->row_stride;
   p.dv_hs = dvv->head_stride;
   p.dv_rs = dvv->row_stride;
-  // Persistent schedule (one CTA per SM looping over tiles) for the bf16
-  // overwrite of the LV-XAttn path; the accumulate / fp32 paths stage their
-  // epilogue in the Q/dO ring and run one tile per CTA.
+  // Persistent schedule (one CTA per SM looping over tiles; bf16 overwrite only,
+  // its drain goes straight from registers since the Q/dO ring feeds the next
+  // tile).  Opt-in (LVX_DKV_PERSIST=1): measured neutral at the N=1 C2 launch
+  // (power-capped), -3 % at N=4 (row-per-lane drain stores), +1..12 % (bimodal)
+  // at the c2gath shape; the default is one tile per CTA with the staged,
+  // coalesced epilogue.
   const int tiles = (int)ceil_div(k->rows, 128) * (int)k->heads;
   static const int persist_env = [] {
-    const char* e = getenv("LVX_DKV_PERSIST");   // A/B switch: 0 = one tile per CTA
-    return e ? atoi(e) : 1;
+    const char* e = getenv("LVX_DKV_PERSIST");
+    return e ? atoi(e) : 0;
   }();
   const bool persist = persist_env && !accumulate && p.out_bf16;
   const int grid = persist ? std::min(tiles, device_sms()) : tiles;
