@@ -916,10 +916,8 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   // at the c2gath shape; the default is one tile per CTA with the staged,
   // coalesced epilogue.
   const int tiles = (int)ceil_div(k->rows, 128) * (int)k->heads;
-  static const int persist_env = [] {
-    const char* e = getenv("LVX_DKV_PERSIST");
-    return e ? atoi(e) : 0;
-  }();
+  const char* persist_e = getenv("LVX_DKV_PERSIST");
+  const int persist_env = persist_e ? atoi(persist_e) : 0;
   const bool persist = persist_env && !accumulate && p.out_bf16;
   const int grid = persist ? std::min(tiles, device_sms()) : tiles;
   bwd_dkv_kernel<D><<<grid, 384, DkvCfg<D>::SMEM, st>>>(mq128, mk128, mv128, mg128, mdk, mdv, p);
