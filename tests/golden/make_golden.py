@@ -226,13 +226,49 @@ def make_analytics() -> None:
     print("golden_analytics.json", (OUT / "golden_analytics.json").stat().st_size, "bytes")
 
 
+def make_lvxt() -> None:
+    """LVXT files written by the reference (tensorio.py:85-130) plus a numeric
+    run (the data path of cli.cmd_run, cli.py:96-177) -> tests/golden/lvxt/."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import json
+    from lvxattn.cluster import ClusterSpec
+    from lvxattn.strategies import run_distributed
+    from lvxattn.tensorio import seeded_random_tensor as srt, store_tensor
+    out = OUT / "lvxt"
+    out.mkdir(exist_ok=True)
+    store_tensor(srt(5, (3, 4, 2), np.float32), out / "f32_3d.lvxt")
+    store_tensor(srt(6, (7,), np.float64, scale=2.0, stream=3), out / "f64_1d.lvxt")
+    store_tensor(srt(7, (2, 5), np.float32, stream=9), out / "f32_2d.lvxt")
+    # inputs + outputs of one numeric run: lvx, n = 3, f64, with backward
+    h, sq, skv, d, seed = 2, 7, 11, 4, 17
+    Q = srt(seed, (h, sq, d), np.float64, stream=0)
+    K = srt(seed, (h, skv, d), np.float64, stream=1)
+    V = srt(seed, (h, skv, d), np.float64, stream=2)
+    dO = srt(seed, (h, sq, d), np.float64, stream=3)
+    for name, t in (("q", Q), ("k", K), ("v", V), ("do", dO)):
+        store_tensor(t, out / f"run_in_{name}.lvxt")
+    res = run_distributed("lvx", Q, K, V, dO=dO, spec=ClusterSpec(3))
+    for name, t in (("o", res.O), ("l", res.L), ("dq", res.grads.dQ), ("dk", res.grads.dK),
+                    ("dv", res.grads.dV)):
+        store_tensor(t, out / f"run_out_{name}.lvxt")
+    (out / "run_stats.json").write_text(json.dumps({
+        "total_bytes": res.stats.total_bytes(),
+        "per_worker_bytes_sent": [res.stats.bytes_sent_by(i) for i in range(3)],
+        "rounds_forward": res.traces_forward[0].num_rounds}))
+    print("lvxt goldens:", sorted(p.name for p in out.iterdir()))
+
+
 if __name__ == "__main__":
     only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     if only == "mllm":
         make_mllm_stack()
     elif only == "analytics":
         make_analytics()
+    elif only == "lvxt":
+        make_lvxt()
     else:
         main()
         make_mllm_stack()
         make_analytics()
+        make_lvxt()
