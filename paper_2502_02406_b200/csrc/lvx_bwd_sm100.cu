@@ -487,6 +487,377 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   }
 }
 
+// ================================================================ dK / dV on CTA pairs
+// The same algorithm as bwd_dkv_kernel on cta_group::2 (M = 256 KV rows per
+// pair, 128 per CTA): the leader issues S^T = K Q^T, dP^T = V dO^T (SS) and
+// dV += P^T dO, dK += dS^T Q (TS) for the pair.  B splits by N (cute's 2x1SM
+// layouts), so each CTA stages the query HALF of Q / dO (64 rows, B of S^T /
+// dP^T) and the d HALF (128 rows x 64 cols, B of dV / dK): per-CTA operand
+// reads drop from 192 to 128 KB per 128-row step, the SMEM ceiling of the
+// 1-CTA kernel.  Softmax, epilogue and TMEM layout are the 1-CTA kernel's;
+// each CTA's softmax warps arrive on the LEADER's p_ready / ds_ready (16).
+// Registers: warpgroup 2 -> 72 (the issuer keeps more descriptors than the
+// 1-CTA one), softmax -> 216: (168 - 72) x 128 >= (216 - 168) x 256, else
+// setmaxnreg.inc waits forever for registers nobody frees.
+template <int D>
+struct Dkv2Cfg {
+  static constexpr int PANELS = D / 64;
+  static constexpr int KV_BYTES = 128 * D * 2;             // own K (or V) rows
+  static constexpr int QH_BYTES = 64 * D * 2;              // query half: 64 rows x D
+  static constexpr int DH_BYTES = 128 * 64 * 2;            // d half: 128 rows x 64 cols
+  static constexpr int OFF_QQ = 0, OFF_GQ = QH_BYTES, OFF_QD = 2 * QH_BYTES,
+                       OFF_GD = 2 * QH_BYTES + DH_BYTES, OFF_LD = 2 * QH_BYTES + 2 * DH_BYTES;
+  static constexpr int SLOT = ((OFF_LD + 1024 + 1023) / 1024) * 1024;
+  static constexpr int STAGES = 2;
+  static constexpr int QT_BYTES = QH_BYTES;   // (epilogue staging uses the slots only)
+  static constexpr int NBAR = 1 + 3 * STAGES + 5;
+  static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
+  static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
+  static_assert(D == 128, "the d halves are one 128-byte panel each");
+  static_assert(8 * 32 * D * 4 <= STAGES * SLOT, "epilogue staging must fit the Q/dO ring");
+};
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG,
+                const __grid_constant__ CUtensorMap tmQh, const __grid_constant__ CUtensorMap tmGh,
+                const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
+                const BwdParams p) {
+  using C = Dkv2Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + C::KV_BYTES;
+  uint8_t* sSlot = sV + C::KV_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + C::STAGES * C::SLOT);
+  uint64_t* kv_full = bars;                   // leader: K / V of both CTAs
+  uint64_t* qd_full = bars + 1;               // leader: Q / dO halves of both CTAs
+  uint64_t* ld_full = qd_full + C::STAGES;    // local: this CTA's nL / nD rows
+  uint64_t* qd_empty = ld_full + C::STAGES;   // both (multicast commit)
+  uint64_t* s_full = qd_empty + C::STAGES;    // both
+  uint64_t* p_ready = s_full + 1;             // leader: one arrival per softmax warp (16)
+  uint64_t* dp_full = p_ready + 1;            // both
+  uint64_t* ds_ready = dp_full + 1;           // leader: 16
+  uint64_t* dkv_done = ds_ready + 1;          // both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int n0 = (blockIdx.x >> 1) * 256 + (int)rank * 128, g = blockIdx.y;
+  const int nsteps = p.G * p.tpq;
+  // one arrival per softmax warp on the leader's copy of bar (16 per pair):
+  // every lane has waited for its TMEM stores and fenced before the warp syncs
+  auto arrive_pair = [&](uint64_t* bar) {
+    __syncwarp();
+    if (lane == 0) {
+      if (rank == 0) mbar_arrive(bar);
+      else mbar_arrive_cluster(leader_addr(bar));
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&qd_full[s], 1);
+      mbar_init(&ld_full[s], 1);
+      mbar_init(&qd_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 16);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 16);
+    mbar_init(dkv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    reg_dealloc<72>();
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmQh);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmG);
+      tma_prefetch(&tmGh);
+      const uint64_t once = l2_evict_first(), shared = l2_evict_last();
+      if (rank == 0) mbar_arrive_expect_tx(kv_full, 2 * 2 * C::KV_BYTES);
+      const uint32_t lkv = leader_addr(kv_full);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma2_load_3d(sK + pn * 128 * 128, &tmK, lkv, pn * 64, n0, g, once);
+        tma2_load_3d(sV + pn * 128 * 128, &tmV, lkv, pn * 64, n0, g, once);
+      }
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % C::STAGES, u = i / C::STAGES;
+        if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
+        const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
+        uint8_t* slot = sSlot + s * C::SLOT;
+        if (rank == 0)
+          mbar_arrive_expect_tx(&qd_full[s], 2 * (2 * C::QH_BYTES + 2 * C::DH_BYTES));
+        const uint32_t lq = leader_addr(&qd_full[s]);
+        for (int pn = 0; pn < C::PANELS; ++pn) {   // query half: rows r0 + 64 rank
+          tma2_load_3d(slot + C::OFF_QQ + pn * 64 * 128, &tmQh, lq, pn * 64,
+                       r0 + 64 * (int)rank, h, shared);
+          tma2_load_3d(slot + C::OFF_GQ + pn * 64 * 128, &tmGh, lq, pn * 64,
+                       r0 + 64 * (int)rank, h, shared);
+        }
+        // d half: all 128 query rows, columns [64 rank, 64 rank + 64)
+        tma2_load_3d(slot + C::OFF_QD, &tmQ, lq, 64 * (int)rank, r0, h, shared);
+        tma2_load_3d(slot + C::OFF_GD, &tmG, lq, 64 * (int)rank, r0, h, shared);
+        const size_t off = (size_t)h * p.rows_pad + r0;
+        mbar_arrive_expect_tx(&ld_full[s], 1024);
+        bulk_load_hint(slot + C::OFF_LD, p.Lp + off, 512, &ld_full[s], shared);
+        bulk_load_hint(slot + C::OFF_LD + 512, p.Dp + off, 512, &ld_full[s], shared);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------- MMA issuer (leader, converged warp)
+    reg_dealloc<72>();
+    if (rank == 0) {
+      constexpr uint32_t idS = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idKV = idesc_bf16(256, D, false, true);
+      const uint64_t dk0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
+      const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
+      const uint64_t dh0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);   // query halves, K-major
+      const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);   // d halves, MN-major
+      auto qslot = [&](int i) { return (uint64_t)(((i % C::STAGES) * C::SLOT) >> 4); };
+      auto issue_st = [&](int i, uint64_t a0, uint32_t col, uint32_t boff, uint64_t* bar) {
+        // col R1: S^T = K Q^T ; col R2: dP^T = V dO^T   (M=256 kv, N=128 q, K=D)
+        if (elect_one()) {
+          const uint64_t b = dh0 + qslot(i) + (boff >> 4);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oa = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t ob = ((kk >> 2) * (64 * 128) + (kk & 3) * 32) >> 4;
+            mma2_bf16_ss(tmem + col, a0 + oa, b + ob, idS, kk > 0);
+          }
+          mma2_commit_mc(bar);
+        }
+        __syncwarp();
+      };
+      auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t boff) {
+        // dV += P^T dO (a_col R1, d half of dO) ; dK += dS^T Q (a_col R2, d half of Q)
+        if (elect_one()) {
+          const uint64_t b = dm0 + qslot(i) + (boff >> 4);
+#pragma unroll
+          for (int kk = 0; kk < 128 / 16; ++kk)
+            mma2_bf16_ts(tmem + acc_col, tmem + a_col + kk * 8, b + ((kk * 16 * 128) >> 4), idKV,
+                         (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+      };
+      mbar_wait_cluster(kv_full, 0);
+      tc_fence_after();
+      mbar_wait_cluster(&qd_full[0], 0);
+      tc_fence_after();
+      issue_st(0, dk0, C::R1, C::OFF_QQ, s_full);
+      issue_st(0, dv0, C::R2, C::OFF_GQ, dp_full);
+      for (int i = 0; i < nsteps; ++i) {
+        const uint32_t ph = i & 1;
+        mbar_wait_cluster(p_ready, ph);
+        tc_fence_after();
+        issue_acc(i, C::DV_COL, C::R1, C::OFF_GD);             // dV(i)
+        if (i + 1 < nsteps) {
+          mbar_wait_cluster(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
+          tc_fence_after();
+          issue_st(i + 1, dk0, C::R1, C::OFF_QQ, s_full);      // S^T(i+1)
+        }
+        mbar_wait_cluster(ds_ready, ph);
+        tc_fence_after();
+        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD);             // dK(i)
+        if (elect_one()) mma2_commit_mc(&qd_empty[i % C::STAGES]);
+        __syncwarp();
+        if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::OFF_GQ, dp_full);   // dP^T(i+1)
+      }
+      if (elect_one()) mma2_commit_mc(dkv_done);
+      __syncwarp();
+    }
+  } else if (warp >= 10) {
+    reg_dealloc<72>();
+  } else {
+    // -------------- softmax: kv row per thread, 64 of the 128 query columns per wg
+    reg_alloc<216>();
+    const int wg = warp >> 2, q4 = warp & 3;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    for (int i = 0; i < nsteps; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = i & 1;
+      const uint32_t lds = smem_u32(sSlot + s * C::SLOT + C::OFF_LD) + wg * 256;
+      // phase A: P^T = exp2(S^T * c + nL[q]), 32 columns at a time
+      mbar_wait(&ld_full[s], (i / C::STAGES) & 1);   // this CTA's nL / nD rows
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      uint32_t pp[32];   // P^T packed for the dV MMA
+      float2 pf[32];     // P^T in fp32 for phase B
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sv[32];
+        tmem_ld32(tl + C::R1 + wg * 64 + hh * 32, sv);
+        tmem_wait_ld();
+        if (hh == 1 && wg == 0) {   // wg 0 is done reading
+          tc_fence_before();
+          named_arrive<1>();
+        }
+        if ((p.debug == 1 || p.debug == 2)) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            pp[hh * 16 + e] = sv[2 * e];
+            pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 32; c4 += 4) {
+            const float4 l4 = p.debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
+                                           : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
+            const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
+            const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
+            const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
+            const float2 p0 = (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
+            const float2 p1 = ((pi + 1) % 8) < kPolyPairsDkv ? ex2_poly2(x1)
+                                                          : make_float2(ex2(x1.x), ex2(x1.y));
+            pp[pi] = pack_bf16(p0.x, p0.y);
+            pp[pi + 1] = pack_bf16(p1.x, p1.y);
+            pf[pi] = p0;
+            pf[pi + 1] = p1;
+          }
+        }
+      }
+      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
+      if (wg == 1) {   // wg 0 has read R1
+        named_sync<1>();
+        tc_fence_after();
+      }
+      tmem_st32(tl + C::R1 + wg * 32, pp);
+      tmem_wait_st();
+      tc_fence_before();
+      arrive_pair(p_ready);
+      // phase B: dS^T = P^T (dP^T + nD[q])
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      uint32_t dd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t gv[32];
+        tmem_ld32(tl + C::R2 + wg * 64 + hh * 32, gv);
+        tmem_wait_ld();
+        if (hh == 1 && wg == 0) {   // wg 0 is done reading
+          tc_fence_before();
+          named_arrive<2>();
+        }
+        if ((p.debug == 1 || p.debug == 2)) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 32; c4 += 4) {
+            const float4 d4 = p.debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                           : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
+            const int pi = (hh * 32 + c4) / 2;
+            const float2 t0 = fadd2(u2f2(gv[c4], gv[c4 + 1]), make_float2(d4.x, d4.y));
+            const float2 t1 = fadd2(u2f2(gv[c4 + 2], gv[c4 + 3]), make_float2(d4.z, d4.w));
+            const float2 r0 = fmul2(pf[pi], t0);
+            const float2 r1 = fmul2(pf[pi + 1], t1);
+            dd[pi] = pack_bf16(r0.x, r0.y);
+            dd[pi + 1] = pack_bf16(r1.x, r1.y);
+          }
+        }
+      }
+      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
+      if (wg == 1) {   // wg 0 has read R2
+        named_sync<2>();
+        tc_fence_after();
+      }
+      tmem_st32(tl + C::R2 + wg * 32, dd);
+      tmem_wait_st();
+      tc_fence_before();
+      arrive_pair(ds_ready);
+    }
+    // epilogue (as bwd_dkv_kernel): this CTA's 128 rows, staged in its Q/dO ring
+    mbar_wait(dkv_done, 0);
+    tc_fence_after();
+    const uint32_t col = wg ? C::DK_COL : C::DV_COL;
+    const float mul = wg ? p.scale : 1.f;
+    uint8_t* stage = sSlot + warp * (32 * D * 4);
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tl + col + c * 32, v);
+      tmem_wait_ld();
+      const uint32_t rowbase = smem_u32(stage + c * 4096) + lane * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        st_shared_v4(rowbase + ((q ^ (lane & 7)) << 4),
+                     __float_as_uint(__uint_as_float(v[4 * q]) * mul),
+                     __float_as_uint(__uint_as_float(v[4 * q + 1]) * mul),
+                     __float_as_uint(__uint_as_float(v[4 * q + 2]) * mul),
+                     __float_as_uint(__uint_as_float(v[4 * q + 3]) * mul));
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (!p.accumulate && p.out_bf16 && p.debug != 4) {
+      // overwrite in bf16: each 8-lane group packs 64 columns of one row (two
+      // staged 32-column chunks) into one full 128-byte line
+      __nv_bfloat16* base = static_cast<__nv_bfloat16*>(wg ? p.dk_ptr : p.dv_ptr);
+      const int64_t hs = wg ? p.dk_hs : p.dv_hs, rs = wg ? p.dk_rs : p.dv_rs;
+#pragma unroll 1
+      for (int cp = 0; cp < D / 64; ++cp) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3), q8 = lane & 7;
+          const int c = cp * 2 + (q8 >> 2), qq = (q8 & 3) * 2;
+          const uint32_t rb = smem_u32(stage + c * 4096) + rr * 128;
+          const float4 a = ld_shared_f4(rb + ((qq ^ (rr & 7)) << 4));
+          const float4 b = ld_shared_f4(rb + (((qq + 1) ^ (rr & 7)) << 4));
+          const int grow = n0 + q4 * 32 + rr;
+          if (grow < p.rows_kv)
+            *reinterpret_cast<uint4*>(base + g * hs + (int64_t)grow * rs + cp * 64 + q8 * 8) =
+                make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
+                           pack_bf16(b.z, b.w));
+        }
+      }
+    } else if (!p.accumulate && p.debug != 4) {   // 4: profiling, no drain
+      // overwrite: each 8-lane group stores one full 128-byte row segment
+      // (STG.128, whole lines); measured ~5 % faster than TMA tensor stores here
+      float* base = static_cast<float*>(wg ? p.dk_ptr : p.dv_ptr);
+      const int64_t hs = wg ? p.dk_hs : p.dv_hs, rs = wg ? p.dk_rs : p.dv_rs;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3), q = lane & 7;
+          const int grow = n0 + q4 * 32 + rr;
+          const float4 val = ld_shared_f4(smem_u32(stage + c * 4096) + rr * 128 +
+                                          ((q ^ (rr & 7)) << 4));
+          if (grow < p.rows_kv)
+            *reinterpret_cast<float4*>(base + g * hs + (int64_t)grow * rs + c * 32 + q * 4) = val;
+        }
+      }
+    } else if (p.accumulate && lane == 0 && p.debug != 4) {   // reduce-add in L2
+      const CUtensorMap* m = wg ? &tmDK : &tmDV;
+      const uint64_t pol = l2_evict_first();   // written once, not re-read here
+      for (int c = 0; c < D / 32; ++c)
+        tma_reduce_add_3d(m, stage + c * 4096, c * 32, n0 + q4 * 32, g, pol);
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+
 // ================================================================ dQ kernel
 // Q-parallel, one 128-row query tile per CTA, split over the KV block in
 // 128-row steps.  Q and dO are copied once into TMEM so that all three MMAs
@@ -925,6 +1296,38 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
+int launch_dkv2(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
+                BwdParams p, const lvx_view* dk, const lvx_view* dvv, int accumulate,
+                cudaStream_t st) {
+  CUtensorMap mq128, mg128, mq64, mg64, mk128, mv128, mdk{}, mdv{};
+  if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
+      !make_tma_3d(&mq64, q, 64) || !make_tma_3d(&mg64, dO, 64) ||
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
+    return LVX_ECUDA;
+  if (accumulate && (!make_tma_f32_3d(&mdk, dk, 32) || !make_tma_f32_3d(&mdv, dvv, 32)))
+    return LVX_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(bwd_dkv2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Dkv2Cfg<128>::SMEM) != cudaSuccess)
+      return LVX_ECUDA;
+    attr = true;
+  }
+  p.accumulate = accumulate;
+  p.dk_ptr = dk->data;
+  p.dv_ptr = dvv->data;
+  p.out_bf16 = dk->dtype == LVX_BF16;
+  p.dk_hs = dk->head_stride;
+  p.dk_rs = dk->row_stride;
+  p.dv_hs = dvv->head_stride;
+  p.dv_rs = dvv->row_stride;
+  const unsigned pairs = (unsigned)ceil_div(k->rows, 256);
+  bwd_dkv2_kernel<128><<<dim3(2 * pairs, (unsigned)k->heads), 384, Dkv2Cfg<128>::SMEM, st>>>(
+      mq128, mk128, mv128, mg128, mq64, mg64, mdk, mdv, p);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
 template <int D>
 int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
               const BwdParams& p, const BwdPlan& pl, cudaStream_t st) {
@@ -1017,6 +1420,14 @@ int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   fill_params(p, pl, q, k, scale, ws);
   int s = launch_prep(p, L, D, st);
   if (s) return s;
+  // CTA-pair kernel (d = 128), opt-in: bit-identical to the 1-CTA kernel and
+  // equal with the softmax stubbed (1423 vs 1457 TFLOP/s at c2gath), but 19 %
+  // slower with real math (1008-1013 vs 1242-1251 at c2full): the pair's two
+  // tensor cores wait for the slower CTA's softmax at both hand-offs of every
+  // step, and those hand-offs, not SMEM bandwidth, are the critical path.
+  const char* two = getenv("LVX_DKV_2CTA");
+  if (q->d == 128 && two && atoi(two) == 1)
+    return launch_dkv2(q, k, v, dO, p, dk, dv, accumulate, st);
   return q->d == 128 ? launch_dkv<128>(q, k, v, dO, p, dk, dv, accumulate, st)
                      : launch_dkv<64>(q, k, v, dO, p, dk, dv, accumulate, st);
 }

@@ -286,3 +286,29 @@ def test_dkv_persistent_schedule_bit_identical(shape, monkeypatch):
         torch.cuda.synchronize()
         outs[flag] = (dk, dv)
     assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
+
+
+@pytest.mark.parametrize("shape,dt,acc", [((8, 2, 300, 5000, 128), torch.bfloat16, False),
+                                          ((8, 2, 300, 5000, 128), torch.float32, False),
+                                          ((4, 4, 256, 3000, 128), torch.float32, True),
+                                          ((32, 8, 128, 1300, 128), torch.bfloat16, False)])
+def test_dkv_cta_pair_kernel_bit_identical(shape, dt, acc, monkeypatch):
+    """The CTA-pair (cta_group::2) dK/dV kernel (LVX_DKV_2CTA=1) writes the same
+    bits as the 1-CTA kernel: bf16 / fp32 outputs, overwrite / accumulate, odd
+    KV-tile counts (the last pair's second CTA is entirely out of range)."""
+    from paper_2502_02406_b200 import kernels as K
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, g), _ = bf16_inputs(hq, hkv, sq, skv, d, seed=13)
+    st = K.blockwise_attention(q, k, v)
+    D = torch.empty(st.L.shape, device="cuda")
+    K.row_stats_into(st.O, g, D)
+    outs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("LVX_DKV_2CTA", flag)
+        dk = torch.full(k.shape, 0.5, dtype=dt, device="cuda")
+        dv = torch.full(v.shape, -0.25, dtype=dt, device="cuda")
+        K.bwd_dkv(q, k, v, st.L, D, g, d ** -0.5, dk, dv, accumulate=acc)
+        torch.cuda.synchronize()
+        outs[flag] = (dk, dv)
+    assert torch.equal(outs["0"][0], outs["1"][0]), (outs["0"][0] - outs["1"][0]).abs().max()
+    assert torch.equal(outs["0"][1], outs["1"][1]), (outs["0"][1] - outs["1"][1]).abs().max()
