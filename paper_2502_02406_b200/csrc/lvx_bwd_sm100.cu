@@ -93,7 +93,7 @@ struct DkvCfg {
   static constexpr int QT_BYTES = 128 * D * 2;             // one Q (or dO) 128-row step tile
   static constexpr int SLOT = ((2 * QT_BYTES + 1024 + 1023) / 1024) * 1024;
   static constexpr int STAGES = D == 128 ? 2 : 4;
-  static constexpr int NBAR = 1 + 2 * STAGES + 7;
+  static constexpr int NBAR = 1 + 2 * STAGES + 5;
   static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
   static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
   static_assert(8 * 32 * D * 4 <= STAGES * SLOT, "epilogue staging must fit the Q/dO ring");
@@ -121,17 +121,11 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   uint64_t* dp_full = p_ready + 1;            // dP^T(i) in R2
   uint64_t* ds_ready = dp_full + 1;           // dS^T(i) packed in R2 (256 arrivals)
   uint64_t* dkv_done = ds_ready + 1;
-  uint64_t* kv_empty = dkv_done + 1;          // last K/V reader of a tile retired
-  uint64_t* acc_free = kv_empty + 1;          // dV / dK drained from TMEM (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * 128, g = blockIdx.y;
   const int nsteps = p.G * p.tpq;
-  // Tiles (128 KV rows of one KV head) are dealt round-robin: gridDim.x = tiles is
-  // one tile per CTA; gridDim.x = SMs is the persistent schedule, where the Q/dO
-  // ring, the step barriers and the MMA stream run on across tile boundaries and
-  // only dV(0) / dK(0) of the next tile wait for the previous drain.
-  const int n_kv_tiles = p.n_tiles, n_tiles_total = n_kv_tiles * p.hkv;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -144,8 +138,6 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     mbar_init(dp_full, 1);
     mbar_init(ds_ready, 256);
     mbar_init(dkv_done, 1);
-    mbar_init(kv_empty, 1);
-    mbar_init(acc_free, 256);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -167,34 +159,29 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       // L2 policy: this CTA's K/V tile is read once (evict first); the GQA
       // group's Q / dO / L / D are swept by every CTA of the group (evict last)
       const uint64_t once = l2_evict_first(), shared = l2_evict_last();
-      int gs = 0;   // global query-step counter (ring position) across tiles
-      for (int tile = blockIdx.x, it = 0; tile < n_tiles_total; tile += gridDim.x, ++it) {
-        const int n0 = (tile % n_kv_tiles) * 128, g = tile / n_kv_tiles;
-        if (it > 0) mbar_wait(kv_empty, (it - 1) & 1);   // previous tile's K / V retired
-        mbar_arrive_expect_tx(kv_full, 2 * C::KV_BYTES);
+      mbar_arrive_expect_tx(kv_full, 2 * C::KV_BYTES);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma_load_3d_hint(sK + pn * 128 * 128, &tmK, kv_full, pn * 64, n0, g, once);
+        tma_load_3d_hint(sV + pn * 128 * 128, &tmV, kv_full, pn * 64, n0, g, once);
+      }
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % C::STAGES, u = i / C::STAGES;
+        if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
+        const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
+        uint8_t* slot = sSlot + s * C::SLOT;
+        if ((p.debug == 2 || p.debug == 3) && u > 0) {   // profiling: no reloads (stale data)
+          mbar_arrive(&qd_full[s]);
+          continue;
+        }
+        mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 1024);
         for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_3d_hint(sK + pn * 128 * 128, &tmK, kv_full, pn * 64, n0, g, once);
-          tma_load_3d_hint(sV + pn * 128 * 128, &tmV, kv_full, pn * 64, n0, g, once);
+          tma_load_3d_hint(slot + pn * 128 * 128, &tmQ, &qd_full[s], pn * 64, r0, h, shared);
+          tma_load_3d_hint(slot + C::QT_BYTES + pn * 128 * 128, &tmG, &qd_full[s], pn * 64, r0,
+                           h, shared);
         }
-        for (int i = 0; i < nsteps; ++i, ++gs) {
-          const int s = gs % C::STAGES, u = gs / C::STAGES;
-          if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
-          const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
-          uint8_t* slot = sSlot + s * C::SLOT;
-          if ((p.debug == 2 || p.debug == 3) && u > 0) {   // profiling: no reloads (stale data)
-            mbar_arrive(&qd_full[s]);
-            continue;
-          }
-          mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 1024);
-          for (int pn = 0; pn < C::PANELS; ++pn) {
-            tma_load_3d_hint(slot + pn * 128 * 128, &tmQ, &qd_full[s], pn * 64, r0, h, shared);
-            tma_load_3d_hint(slot + C::QT_BYTES + pn * 128 * 128, &tmG, &qd_full[s], pn * 64,
-                             r0, h, shared);
-          }
-          const size_t off = (size_t)h * p.rows_pad + r0;
-          bulk_load_hint(slot + 2 * C::QT_BYTES, p.Lp + off, 512, &qd_full[s], shared);
-          bulk_load_hint(slot + 2 * C::QT_BYTES + 512, p.Dp + off, 512, &qd_full[s], shared);
-        }
+        const size_t off = (size_t)h * p.rows_pad + r0;
+        bulk_load_hint(slot + 2 * C::QT_BYTES, p.Lp + off, 512, &qd_full[s], shared);
+        bulk_load_hint(slot + 2 * C::QT_BYTES + 512, p.Dp + off, 512, &qd_full[s], shared);
       }
     }
   } else if (warp == 9) {
@@ -206,11 +193,11 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
     const uint64_t ds0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);        // K-major Q / dO
     const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), 128 * 128, 1024);  // MN-major Q / dO
-    auto qslot = [&](int gs) { return (uint64_t)(((gs % C::STAGES) * C::SLOT) >> 4); };
-    auto issue_st = [&](int gs, uint64_t a0, uint32_t col, uint32_t xoff, uint64_t* bar) {
+    auto qslot = [&](int i) { return (uint64_t)(((i % C::STAGES) * C::SLOT) >> 4); };
+    auto issue_st = [&](int i, uint64_t a0, uint32_t col, uint32_t xoff, uint64_t* bar) {
       // col R1: S^T = K Q^T ; col R2: dP^T = V dO^T   (M=128 kv, N=128 q, K=D)
       if (elect_one()) {
-        const uint64_t b = ds0 + qslot(gs) + (xoff >> 4);
+        const uint64_t b = ds0 + qslot(i) + (xoff >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t o = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
@@ -220,10 +207,10 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       }
       __syncwarp();
     };
-    auto issue_acc = [&](int i, int gs, uint32_t acc_col, uint32_t a_col, uint32_t xoff) {
-      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0); i = tile step
+    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t xoff) {
+      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0)
       if (elect_one()) {
-        const uint64_t b = dm0 + qslot(gs) + (xoff >> 4);
+        const uint64_t b = dm0 + qslot(i) + (xoff >> 4);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
           mma_bf16_ts(tmem + acc_col, tmem + a_col + kk * 8, b + ((kk * 16 * 128) >> 4), idKV,
@@ -231,47 +218,31 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       }
       __syncwarp();
     };
-    int gs0 = 0;   // global step index of the tile's step 0
-    for (int tile = blockIdx.x, it = 0; tile < n_tiles_total; tile += gridDim.x, ++it) {
-      mbar_wait(kv_full, it & 1);
+    mbar_wait(kv_full, 0);
+    tc_fence_after();
+    mbar_wait(&qd_full[0], 0);
+    tc_fence_after();
+    issue_st(0, dk0, C::R1, 0, s_full);
+    issue_st(0, dv0, C::R2, C::QT_BYTES, dp_full);
+    for (int i = 0; i < nsteps; ++i) {
+      const uint32_t ph = i & 1;
+      mbar_wait(p_ready, ph);
       tc_fence_after();
-      mbar_wait(&qd_full[gs0 % C::STAGES], (gs0 / C::STAGES) & 1);
-      tc_fence_after();
-      // R1 / R2 are free in issue order: the previous tile's dV / dK read them last
-      issue_st(gs0, dk0, C::R1, 0, s_full);
-      issue_st(gs0, dv0, C::R2, C::QT_BYTES, dp_full);
-      if (nsteps == 1 && elect_one()) mma_commit(kv_empty);
-      __syncwarp();
-      for (int i = 0; i < nsteps; ++i) {
-        const int gs = gs0 + i;
-        const uint32_t ph = gs & 1;
-        mbar_wait(p_ready, ph);
+      issue_acc(i, C::DV_COL, C::R1, C::QT_BYTES);            // dV(i)
+      if (i + 1 < nsteps) {
+        mbar_wait(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
         tc_fence_after();
-        if (i == 0 && it > 0) {   // dV(0) / dK(0) overwrite the accumulators: drained?
-          mbar_wait(acc_free, (it - 1) & 1);
-          tc_fence_after();
-        }
-        issue_acc(i, gs, C::DV_COL, C::R1, C::QT_BYTES);       // dV(i)
-        if (i + 1 < nsteps) {
-          mbar_wait(&qd_full[(gs + 1) % C::STAGES], ((gs + 1) / C::STAGES) & 1);
-          tc_fence_after();
-          issue_st(gs + 1, dk0, C::R1, 0, s_full);             // S^T(i+1) after dV(i) read R1
-        }
-        mbar_wait(ds_ready, ph);
-        tc_fence_after();
-        issue_acc(i, gs, C::DK_COL, C::R2, 0);                 // dK(i)
-        if (elect_one()) mma_commit(&qd_empty[gs % C::STAGES]);
-        __syncwarp();
-        if (i + 1 < nsteps) {
-          issue_st(gs + 1, dv0, C::R2, C::QT_BYTES, dp_full);  // dP^T(i+1)
-          if (i + 2 == nsteps && elect_one()) mma_commit(kv_empty);   // last K / V reader
-          __syncwarp();
-        }
+        issue_st(i + 1, dk0, C::R1, 0, s_full);               // S^T(i+1) after dV(i) read R1
       }
-      if (elect_one()) mma_commit(dkv_done);
+      mbar_wait(ds_ready, ph);
+      tc_fence_after();
+      issue_acc(i, C::DK_COL, C::R2, 0);                      // dK(i)
+      if (elect_one()) mma_commit(&qd_empty[i % C::STAGES]);
       __syncwarp();
-      gs0 += nsteps;
+      if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::QT_BYTES, dp_full);   // dP^T(i+1)
     }
+    if (elect_one()) mma_commit(dkv_done);
+    __syncwarp();
   } else if (warp >= 10) {
     reg_dealloc<56>();
   } else {
@@ -280,13 +251,9 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const int wg = warp >> 2, q4 = warp & 3;
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    const bool persistent = (int)gridDim.x < n_tiles_total;
-    int gs = 0;
-    for (int tile = blockIdx.x, it = 0; tile < n_tiles_total; tile += gridDim.x, ++it) {
-    const int n0 = (tile % n_kv_tiles) * 128, g = tile / n_kv_tiles;
-    for (int i = 0; i < nsteps; ++i, ++gs) {
-      const int s = gs % C::STAGES;
-      const uint32_t ph = gs & 1;
+    for (int i = 0; i < nsteps; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = i & 1;
       const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 256;
       // phase A: P^T = exp2(S^T * c + nL[q]), 32 columns at a time
       mbar_wait(s_full, ph);
@@ -381,38 +348,10 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     // either stores them row-contiguously (whole 128-byte lines per 8 lanes) or,
     // when accumulating, hands them to TMA as 32x32 fp32 reduce-add boxes (the
     // add happens in L2, no read-modify-write through the SM).
-    mbar_wait(dkv_done, it & 1);
+    mbar_wait(dkv_done, 0);
     tc_fence_after();
     const uint32_t col = wg ? C::DK_COL : C::DV_COL;
     const float mul = wg ? p.scale : 1.f;
-    if (persistent) {
-      // The Q/dO ring already feeds the next tile: drain straight from
-      // registers.  All of this thread's row (bf16) comes out of TMEM first,
-      // then acc_free lets dV(0) / dK(0) of the next tile overwrite the
-      // accumulators while the row goes out as 16-byte stores.
-      uint32_t pk[D / 2];
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tl + col + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          pk[c * 16 + e / 2] = pack_bf16(__uint_as_float(v[e]) * mul, __uint_as_float(v[e + 1]) * mul);
-      }
-      tc_fence_before();
-      mbar_arrive(acc_free);
-      const int row = n0 + q4 * 32 + lane;
-      if (row < p.rows_kv && p.debug != 4) {
-        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(wg ? p.dk_ptr : p.dv_ptr) +
-                              g * (wg ? p.dk_hs : p.dv_hs) + (int64_t)row * (wg ? p.dk_rs : p.dv_rs);
-#pragma unroll
-        for (int q8 = 0; q8 < D / 8; ++q8)
-          *reinterpret_cast<uint4*>(base + q8 * 8) =
-              make_uint4(pk[q8 * 4], pk[q8 * 4 + 1], pk[q8 * 4 + 2], pk[q8 * 4 + 3]);
-      }
-      continue;
-    }
     uint8_t* stage = sSlot + warp * (32 * D * 4);
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
@@ -477,7 +416,6 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       bulk_wait_read0();
     }
     __syncwarp();
-    }   // tile loop
   }
   tc_fence_before();
   __syncthreads();
@@ -1280,18 +1218,8 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   p.dk_rs = dk->row_stride;
   p.dv_hs = dvv->head_stride;
   p.dv_rs = dvv->row_stride;
-  // Persistent schedule (one CTA per SM looping over tiles; bf16 overwrite only,
-  // its drain goes straight from registers since the Q/dO ring feeds the next
-  // tile).  Opt-in (LVX_DKV_PERSIST=1): measured neutral at the N=1 C2 launch
-  // (power-capped), -3 % at N=4 (row-per-lane drain stores), +1..12 % (bimodal)
-  // at the c2gath shape; the default is one tile per CTA with the staged,
-  // coalesced epilogue.
-  const int tiles = (int)ceil_div(k->rows, 128) * (int)k->heads;
-  const char* persist_e = getenv("LVX_DKV_PERSIST");
-  const int persist_env = persist_e ? atoi(persist_e) : 0;
-  const bool persist = persist_env && !accumulate && p.out_bf16;
-  const int grid = persist ? std::min(tiles, device_sms()) : tiles;
-  bwd_dkv_kernel<D><<<grid, 384, DkvCfg<D>::SMEM, st>>>(mq128, mk128, mv128, mg128, mdk, mdv, p);
+  bwd_dkv_kernel<D><<<dim3((unsigned)ceil_div(k->rows, 128), (unsigned)k->heads), 384,
+                      DkvCfg<D>::SMEM, st>>>(mq128, mk128, mv128, mg128, mdk, mdv, p);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }

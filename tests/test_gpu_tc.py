@@ -266,28 +266,6 @@ def test_tc_random_shapes_fwd_bwd_vs_oracle(shape):
     assert max(errs.values()) <= TOL_BF16, (shape, errs)
 
 
-@pytest.mark.parametrize("shape", [(8, 2, 300, 5000, 128), (4, 4, 128, 2000, 64)])
-def test_dkv_persistent_schedule_bit_identical(shape, monkeypatch):
-    """The opt-in persistent dK/dV schedule (LVX_DKV_PERSIST=1: one CTA per SM
-    looping over tiles, register drain) writes the same bf16 dK/dV bits as the
-    default one-tile-per-CTA kernel."""
-    from paper_2502_02406_b200 import kernels as K
-    hq, hkv, sq, skv, d = shape
-    (q, k, v, g), _ = bf16_inputs(hq, hkv, sq, skv, d, seed=7)
-    st = K.blockwise_attention(q, k, v)
-    D = torch.empty(st.L.shape, device="cuda")
-    K.row_stats_into(st.O, g, D)
-    outs = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("LVX_DKV_PERSIST", flag)
-        dk = torch.empty(k.shape, dtype=torch.bfloat16, device="cuda")
-        dv = torch.empty(v.shape, dtype=torch.bfloat16, device="cuda")
-        K.bwd_dkv(q, k, v, st.L, D, g, d ** -0.5, dk, dv, accumulate=False)
-        torch.cuda.synchronize()
-        outs[flag] = (dk, dv)
-    assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
-
-
 @pytest.mark.parametrize("shape,dt,acc", [((8, 2, 300, 5000, 128), torch.bfloat16, False),
                                           ((8, 2, 300, 5000, 128), torch.float32, False),
                                           ((4, 4, 256, 3000, 128), torch.float32, True),
