@@ -143,25 +143,30 @@ def cpu_reference_rate(budget_s: float = 12.0):
     Q, K, V, dO = orc.make_inputs(sq, skv, CFG["hq"], CFG["d"], seed=7, hkv=CFG["hkv"])
     Q, K, V, dO = (t.astype(np.float32) for t in (Q, K, V, dO))
     flops = orc.attention_flops(sq, skv, CFG["hq"], CFG["d"])
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        orc.simulate("lvx", Q, K, V, dO, n=1)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or reps >= 50:
-            break
-    sample = (f"oracle port of lvx fwd+bwd (numpy f64, {os.cpu_count()} host threads BLAS), "
+    # all host cores for BLAS, whatever OMP_NUM_THREADS torchrun exported
+    from threadpoolctl import threadpool_info, threadpool_limits
+    with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()
+                       if i.get("user_api") == "blas"), default=1)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            orc.simulate("lvx", Q, K, V, dO, n=1)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or reps >= 50:
+                break
+    sample = (f"oracle port of lvx fwd+bwd (numpy f64, {threads} host threads BLAS), "
               f"Lq={sq} x Lkv={skv}, hq=32/hkv=8, d=128, fp32 in, {reps} reps in {el:.1f}s")
-    return flops * reps / el / 1e12, sample
+    return flops * reps / el / 1e12, sample, threads
 
 
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, sample = [], ""
+    vals, sample, threads = [], "", 1
     for i in range(args.warmup + args.steps):
-        v, sample = cpu_reference_rate(budget_s=4.0)
+        v, sample, threads = cpu_reference_rate(budget_s=4.0)
         if i >= args.warmup:
             vals.append(v)
     val = statistics.median(vals)
@@ -172,7 +177,7 @@ def reference_arm(args):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**CFG, "note": "CPU sample of the workload; ms_per_step extrapolated"},
-            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": os.cpu_count(),
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -397,8 +402,8 @@ def native_arm(args):
 
     # --- CPU reference on the host cores (rank 0, N=1 only)
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample = cpu_reference_rate()
-        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": os.cpu_count(),
+        v, sample, threads = cpu_reference_rate()
+        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": threads,
                                "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(out), flush=True)
