@@ -5,6 +5,12 @@ hot path (kernels + query/KV-rotation strategies).
 Kernels: hand-written sm_100a CUDA (tcgen05/TMEM/TMA) in ``liblvx_b200.so``
 behind the C ABI of ``include/lvx_b200.h``.  Schedulers: one process per GPU
 over NCCL (``strategies``).  There is no CPU fallback.
+
+Submodules beyond the kernels and schedulers: ``recompute`` (the CA layer with
+the K/V recompute), ``mllm`` (the toy MLLM stack, memory ledger, frame
+budget), ``host_pipeline`` (host-resident inputs streamed over PCIe),
+``analytics`` (the cost model), ``volumes`` (byte closed forms),
+``tensorio`` (LVXT files, file-to-file runs).
 """
 from .comm import (ClusterError, ClusterSpec, CollectiveTimeout, DeviceContext, Instant,
                    TransportStats, WorkerFailed)
@@ -16,7 +22,7 @@ from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, Strategy
                          head_parallel_backward, head_parallel_forward,
                          lvx_backward, lvx_forward, partition_rows, ring_backward, ring_forward,
                          run_distributed, run_rank)
-from . import volumes
+from . import analytics, tensorio, volumes
 
 __version__ = "0.1.0"
 
@@ -27,5 +33,5 @@ __all__ = [
     "blockwise_attention", "blockwise_attention_backward", "default_scale", "dense_attention",
     "dense_attention_backward", "empty_state", "lvx_backward", "lvx_forward", "merge_states",
     "partition_rows", "project", "project_backward", "ring_backward", "ring_forward",
-    "run_distributed", "run_rank", "validate_qkv", "volumes",
+    "run_distributed", "run_rank", "validate_qkv", "volumes", "analytics", "tensorio",
 ]
