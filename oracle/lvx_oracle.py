@@ -478,3 +478,96 @@ def ca_block_backward(g, x, O, L, y, w_q, w_k, w_v, w_o, hq, hkv=None, scale=Non
     d_y_k, g_wk = project_backward(y, w_k, dk)
     d_y_v, g_wv = project_backward(y, w_v, dv)
     return g + d_x_q, d_y_k + d_y_v, g_wq, g_wk, g_wv, g_wo
+
+
+# ---------------------------------------------------------------------------
+# toy MLLM stack, memory ledger, frame budget — pkg/src/lvxattn/mllm.py
+# ---------------------------------------------------------------------------
+
+
+def mllm_stack_forward(x0, y, ca_params: dict, lm_params: list, ca_positions, hq, hkv=None,
+                       store_kv: bool = False, scale=None):
+    """mllm.py:274-305: for every block, a CA layer first when the block is
+    in ``ca_positions`` (x += flatten(O) W_O), then u = x, x = u + tanh(u W1) W2.
+    ``ca_params[pos] = (w_q, w_k, w_v, w_o)``, ``lm_params[i] = (w1, w2)``.
+    Returns (out, saved) with saved = {"lm_inputs": [...], "ca": {pos: {...}}}."""
+    saved = {"lm_inputs": [], "ca": {}}
+    x = x0
+    for blk, (w1, w2) in enumerate(lm_params):
+        if blk in ca_positions:
+            w_q, w_k, w_v, w_o = ca_params[blk]
+            xn, O, L = ca_block_forward(x, y, w_q, w_k, w_v, w_o, hq, hkv, scale)
+            entry = {"x": x, "O": O, "L": L}
+            if store_kv:   # mllm.py:297-299
+                h2 = hq if hkv is None else hkv
+                entry["K"], entry["V"] = project(y, w_k, h2), project(y, w_v, h2)
+            saved["ca"][blk] = entry
+            x = xn
+        saved["lm_inputs"].append(x)
+        x = x + np.tanh(x @ w1) @ w2
+    return x, saved
+
+
+def mllm_stack_backward(g, saved, y, ca_params: dict, lm_params: list, ca_positions, hq,
+                        hkv=None, scale=None):
+    """mllm.py:314-371 (both policies give the same gradients).  Returns
+    (d_x0, d_y, {pos: (g_wq, g_wk, g_wv, g_wo)}, [(g_w1, g_w2)])."""
+    d_y = np.zeros_like(y, dtype=np.float64)
+    ca_g, lm_g = {}, [None] * len(lm_params)
+    for blk in reversed(range(len(lm_params))):
+        w1, w2 = lm_params[blk]
+        u = saved["lm_inputs"][blk]
+        t = np.tanh(u @ w1)
+        d_pre = (g @ w2.T) * (1.0 - t * t)
+        lm_g[blk] = (u.T @ d_pre, t.T @ g)
+        g = g + d_pre @ w1.T
+        if blk in ca_positions:
+            e = saved["ca"][blk]
+            g, dy, *gw = ca_block_backward(g, e["x"], e["O"], e["L"], y, *ca_params[blk],
+                                           hq, hkv, scale)
+            d_y = d_y + dy
+            ca_g[blk] = tuple(gw)
+    return g, d_y, ca_g, lm_g
+
+
+def analytic_ledger(num_lm_blocks, num_ca_layers, d_embed, h, d, s_q, s_kv, store_kv: bool,
+                    b: int, hkv=None, b_state=None, b_params=None):
+    """mllm.py:190-210 peak activation ledger.  With one element size b (and
+    hkv = h) it is the reference's formula; the extra arguments express the
+    B200 layout: K/V with hkv heads, O/L in the fp32 state dtype (b_state),
+    parameters in their own dtype (b_params)."""
+    hkv = h if hkv is None else hkv
+    b_state = b if b_state is None else b_state
+    b_params = b if b_params is None else b_params
+    c = num_ca_layers
+    params = (c * (2 * d_embed * h * d + 2 * d_embed * hkv * d) +
+              num_lm_blocks * 2 * d_embed * d_embed) * b_params
+    yb = s_kv * d_embed * b
+    x = s_q * d_embed * b if c else 0
+    o_l = (s_q * h * d + s_q * h) * b_state if c else 0
+    kv = 2 * s_kv * hkv * d * b if (c and store_kv) else 0
+    peak = params + yb + c * (x + o_l + kv)
+    return {"params_bytes": params, "visual_features_y": yb, "per_layer_saved_x": x,
+            "per_layer_saved_o_l": o_l, "per_layer_saved_kv": kv, "num_ca_layers": c,
+            "peak_total": peak}
+
+
+def max_frames_under_budget(peak_of_frames, budget_bytes: int) -> int:
+    """mllm.py:374-397: largest frame count whose peak fits; 0 when even the
+    frame-independent part does not (doubling, then bisection)."""
+    if budget_bytes <= 0:
+        raise ValueError(f"budget must be positive, got {budget_bytes}")
+    if peak_of_frames(0) > budget_bytes:
+        return 0
+    lo, hi = 0, 1
+    while peak_of_frames(hi) <= budget_bytes:
+        lo, hi = hi, hi * 2
+        if hi > 2 ** 60:
+            raise ValueError("budget admits an absurd frame count; check inputs")
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if peak_of_frames(mid) <= budget_bytes:
+            lo = mid
+        else:
+            hi = mid
+    return lo
