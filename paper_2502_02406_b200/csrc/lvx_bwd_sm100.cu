@@ -77,15 +77,15 @@ struct BwdParams {
 // 128-row query steps so every SS MMA has N = 128 (A 4 KB + B 4 KB per 64
 // clk = the 128 B/clk SMEM read rate; 64-row steps re-read the 128-row A
 // operand twice as often and capped the kernel at ~80 % of peak).  TMEM:
-//   R1 [0,128)    S^T(i), then P^T(i) packed bf16 in its first 64 columns
-//   R2 [128,256)  dP^T(i), then dS^T(i) packed bf16
+//   R1 [0,128)    S^T(i), then P^T(i) packed bf16 (columns [0,32) + [64,96))
+//   R2 [128,256)  dP^T(i), then dS^T(i) packed bf16 (the same columns of R2)
 //   dV [256, 256+D), dK [256+D, 256+2D)
 // Two-phase softmax per step: phase A turns S^T into P^T (the exponentials)
-// and releases dV(i) and S^T(i+1); phase B turns dP^T into dS^T while the
-// tensor pipe runs dV(i) / S^T(i+1), then releases dK(i) and dP^T(i+1).
-// P stays packed in registers between the phases (R1 is overwritten by
-// S^T(i+1) as soon as dV(i) has read it).  Two softmax warpgroups split the
-// 128 query columns; both read before either packs over the shared lanes.
+// and releases dV(i) in two halves, then S^T(i+1); phase B turns dP^T into
+// dS^T while the tensor pipe runs dV(i) / S^T(i+1), then releases dK(i) and
+// dP^T(i+1).  P stays in fp32 registers between the phases (R1 is
+// overwritten by S^T(i+1) as soon as dV(i) has read it).  Two softmax
+// warpgroups split the 128 query columns, each packing into its own columns.
 template <int D>
 struct DkvCfg {
   static constexpr int PANELS = D / 64;
@@ -93,11 +93,102 @@ struct DkvCfg {
   static constexpr int QT_BYTES = 128 * D * 2;             // one Q (or dO) 128-row step tile
   static constexpr int SLOT = ((2 * QT_BYTES + 1024 + 1023) / 1024) * 1024;
   static constexpr int STAGES = D == 128 ? 2 : 4;
-  static constexpr int NBAR = 1 + 2 * STAGES + 5;
+  static constexpr int NBAR = 1 + 2 * STAGES + 6;
   static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
   static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
   static_assert(8 * 32 * D * 4 <= STAGES * SLOT, "epilogue staging must fit the Q/dO ring");
 };
+
+// dK / dV softmax, shared by the 1-CTA and CTA-pair kernels.  Thread = one kv
+// row (TMEM lane); warpgroup wg owns query columns [64 wg, 64 wg + 64) of S^T
+// / dP^T and packs its bf16 P^T / dS^T into the first 32 of those columns, so
+// the two warpgroups never touch each other's columns.  P^T is published in
+// two halves (query columns 32 hh .. 32 hh + 31 of each wg -> packed columns
+// 16 hh .. 16 hh + 15) so the dV MMAs of the first half run while the second
+// half is exponentiated.  The TS MMA k-step kk (query rows 16 kk ..) reads A
+// at column dkv_a_col(kk).
+__device__ __forceinline__ uint32_t dkv_a_col(int kk) { return (kk >> 2) * 64 + (kk & 3) * 8; }
+// k-step j (0..3) of half h: kk 2h, 2h + 1 (wg 0) and 4 + 2h, 5 + 2h (wg 1)
+__device__ __forceinline__ int dkv_half_kk(int h, int j) { return (j >> 1) * 4 + 2 * h + (j & 1); }
+
+// phase A: P^T = exp2(S^T c + nL[q]) over this thread's 64 columns at tS; the
+// fp32 P^T stays in pf for phase B; arrive(hh) after each packed half is stored
+template <class Arrive>
+__device__ __forceinline__ void dkv_phase_a(uint32_t tS, uint32_t lds, float2 sc2, int debug,
+                                            float2 (&pf)[32], Arrive&& arrive) {
+  uint32_t sv[2][32];
+  tmem_ld32(tS, sv[0]);
+  tmem_ld32(tS + 32, sv[1]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    uint32_t pp[16];
+    if (debug == 1 || debug == 2) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        pp[e] = sv[hh][2 * e];
+        pf[hh * 16 + e] = u2f2(sv[hh][2 * e], sv[hh][2 * e + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int c4 = 0; c4 < 32; c4 += 4) {
+        const float4 l4 = debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
+                                     : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
+        const float2 x0 = ffma2(u2f2(sv[hh][c4], sv[hh][c4 + 1]), sc2, make_float2(l4.x, l4.y));
+        const float2 x1 =
+            ffma2(u2f2(sv[hh][c4 + 2], sv[hh][c4 + 3]), sc2, make_float2(l4.z, l4.w));
+        const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
+        const float2 p0 =
+            (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
+        const float2 p1 =
+            ((pi + 1) % 8) < kPolyPairsDkv ? ex2_poly2(x1) : make_float2(ex2(x1.x), ex2(x1.y));
+        pp[c4 / 2] = pack_bf16(p0.x, p0.y);
+        pp[c4 / 2 + 1] = pack_bf16(p1.x, p1.y);
+        pf[pi] = p0;
+        pf[pi + 1] = p1;
+      }
+    }
+    tmem_st16(tS + hh * 16, pp);   // over S^T columns this thread has already read
+    tmem_wait_st();
+    tc_fence_before();
+    arrive(hh);
+  }
+}
+
+// phase B: dS^T = P^T (dP^T + nD[q]) over this thread's 64 columns at tP,
+// packed into the first 32 of them; arrive() once stored
+template <class Arrive>
+__device__ __forceinline__ void dkv_phase_b(uint32_t tP, uint32_t lds, int debug,
+                                            const float2 (&pf)[32], Arrive&& arrive) {
+  uint32_t gv[2][32], dd[32];
+  tmem_ld32(tP, gv[0]);
+  tmem_ld32(tP + 32, gv[1]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    if (debug == 1 || debug == 2) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[hh][2 * e];
+    } else {
+#pragma unroll
+      for (int c4 = 0; c4 < 32; c4 += 4) {
+        const float4 d4 = debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                     : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
+        const int pi = (hh * 32 + c4) / 2;
+        const float2 t0 = fadd2(u2f2(gv[hh][c4], gv[hh][c4 + 1]), make_float2(d4.x, d4.y));
+        const float2 t1 = fadd2(u2f2(gv[hh][c4 + 2], gv[hh][c4 + 3]), make_float2(d4.z, d4.w));
+        const float2 r0 = fmul2(pf[pi], t0);
+        const float2 r1 = fmul2(pf[pi + 1], t1);
+        dd[pi] = pack_bf16(r0.x, r0.y);
+        dd[pi + 1] = pack_bf16(r1.x, r1.y);
+      }
+    }
+  }
+  tmem_st32(tP, dd);
+  tmem_wait_st();
+  tc_fence_before();
+  arrive();
+}
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
@@ -117,8 +208,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   uint64_t* qd_full = bars + 1;
   uint64_t* qd_empty = qd_full + C::STAGES;
   uint64_t* s_full = qd_empty + C::STAGES;    // S^T(i) in R1
-  uint64_t* p_ready = s_full + 1;             // P^T(i) packed in R1 (256 arrivals)
-  uint64_t* dp_full = p_ready + 1;            // dP^T(i) in R2
+  uint64_t* p_ready = s_full + 1;             // [2]: P^T(i) halves packed in R1 (256 each)
+  uint64_t* dp_full = p_ready + 2;            // dP^T(i) in R2
   uint64_t* ds_ready = dp_full + 1;           // dS^T(i) packed in R2 (256 arrivals)
   uint64_t* dkv_done = ds_ready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
@@ -134,7 +225,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       mbar_init(&qd_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_ready, 256);
+    mbar_init(&p_ready[0], 256);
+    mbar_init(&p_ready[1], 256);
     mbar_init(dp_full, 1);
     mbar_init(ds_ready, 256);
     mbar_init(dkv_done, 1);
@@ -207,14 +299,16 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       }
       __syncwarp();
     };
-    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t xoff) {
-      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0)
+    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t xoff, int h) {
+      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0); half h
       if (elect_one()) {
         const uint64_t b = dm0 + qslot(i) + (xoff >> 4);
 #pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ts(tmem + acc_col, tmem + a_col + kk * 8, b + ((kk * 16 * 128) >> 4), idKV,
-                      (i > 0 || kk > 0) ? 1u : 0u);
+        for (int j = 0; j < 4; ++j) {
+          const int kk = dkv_half_kk(h, j);
+          mma_bf16_ts(tmem + acc_col, tmem + a_col + dkv_a_col(kk), b + ((kk * 16 * 128) >> 4),
+                      idKV, (i > 0 || h > 0 || j > 0) ? 1u : 0u);
+        }
       }
       __syncwarp();
     };
@@ -226,9 +320,12 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     issue_st(0, dv0, C::R2, C::QT_BYTES, dp_full);
     for (int i = 0; i < nsteps; ++i) {
       const uint32_t ph = i & 1;
-      mbar_wait(p_ready, ph);
-      tc_fence_after();
-      issue_acc(i, C::DV_COL, C::R1, C::QT_BYTES);            // dV(i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {                           // dV(i), as P^T halves land
+        mbar_wait(&p_ready[h], ph);
+        tc_fence_after();
+        issue_acc(i, C::DV_COL, C::R1, C::QT_BYTES, h);
+      }
       if (i + 1 < nsteps) {
         mbar_wait(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
         tc_fence_after();
@@ -236,7 +333,8 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       }
       mbar_wait(ds_ready, ph);
       tc_fence_after();
-      issue_acc(i, C::DK_COL, C::R2, 0);                      // dK(i)
+      issue_acc(i, C::DK_COL, C::R2, 0, 0);                   // dK(i)
+      issue_acc(i, C::DK_COL, C::R2, 0, 1);
       if (elect_one()) mma_commit(&qd_empty[i % C::STAGES]);
       __syncwarp();
       if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::QT_BYTES, dp_full);   // dP^T(i+1)
@@ -255,93 +353,14 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       const int s = i % C::STAGES;
       const uint32_t ph = i & 1;
       const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 256;
-      // phase A: P^T = exp2(S^T * c + nL[q]), 32 columns at a time
       mbar_wait(s_full, ph);
       tc_fence_after();
-      uint32_t pp[32];   // P^T packed for the dV MMA
       float2 pf[32];     // P^T in fp32 for phase B
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sv[32];
-        tmem_ld32(tl + C::R1 + wg * 64 + hh * 32, sv);
-        tmem_wait_ld();
-        if (hh == 1 && wg == 0) {   // wg 0 is done reading
-          tc_fence_before();
-          named_arrive<1>();
-        }
-        if ((p.debug == 1 || p.debug == 2)) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            pp[hh * 16 + e] = sv[2 * e];
-            pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
-          }
-        } else {
-#pragma unroll
-          for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 l4 = p.debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
-                                           : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
-            const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
-            const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
-            const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
-            const float2 p0 = (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
-            const float2 p1 = ((pi + 1) % 8) < kPolyPairsDkv ? ex2_poly2(x1)
-                                                          : make_float2(ex2(x1.x), ex2(x1.y));
-            pp[pi] = pack_bf16(p0.x, p0.y);
-            pp[pi + 1] = pack_bf16(p1.x, p1.y);
-            pf[pi] = p0;
-            pf[pi + 1] = p1;
-          }
-        }
-      }
-      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
-      if (wg == 1) {   // wg 0 has read R1
-        named_sync<1>();
-        tc_fence_after();
-      }
-      tmem_st32(tl + C::R1 + wg * 32, pp);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_ready);
-      // phase B: dS^T = P^T (dP^T + nD[q])
+      dkv_phase_a(tl + C::R1 + wg * 64, lds, sc2, p.debug, pf,
+                  [&](int hh) { mbar_arrive(&p_ready[hh]); });
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      uint32_t dd[32];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t gv[32];
-        tmem_ld32(tl + C::R2 + wg * 64 + hh * 32, gv);
-        tmem_wait_ld();
-        if (hh == 1 && wg == 0) {   // wg 0 is done reading
-          tc_fence_before();
-          named_arrive<2>();
-        }
-        if ((p.debug == 1 || p.debug == 2)) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
-        } else {
-#pragma unroll
-          for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 d4 = p.debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                           : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
-            const int pi = (hh * 32 + c4) / 2;
-            const float2 t0 = fadd2(u2f2(gv[c4], gv[c4 + 1]), make_float2(d4.x, d4.y));
-            const float2 t1 = fadd2(u2f2(gv[c4 + 2], gv[c4 + 3]), make_float2(d4.z, d4.w));
-            const float2 r0 = fmul2(pf[pi], t0);
-            const float2 r1 = fmul2(pf[pi + 1], t1);
-            dd[pi] = pack_bf16(r0.x, r0.y);
-            dd[pi + 1] = pack_bf16(r1.x, r1.y);
-          }
-        }
-      }
-      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
-      if (wg == 1) {   // wg 0 has read R2
-        named_sync<2>();
-        tc_fence_after();
-      }
-      tmem_st32(tl + C::R2 + wg * 32, dd);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(ds_ready);
+      dkv_phase_b(tl + C::R2 + wg * 64, lds, p.debug, pf, [&]() { mbar_arrive(ds_ready); });
     }
     // epilogue: warpgroup 0 drains dV, warpgroup 1 drains scale * dK.  Each warp
     // stages its 32 rows in the (now idle) Q/dO ring with the 128B swizzle, then
@@ -448,7 +467,7 @@ struct Dkv2Cfg {
   static constexpr int SLOT = ((OFF_LD + 1024 + 1023) / 1024) * 1024;
   static constexpr int STAGES = 2;
   static constexpr int QT_BYTES = QH_BYTES;   // (epilogue staging uses the slots only)
-  static constexpr int NBAR = 1 + 3 * STAGES + 5;
+  static constexpr int NBAR = 1 + 3 * STAGES + 6;
   static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
   static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
   static_assert(D == 128, "the d halves are one 128-byte panel each");
@@ -475,8 +494,8 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   uint64_t* ld_full = qd_full + C::STAGES;    // local: this CTA's nL / nD rows
   uint64_t* qd_empty = ld_full + C::STAGES;   // both (multicast commit)
   uint64_t* s_full = qd_empty + C::STAGES;    // both
-  uint64_t* p_ready = s_full + 1;             // leader: one arrival per softmax warp (16)
-  uint64_t* dp_full = p_ready + 1;            // both
+  uint64_t* p_ready = s_full + 1;             // leader [2]: one arrival per softmax warp (16)
+  uint64_t* dp_full = p_ready + 2;            // both
   uint64_t* ds_ready = dp_full + 1;           // leader: 16
   uint64_t* dkv_done = ds_ready + 1;          // both
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
@@ -503,7 +522,8 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_init(&qd_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_ready, 16);
+    mbar_init(&p_ready[0], 16);
+    mbar_init(&p_ready[1], 16);
     mbar_init(dp_full, 1);
     mbar_init(ds_ready, 16);
     mbar_init(dkv_done, 1);
@@ -580,14 +600,16 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         __syncwarp();
       };
-      auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t boff) {
+      auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t boff, int h) {
         // dV += P^T dO (a_col R1, d half of dO) ; dK += dS^T Q (a_col R2, d half of Q)
         if (elect_one()) {
           const uint64_t b = dm0 + qslot(i) + (boff >> 4);
 #pragma unroll
-          for (int kk = 0; kk < 128 / 16; ++kk)
-            mma2_bf16_ts(tmem + acc_col, tmem + a_col + kk * 8, b + ((kk * 16 * 128) >> 4), idKV,
-                         (i > 0 || kk > 0) ? 1u : 0u);
+          for (int j = 0; j < 4; ++j) {
+            const int kk = dkv_half_kk(h, j);
+            mma2_bf16_ts(tmem + acc_col, tmem + a_col + dkv_a_col(kk),
+                         b + ((kk * 16 * 128) >> 4), idKV, (i > 0 || h > 0 || j > 0) ? 1u : 0u);
+          }
         }
         __syncwarp();
       };
@@ -599,9 +621,12 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       issue_st(0, dv0, C::R2, C::OFF_GQ, dp_full);
       for (int i = 0; i < nsteps; ++i) {
         const uint32_t ph = i & 1;
-        mbar_wait_cluster(p_ready, ph);
-        tc_fence_after();
-        issue_acc(i, C::DV_COL, C::R1, C::OFF_GD);             // dV(i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {                          // dV(i), as P^T halves land
+          mbar_wait_cluster(&p_ready[h], ph);
+          tc_fence_after();
+          issue_acc(i, C::DV_COL, C::R1, C::OFF_GD, h);
+        }
         if (i + 1 < nsteps) {
           mbar_wait_cluster(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
           tc_fence_after();
@@ -609,7 +634,8 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         mbar_wait_cluster(ds_ready, ph);
         tc_fence_after();
-        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD);             // dK(i)
+        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD, 0);          // dK(i)
+        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD, 1);
         if (elect_one()) mma2_commit_mc(&qd_empty[i % C::STAGES]);
         __syncwarp();
         if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::OFF_GQ, dp_full);   // dP^T(i+1)
@@ -633,90 +659,12 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_wait(&ld_full[s], (i / C::STAGES) & 1);   // this CTA's nL / nD rows
       mbar_wait(s_full, ph);
       tc_fence_after();
-      uint32_t pp[32];   // P^T packed for the dV MMA
       float2 pf[32];     // P^T in fp32 for phase B
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sv[32];
-        tmem_ld32(tl + C::R1 + wg * 64 + hh * 32, sv);
-        tmem_wait_ld();
-        if (hh == 1 && wg == 0) {   // wg 0 is done reading
-          tc_fence_before();
-          named_arrive<1>();
-        }
-        if ((p.debug == 1 || p.debug == 2)) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            pp[hh * 16 + e] = sv[2 * e];
-            pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
-          }
-        } else {
-#pragma unroll
-          for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 l4 = p.debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
-                                           : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
-            const float2 x0 = ffma2(u2f2(sv[c4], sv[c4 + 1]), sc2, make_float2(l4.x, l4.y));
-            const float2 x1 = ffma2(u2f2(sv[c4 + 2], sv[c4 + 3]), sc2, make_float2(l4.z, l4.w));
-            const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
-            const float2 p0 = (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
-            const float2 p1 = ((pi + 1) % 8) < kPolyPairsDkv ? ex2_poly2(x1)
-                                                          : make_float2(ex2(x1.x), ex2(x1.y));
-            pp[pi] = pack_bf16(p0.x, p0.y);
-            pp[pi + 1] = pack_bf16(p1.x, p1.y);
-            pf[pi] = p0;
-            pf[pi + 1] = p1;
-          }
-        }
-      }
-      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
-      if (wg == 1) {   // wg 0 has read R1
-        named_sync<1>();
-        tc_fence_after();
-      }
-      tmem_st32(tl + C::R1 + wg * 32, pp);
-      tmem_wait_st();
-      tc_fence_before();
-      arrive_pair(p_ready);
-      // phase B: dS^T = P^T (dP^T + nD[q])
+      dkv_phase_a(tl + C::R1 + wg * 64, lds, sc2, p.debug, pf,
+                  [&](int hh) { arrive_pair(&p_ready[hh]); });
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      uint32_t dd[32];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t gv[32];
-        tmem_ld32(tl + C::R2 + wg * 64 + hh * 32, gv);
-        tmem_wait_ld();
-        if (hh == 1 && wg == 0) {   // wg 0 is done reading
-          tc_fence_before();
-          named_arrive<2>();
-        }
-        if ((p.debug == 1 || p.debug == 2)) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
-        } else {
-#pragma unroll
-          for (int c4 = 0; c4 < 32; c4 += 4) {
-            const float4 d4 = p.debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                           : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
-            const int pi = (hh * 32 + c4) / 2;
-            const float2 t0 = fadd2(u2f2(gv[c4], gv[c4 + 1]), make_float2(d4.x, d4.y));
-            const float2 t1 = fadd2(u2f2(gv[c4 + 2], gv[c4 + 3]), make_float2(d4.z, d4.w));
-            const float2 r0 = fmul2(pf[pi], t0);
-            const float2 r1 = fmul2(pf[pi + 1], t1);
-            dd[pi] = pack_bf16(r0.x, r0.y);
-            dd[pi + 1] = pack_bf16(r1.x, r1.y);
-          }
-        }
-      }
-      // wg 1 packs into columns wg 0 reads; wg 0 only overwrites its own inputs
-      if (wg == 1) {   // wg 0 has read R2
-        named_sync<2>();
-        tc_fence_after();
-      }
-      tmem_st32(tl + C::R2 + wg * 32, dd);
-      tmem_wait_st();
-      tc_fence_before();
-      arrive_pair(ds_ready);
+      dkv_phase_b(tl + C::R2 + wg * 64, lds, p.debug, pf, [&]() { arrive_pair(ds_ready); });
     }
     // epilogue (as bwd_dkv_kernel): this CTA's 128 rows, staged in its Q/dO ring
     mbar_wait(dkv_done, 0);
