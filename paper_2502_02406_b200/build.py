@@ -7,7 +7,8 @@ Each ``csrc/*.cu`` is compiled to an object in parallel with
 ``paper_2502_02406_b200/liblvx_b200.so`` with the static CUDA runtime, so the
 library loads on a CPU-only host (the driver is reached at run time through
 ``cudaGetDriverEntryPoint``).  ``-Xptxas -v`` output goes to
-``build/ptxas.log``.
+``build/ptxas.log``.  ``LVX_NVCC_EXTRA`` appends flags (variant builds for
+same-box A/B runs: tools/build_variant.sh).
 """
 from __future__ import annotations
 
@@ -25,7 +26,7 @@ BUILD = ROOT / "build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-         "-I", str(ROOT / "include")]
+         "-I", str(ROOT / "include")] + os.environ.get("LVX_NVCC_EXTRA", "").split()
 
 
 def _sources():

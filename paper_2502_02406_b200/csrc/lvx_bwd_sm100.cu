@@ -38,6 +38,36 @@ constexpr int kStep = 64;      // q rows per step (dkv kernel) / kv rows per ste
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kPolyPairs = 3;   // of every 8 column pairs, exp2 by polynomial (FMA pipe)
 constexpr int kPolyPairsDkv = 2; // the same for the dK/dV kernel's phase A
+#ifndef LVX_DKV_CHUNKS
+#define LVX_DKV_CHUNKS 2
+#endif
+constexpr int kDkvChunks = LVX_DKV_CHUNKS;   // P^T publication chunks per step (dK/dV kernel)
+#ifndef LVX_DKV_ARRIVALS
+#define LVX_DKV_ARRIVALS 256
+#endif
+constexpr int kDkvArrivals = LVX_DKV_ARRIVALS;   // per hand-off barrier: 256 threads or 8 warps
+
+// Profiling switches (p.debug) compile to nothing in the product build
+#ifdef LVX_BWD_DEBUG_MODES
+#define BWD_DBG(cond) (cond)
+#else
+#define BWD_DBG(cond) false
+#endif
+
+// LVX_DKV_TRACE=<cta x> (profiling builds only, tools/dkv_trace.py): clock64
+// stamps of one dK/dV CTA's hand-offs, [role][step][event]
+#ifdef LVX_DKV_TRACE
+__device__ long long g_dkv_trace[4][64][8];
+#define DKV_STAMP(role, step, ev)                                                  \
+  do {                                                                             \
+    if (blockIdx.x == LVX_DKV_TRACE && blockIdx.y == 0 && (step) < 64 && lane == 0) \
+      g_dkv_trace[role][step][ev] = clock64();                                     \
+  } while (0)
+#else
+#define DKV_STAMP(role, step, ev) \
+  do {                            \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------- prep
 __global__ void bwd_prep_kernel(View3<const float> L, View3<const float> Dv, int hq, int rows,
@@ -68,7 +98,8 @@ struct BwdParams {
   int out_bf16;                   //   when overwriting in the input dtype
   int64_t dk_hs, dk_rs, dv_hs, dv_rs;
   float* ws_dq;       // [splits][hq][rows_q][D]
-  int debug;          // LVX_BWD_DEBUG (profiling only): 1 = skip exp / dS math,
+  int debug;          // LVX_BWD_DEBUG, honoured only by -DLVX_BWD_DEBUG_MODES builds
+                      // (tools/build_variant.sh; profiling): 1 = skip exp / dS math,
                       // 2 = also skip Q/dO reloads (dkv), 3 = skip reloads only,
                       // 4 = skip the dK/dV drain, 5 = no nL/nD shared loads (dkv)
 };
@@ -81,7 +112,7 @@ struct BwdParams {
 //   R2 [128,256)  dP^T(i), then dS^T(i) packed bf16 (the same columns of R2)
 //   dV [256, 256+D), dK [256+D, 256+2D)
 // Two-phase softmax per step: phase A turns S^T into P^T (the exponentials)
-// and releases dV(i) in two halves, then S^T(i+1); phase B turns dP^T into
+// and releases dV(i) in kDkvChunks chunks, then S^T(i+1); phase B turns dP^T into
 // dS^T while the tensor pipe runs dV(i) / S^T(i+1), then releases dK(i) and
 // dP^T(i+1).  P stays in fp32 registers between the phases (R1 is
 // overwritten by S^T(i+1) as soon as dV(i) has read it).  Two softmax
@@ -91,53 +122,70 @@ struct DkvCfg {
   static constexpr int PANELS = D / 64;
   static constexpr int KV_BYTES = 128 * D * 2;             // resident K (or V) tile
   static constexpr int QT_BYTES = 128 * D * 2;             // one Q (or dO) 128-row step tile
-  static constexpr int SLOT = ((2 * QT_BYTES + 1024 + 1023) / 1024) * 1024;
-  static constexpr int STAGES = D == 128 ? 2 : 4;
-  static constexpr int NBAR = 1 + 2 * STAGES + 6;
-  static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
+  // separate rings: Q (+ the step's nL / nD rows) is released after dK, dO
+  // after dV, so each load gets more than one step of lead time (the L2 ->
+  // SMEM stream of all CTAs runs at ~75 % of the chip's TMA throughput)
+  static constexpr int QSTAGES = D == 128 ? 3 : 4, GSTAGES = D == 128 ? 2 : 4;
+  // nD (read in phase B, until dK) rides with Q, nL (read in phase A, before
+  // dV) with dO
+  static constexpr int OFF_G = QSTAGES * QT_BYTES;                // dO tiles
+  static constexpr int OFF_LD = OFF_G + GSTAGES * QT_BYTES;      // nD rows [QSTAGES][512]
+  static constexpr int OFF_LL = OFF_LD + QSTAGES * 512;          // nL rows [GSTAGES][512]
+  static constexpr int NBAR = 1 + 2 * QSTAGES + 2 * GSTAGES + 4 + kDkvChunks;
+  static constexpr int RING = OFF_LL + GSTAGES * 512;
+  // no alignment pad at d = 128 (it would not fit 227 KB): the kernel traps
+  // unless the dynamic shared memory base is 1024-byte aligned
+  static constexpr int PAD = D == 128 ? 0 : 1024;
+  static constexpr int SMEM = PAD + 2 * KV_BYTES + RING + NBAR * 8 + 16;
   static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
-  static_assert(8 * 32 * D * 4 <= STAGES * SLOT, "epilogue staging must fit the Q/dO ring");
+  static_assert(8 * 32 * D * 4 <= OFF_LD, "epilogue staging must fit the Q/dO rings");
+  static_assert(SMEM <= 232448, "227 KB of shared memory per CTA");
 };
 
 // dK / dV softmax, shared by the 1-CTA and CTA-pair kernels.  Thread = one kv
 // row (TMEM lane); warpgroup wg owns query columns [64 wg, 64 wg + 64) of S^T
 // / dP^T and packs its bf16 P^T / dS^T into the first 32 of those columns, so
 // the two warpgroups never touch each other's columns.  P^T is published in
-// two halves (query columns 32 hh .. 32 hh + 31 of each wg -> packed columns
-// 16 hh .. 16 hh + 15) so the dV MMAs of the first half run while the second
-// half is exponentiated.  The TS MMA k-step kk (query rows 16 kk ..) reads A
-// at column dkv_a_col(kk).
+// kDkvChunks chunks (query columns 64/kDkvChunks c .. of each wg) so the dV
+// MMAs of the first chunks run while later ones are still exponentiated.
+// The TS MMA k-step kk (query rows 16 kk ..) reads A at column dkv_a_col(kk).
 __device__ __forceinline__ uint32_t dkv_a_col(int kk) { return (kk >> 2) * 64 + (kk & 3) * 8; }
-// k-step j (0..3) of half h: kk 2h, 2h + 1 (wg 0) and 4 + 2h, 5 + 2h (wg 1)
-__device__ __forceinline__ int dkv_half_kk(int h, int j) { return (j >> 1) * 4 + 2 * h + (j & 1); }
+// k-step j (0 .. 8/kDkvChunks - 1) of chunk c, both warpgroups' columns
+__device__ __forceinline__ int dkv_chunk_kk(int c, int j) {
+  constexpr int kpw = 4 / kDkvChunks;
+  return (j / kpw) * 4 + c * kpw + j % kpw;
+}
 
 // phase A: P^T = exp2(S^T c + nL[q]) over this thread's 64 columns at tS; the
-// fp32 P^T stays in pf for phase B; arrive(hh) after each packed half is stored
+// fp32 P^T stays in pf for phase B; arrive(c) after each packed chunk is stored
 template <class Arrive>
 __device__ __forceinline__ void dkv_phase_a(uint32_t tS, uint32_t lds, float2 sc2, int debug,
                                             float2 (&pf)[32], Arrive&& arrive) {
+  constexpr int CW = 64 / kDkvChunks;   // query columns per chunk
   uint32_t sv[2][32];
   tmem_ld32(tS, sv[0]);
   tmem_ld32(tS + 32, sv[1]);
   tmem_wait_ld();
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    uint32_t pp[16];
-    if (debug == 1 || debug == 2) {
+  for (int c = 0; c < kDkvChunks; ++c) {
+    uint32_t pp[CW / 2];
+    if (BWD_DBG(debug == 1 || debug == 2)) {   // profiling: no exp math
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        pp[e] = sv[hh][2 * e];
-        pf[hh * 16 + e] = u2f2(sv[hh][2 * e], sv[hh][2 * e + 1]);
+      for (int c2 = 0; c2 < CW; c2 += 2) {
+        const int col = c * CW + c2;
+        pp[c2 / 2] = sv[col / 32][col % 32];
+        pf[col / 2] = u2f2(sv[col / 32][col % 32], sv[col / 32][col % 32 + 1]);
       }
     } else {
 #pragma unroll
-      for (int c4 = 0; c4 < 32; c4 += 4) {
-        const float4 l4 = debug == 5 ? make_float4(-1.f, -1.f, -1.f, -1.f)
-                                     : ld_shared_f4(lds + (hh * 32 + c4) * 4);   // -L log2 e per q
-        const float2 x0 = ffma2(u2f2(sv[hh][c4], sv[hh][c4 + 1]), sc2, make_float2(l4.x, l4.y));
+      for (int c4 = 0; c4 < CW; c4 += 4) {
+        const int col = c * CW + c4, hh = col / 32, k = col % 32, pi = col / 2;
+        const float4 l4 = BWD_DBG(debug == 5) ? make_float4(-1.f, -1.f, -1.f, -1.f)
+                                              : ld_shared_f4(lds + col * 4);   // -L log2 e per q
+        const float2 x0 = ffma2(u2f2(sv[hh][k], sv[hh][k + 1]), sc2, make_float2(l4.x, l4.y));
         const float2 x1 =
-            ffma2(u2f2(sv[hh][c4 + 2], sv[hh][c4 + 3]), sc2, make_float2(l4.z, l4.w));
-        const int pi = (hh * 32 + c4) / 2;   // phase A is MUFU-bound: some pairs on the FMA pipe
+            ffma2(u2f2(sv[hh][k + 2], sv[hh][k + 3]), sc2, make_float2(l4.z, l4.w));
+        // phase A is MUFU-bound: some pairs on the FMA pipe
         const float2 p0 =
             (pi % 8) < kPolyPairsDkv ? ex2_poly2(x0) : make_float2(ex2(x0.x), ex2(x0.y));
         const float2 p1 =
@@ -148,17 +196,17 @@ __device__ __forceinline__ void dkv_phase_a(uint32_t tS, uint32_t lds, float2 sc
         pf[pi + 1] = p1;
       }
     }
-    tmem_st16(tS + hh * 16, pp);   // over S^T columns this thread has already read
+    tmem_st_n(tS + c * (CW / 2), pp);   // over columns this thread has already read
     tmem_wait_st();
     tc_fence_before();
-    arrive(hh);
+    arrive(c);
   }
 }
 
 // phase B: dS^T = P^T (dP^T + nD[q]) over this thread's 64 columns at tP,
 // packed into the first 32 of them; arrive() once stored
 template <class Arrive>
-__device__ __forceinline__ void dkv_phase_b(uint32_t tP, uint32_t lds, int debug,
+__device__ __forceinline__ void dkv_phase_b(uint32_t tP, uint32_t ldd, int debug,
                                             const float2 (&pf)[32], Arrive&& arrive) {
   uint32_t gv[2][32], dd[32];
   tmem_ld32(tP, gv[0]);
@@ -166,14 +214,14 @@ __device__ __forceinline__ void dkv_phase_b(uint32_t tP, uint32_t lds, int debug
   tmem_wait_ld();
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
-    if (debug == 1 || debug == 2) {
+    if (BWD_DBG(debug == 1 || debug == 2)) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[hh][2 * e];
     } else {
 #pragma unroll
       for (int c4 = 0; c4 < 32; c4 += 4) {
-        const float4 d4 = debug == 5 ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                     : ld_shared_f4(lds + 512 + (hh * 32 + c4) * 4);   // -D per q
+        const float4 d4 = BWD_DBG(debug == 5) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                              : ld_shared_f4(ldd + (hh * 32 + c4) * 4);   // -D per q
         const int pi = (hh * 32 + c4) / 2;
         const float2 t0 = fadd2(u2f2(gv[hh][c4], gv[hh][c4 + 1]), make_float2(d4.x, d4.y));
         const float2 t1 = fadd2(u2f2(gv[hh][c4 + 2], gv[hh][c4 + 3]), make_float2(d4.z, d4.w));
@@ -202,14 +250,16 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::KV_BYTES;
-  uint8_t* sSlot = sV + C::KV_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + C::STAGES * C::SLOT);
+  uint8_t* sSlot = sV + C::KV_BYTES;          // Q tiles | dO tiles | nL/nD rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + C::RING);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;
-  uint64_t* qd_empty = qd_full + C::STAGES;
-  uint64_t* s_full = qd_empty + C::STAGES;    // S^T(i) in R1
-  uint64_t* p_ready = s_full + 1;             // [2]: P^T(i) halves packed in R1 (256 each)
-  uint64_t* dp_full = p_ready + 2;            // dP^T(i) in R2
+  uint64_t* q_full = bars + 1;                // Q(i), nD(i)
+  uint64_t* q_empty = q_full + C::QSTAGES;    // after dK(i)
+  uint64_t* g_full = q_empty + C::QSTAGES;    // dO(i), nL(i)
+  uint64_t* g_empty = g_full + C::GSTAGES;    // after dV(i)
+  uint64_t* s_full = g_empty + C::GSTAGES;    // S^T(i) in R1
+  uint64_t* p_ready = s_full + 1;             // [kDkvChunks]: P^T(i) chunks in R1 (256 each)
+  uint64_t* dp_full = p_ready + kDkvChunks;   // dP^T(i) in R2
   uint64_t* ds_ready = dp_full + 1;           // dS^T(i) packed in R2 (256 arrivals)
   uint64_t* dkv_done = ds_ready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
@@ -218,17 +268,21 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   const int n0 = blockIdx.x * 128, g = blockIdx.y;
   const int nsteps = p.G * p.tpq;
 
+  if (C::PAD == 0 && (raw_u & 1023u)) __trap();   // SW128 tiles need 1024-byte alignment
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&qd_full[s], 1);
-      mbar_init(&qd_empty[s], 1);
+    for (int s = 0; s < C::QSTAGES; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < C::GSTAGES; ++s) {
+      mbar_init(&g_full[s], 1);
+      mbar_init(&g_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(&p_ready[0], 256);
-    mbar_init(&p_ready[1], 256);
+    for (int c = 0; c < kDkvChunks; ++c) mbar_init(&p_ready[c], kDkvArrivals);
     mbar_init(dp_full, 1);
-    mbar_init(ds_ready, 256);
+    mbar_init(ds_ready, kDkvArrivals);
     mbar_init(dkv_done, 1);
     fence_barrier_init();
   }
@@ -256,24 +310,36 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         tma_load_3d_hint(sK + pn * 128 * 128, &tmK, kv_full, pn * 64, n0, g, once);
         tma_load_3d_hint(sV + pn * 128 * 128, &tmV, kv_full, pn * 64, n0, g, once);
       }
+      // in pipe order a Q slot frees (dK(i - QSTAGES)) before a dO slot (dV(i - GSTAGES))
       for (int i = 0; i < nsteps; ++i) {
-        const int s = i % C::STAGES, u = i / C::STAGES;
-        if (u > 0) mbar_wait(&qd_empty[s], (u - 1) & 1);
+        const int sq = i % C::QSTAGES, uq = i / C::QSTAGES;
+        const int sg = i % C::GSTAGES, ug = i / C::GSTAGES;
         const int h = g * p.G + i / p.tpq, r0 = (i % p.tpq) * 128;
-        uint8_t* slot = sSlot + s * C::SLOT;
-        if ((p.debug == 2 || p.debug == 3) && u > 0) {   // profiling: no reloads (stale data)
-          mbar_arrive(&qd_full[s]);
-          continue;
+        const bool reload = !BWD_DBG((p.debug == 2 || p.debug == 3) && i >= C::QSTAGES);
+        if (uq > 0) mbar_wait(&q_empty[sq], (uq - 1) & 1);
+        DKV_STAMP(3, i, 0);
+        if (!reload) {   // profiling: no reloads (stale data)
+          mbar_arrive(&q_full[sq]);
+        } else {
+          uint8_t* qt = sSlot + sq * C::QT_BYTES;
+          mbar_arrive_expect_tx(&q_full[sq], C::QT_BYTES + 512);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_3d_hint(qt + pn * 128 * 128, &tmQ, &q_full[sq], pn * 64, r0, h, shared);
+          bulk_load_hint(sSlot + C::OFF_LD + sq * 512, p.Dp + (size_t)h * p.rows_pad + r0, 512,
+                         &q_full[sq], shared);
         }
-        mbar_arrive_expect_tx(&qd_full[s], 2 * C::QT_BYTES + 1024);
-        for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_3d_hint(slot + pn * 128 * 128, &tmQ, &qd_full[s], pn * 64, r0, h, shared);
-          tma_load_3d_hint(slot + C::QT_BYTES + pn * 128 * 128, &tmG, &qd_full[s], pn * 64, r0,
-                           h, shared);
+        if (ug > 0) mbar_wait(&g_empty[sg], (ug - 1) & 1);
+        DKV_STAMP(3, i, 1);
+        if (!reload || BWD_DBG((p.debug == 2 || p.debug == 3) && i >= C::GSTAGES)) {
+          mbar_arrive(&g_full[sg]);
+        } else {
+          uint8_t* gt = sSlot + C::OFF_G + sg * C::QT_BYTES;
+          mbar_arrive_expect_tx(&g_full[sg], C::QT_BYTES + 512);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_3d_hint(gt + pn * 128 * 128, &tmG, &g_full[sg], pn * 64, r0, h, shared);
+          bulk_load_hint(sSlot + C::OFF_LL + sg * 512, p.Lp + (size_t)h * p.rows_pad + r0, 512,
+                         &g_full[sg], shared);
         }
-        const size_t off = (size_t)h * p.rows_pad + r0;
-        bulk_load_hint(slot + 2 * C::QT_BYTES, p.Lp + off, 512, &qd_full[s], shared);
-        bulk_load_hint(slot + 2 * C::QT_BYTES + 512, p.Dp + off, 512, &qd_full[s], shared);
       }
     }
   } else if (warp == 9) {
@@ -285,11 +351,14 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const uint64_t dv0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
     const uint64_t ds0 = umma_desc_sw128(smem_u32(sSlot), 0, 1024);        // K-major Q / dO
     const uint64_t dm0 = umma_desc_sw128(smem_u32(sSlot), 128 * 128, 1024);  // MN-major Q / dO
-    auto qslot = [&](int i) { return (uint64_t)(((i % C::STAGES) * C::SLOT) >> 4); };
-    auto issue_st = [&](int i, uint64_t a0, uint32_t col, uint32_t xoff, uint64_t* bar) {
+    auto qoff = [&](int i) { return (uint64_t)(((i % C::QSTAGES) * C::QT_BYTES) >> 4); };
+    auto goff = [&](int i) {
+      return (uint64_t)((C::OFF_G + (i % C::GSTAGES) * C::QT_BYTES) >> 4);
+    };
+    auto issue_st = [&](uint64_t a0, uint32_t col, uint64_t boff, uint64_t* bar) {
       // col R1: S^T = K Q^T ; col R2: dP^T = V dO^T   (M=128 kv, N=128 q, K=D)
       if (elect_one()) {
-        const uint64_t b = ds0 + qslot(i) + (xoff >> 4);
+        const uint64_t b = ds0 + boff;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t o = ((kk >> 2) * (128 * 128) + (kk & 3) * 32) >> 4;
@@ -299,45 +368,59 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
       }
       __syncwarp();
     };
-    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t xoff, int h) {
-      // dV += P^T dO (a_col R1, xoff dO) ; dK += dS^T Q (a_col R2, xoff 0); half h
+    auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint64_t boff, int c) {
+      // dV += P^T dO (a_col R1, dO) ; dK += dS^T Q (a_col R2, Q); chunk c
       if (elect_one()) {
-        const uint64_t b = dm0 + qslot(i) + (xoff >> 4);
+        const uint64_t b = dm0 + boff;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int kk = dkv_half_kk(h, j);
+        for (int j = 0; j < 8 / kDkvChunks; ++j) {
+          const int kk = dkv_chunk_kk(c, j);
           mma_bf16_ts(tmem + acc_col, tmem + a_col + dkv_a_col(kk), b + ((kk * 16 * 128) >> 4),
-                      idKV, (i > 0 || h > 0 || j > 0) ? 1u : 0u);
+                      idKV, (i > 0 || c > 0 || j > 0) ? 1u : 0u);
         }
       }
       __syncwarp();
     };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) mma_commit(bar);
+      __syncwarp();
+    };
     mbar_wait(kv_full, 0);
     tc_fence_after();
-    mbar_wait(&qd_full[0], 0);
+    mbar_wait(&q_full[0], 0);
     tc_fence_after();
-    issue_st(0, dk0, C::R1, 0, s_full);
-    issue_st(0, dv0, C::R2, C::QT_BYTES, dp_full);
+    issue_st(dk0, C::R1, qoff(0), s_full);
+    mbar_wait(&g_full[0], 0);
+    tc_fence_after();
+    issue_st(dv0, C::R2, goff(0), dp_full);
     for (int i = 0; i < nsteps; ++i) {
       const uint32_t ph = i & 1;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {                           // dV(i), as P^T halves land
-        mbar_wait(&p_ready[h], ph);
+      for (int c = 0; c < kDkvChunks; ++c) {                  // dV(i), as P^T chunks land
+        mbar_wait(&p_ready[c], ph);
+        DKV_STAMP(2, i, c);
         tc_fence_after();
-        issue_acc(i, C::DV_COL, C::R1, C::QT_BYTES, h);
+        issue_acc(i, C::DV_COL, C::R1, goff(i), c);
       }
+      commit(&g_empty[i % C::GSTAGES]);                       // dO(i) slot after dV(i)
       if (i + 1 < nsteps) {
-        mbar_wait(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
+        mbar_wait(&q_full[(i + 1) % C::QSTAGES], ((i + 1) / C::QSTAGES) & 1);
+        DKV_STAMP(2, i, 4);
         tc_fence_after();
-        issue_st(i + 1, dk0, C::R1, 0, s_full);               // S^T(i+1) after dV(i) read R1
+        issue_st(dk0, C::R1, qoff(i + 1), s_full);            // S^T(i+1) after dV(i) read R1
       }
       mbar_wait(ds_ready, ph);
+      DKV_STAMP(2, i, 5);
       tc_fence_after();
-      issue_acc(i, C::DK_COL, C::R2, 0, 0);                   // dK(i)
-      issue_acc(i, C::DK_COL, C::R2, 0, 1);
-      if (elect_one()) mma_commit(&qd_empty[i % C::STAGES]);
-      __syncwarp();
-      if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::QT_BYTES, dp_full);   // dP^T(i+1)
+#pragma unroll
+      for (int c = 0; c < kDkvChunks; ++c) issue_acc(i, C::DK_COL, C::R2, qoff(i), c);   // dK(i)
+      commit(&q_empty[i % C::QSTAGES]);                       // Q(i), nL / nD(i) after dK(i)
+      if (i + 1 < nsteps) {
+        mbar_wait(&g_full[(i + 1) % C::GSTAGES], ((i + 1) / C::GSTAGES) & 1);
+        DKV_STAMP(2, i, 6);
+        tc_fence_after();
+        issue_st(dv0, C::R2, goff(i + 1), dp_full);           // dP^T(i+1)
+      }
     }
     if (elect_one()) mma_commit(dkv_done);
     __syncwarp();
@@ -350,17 +433,31 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     for (int i = 0; i < nsteps; ++i) {
-      const int s = i % C::STAGES;
       const uint32_t ph = i & 1;
-      const uint32_t lds = smem_u32(sSlot + s * C::SLOT + 2 * C::QT_BYTES) + wg * 256;
+      const uint32_t ldl = smem_u32(sSlot + C::OFF_LL + (i % C::GSTAGES) * 512) + wg * 256;
+      const uint32_t ldd = smem_u32(sSlot + C::OFF_LD + (i % C::QSTAGES) * 512) + wg * 256;
+      mbar_wait(&g_full[i % C::GSTAGES], (i / C::GSTAGES) & 1);   // nL(i)
       mbar_wait(s_full, ph);
+      if (q4 == 0) DKV_STAMP(wg, i, 0);
       tc_fence_after();
       float2 pf[32];     // P^T in fp32 for phase B
-      dkv_phase_a(tl + C::R1 + wg * 64, lds, sc2, p.debug, pf,
-                  [&](int hh) { mbar_arrive(&p_ready[hh]); });
+      auto arrive = [&](uint64_t* bar) {
+        if constexpr (kDkvArrivals == 8) {   // one lane per warp after the warp converges
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar);
+        } else {
+          mbar_arrive(bar);
+        }
+      };
+      dkv_phase_a(tl + C::R1 + wg * 64, ldl, sc2, p.debug, pf, [&](int c) {
+        arrive(&p_ready[c]);
+        if (q4 == 0) DKV_STAMP(wg, i, 1 + c);
+      });
       mbar_wait(dp_full, ph);
+      if (q4 == 0) DKV_STAMP(wg, i, 5);
       tc_fence_after();
-      dkv_phase_b(tl + C::R2 + wg * 64, lds, p.debug, pf, [&]() { mbar_arrive(ds_ready); });
+      dkv_phase_b(tl + C::R2 + wg * 64, ldd, p.debug, pf, [&]() { arrive(ds_ready); });
+      if (q4 == 0) DKV_STAMP(wg, i, 6);
     }
     // epilogue: warpgroup 0 drains dV, warpgroup 1 drains scale * dK.  Each warp
     // stages its 32 rows in the (now idle) Q/dO ring with the 128B swizzle, then
@@ -388,7 +485,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (!p.accumulate && p.out_bf16 && p.debug != 4) {
+    if (!p.accumulate && p.out_bf16 && !BWD_DBG(p.debug == 4)) {
       // overwrite in bf16: each 8-lane group packs 64 columns of one row (two
       // staged 32-column chunks) into one full 128-byte line
       __nv_bfloat16* base = static_cast<__nv_bfloat16*>(wg ? p.dk_ptr : p.dv_ptr);
@@ -409,7 +506,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                            pack_bf16(b.z, b.w));
         }
       }
-    } else if (!p.accumulate && p.debug != 4) {   // 4: profiling, no drain
+    } else if (!p.accumulate && !BWD_DBG(p.debug == 4)) {   // 4: profiling, no drain
       // overwrite: each 8-lane group stores one full 128-byte row segment
       // (STG.128, whole lines); measured ~5 % faster than TMA tensor stores here
       float* base = static_cast<float*>(wg ? p.dk_ptr : p.dv_ptr);
@@ -426,7 +523,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             *reinterpret_cast<float4*>(base + g * hs + (int64_t)grow * rs + c * 32 + q * 4) = val;
         }
       }
-    } else if (p.accumulate && lane == 0 && p.debug != 4) {   // reduce-add in L2
+    } else if (p.accumulate && lane == 0 && !BWD_DBG(p.debug == 4)) {   // reduce-add in L2
       const CUtensorMap* m = wg ? &tmDK : &tmDV;
       const uint64_t pol = l2_evict_first();   // written once, not re-read here
       for (int c = 0; c < D / 32; ++c)
@@ -467,7 +564,7 @@ struct Dkv2Cfg {
   static constexpr int SLOT = ((OFF_LD + 1024 + 1023) / 1024) * 1024;
   static constexpr int STAGES = 2;
   static constexpr int QT_BYTES = QH_BYTES;   // (epilogue staging uses the slots only)
-  static constexpr int NBAR = 1 + 3 * STAGES + 6;
+  static constexpr int NBAR = 1 + 3 * STAGES + 4 + kDkvChunks;
   static constexpr int SMEM = 1024 + 2 * KV_BYTES + STAGES * SLOT + NBAR * 8 + 16;
   static constexpr int R1 = 0, R2 = 128, DV_COL = 256, DK_COL = 256 + D;
   static_assert(D == 128, "the d halves are one 128-byte panel each");
@@ -494,9 +591,9 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   uint64_t* ld_full = qd_full + C::STAGES;    // local: this CTA's nL / nD rows
   uint64_t* qd_empty = ld_full + C::STAGES;   // both (multicast commit)
   uint64_t* s_full = qd_empty + C::STAGES;    // both
-  uint64_t* p_ready = s_full + 1;             // leader [2]: one arrival per softmax warp (16)
-  uint64_t* dp_full = p_ready + 2;            // both
-  uint64_t* ds_ready = dp_full + 1;           // leader: 16
+  uint64_t* p_ready = s_full + 1;             // leader [kDkvChunks]: 512 arrivals each
+  uint64_t* dp_full = p_ready + kDkvChunks;   // both
+  uint64_t* ds_ready = dp_full + 1;           // leader: 512
   uint64_t* dkv_done = ds_ready + 1;          // both
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
@@ -504,14 +601,10 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   const uint32_t rank = cluster_ctarank();
   const int n0 = (blockIdx.x >> 1) * 256 + (int)rank * 128, g = blockIdx.y;
   const int nsteps = p.G * p.tpq;
-  // one arrival per softmax warp on the leader's copy of bar (16 per pair):
-  // every lane has waited for its TMEM stores and fenced before the warp syncs
+  // one arrival per softmax thread of both CTAs on the leader's copy of bar (512)
   auto arrive_pair = [&](uint64_t* bar) {
-    __syncwarp();
-    if (lane == 0) {
-      if (rank == 0) mbar_arrive(bar);
-      else mbar_arrive_cluster(leader_addr(bar));
-    }
+    if (rank == 0) mbar_arrive(bar);
+    else mbar_arrive_cluster(leader_addr(bar));
   };
 
   if (threadIdx.x == 0) {
@@ -522,10 +615,9 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_init(&qd_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(&p_ready[0], 16);
-    mbar_init(&p_ready[1], 16);
+    for (int c = 0; c < kDkvChunks; ++c) mbar_init(&p_ready[c], 512);
     mbar_init(dp_full, 1);
-    mbar_init(ds_ready, 16);
+    mbar_init(ds_ready, 512);
     mbar_init(dkv_done, 1);
     fence_barrier_init();
   }
@@ -600,15 +692,15 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         __syncwarp();
       };
-      auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t boff, int h) {
+      auto issue_acc = [&](int i, uint32_t acc_col, uint32_t a_col, uint32_t boff, int c) {
         // dV += P^T dO (a_col R1, d half of dO) ; dK += dS^T Q (a_col R2, d half of Q)
         if (elect_one()) {
           const uint64_t b = dm0 + qslot(i) + (boff >> 4);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int kk = dkv_half_kk(h, j);
+          for (int j = 0; j < 8 / kDkvChunks; ++j) {
+            const int kk = dkv_chunk_kk(c, j);
             mma2_bf16_ts(tmem + acc_col, tmem + a_col + dkv_a_col(kk),
-                         b + ((kk * 16 * 128) >> 4), idKV, (i > 0 || h > 0 || j > 0) ? 1u : 0u);
+                         b + ((kk * 16 * 128) >> 4), idKV, (i > 0 || c > 0 || j > 0) ? 1u : 0u);
           }
         }
         __syncwarp();
@@ -622,10 +714,10 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       for (int i = 0; i < nsteps; ++i) {
         const uint32_t ph = i & 1;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {                          // dV(i), as P^T halves land
-          mbar_wait_cluster(&p_ready[h], ph);
+        for (int c = 0; c < kDkvChunks; ++c) {                 // dV(i), as P^T chunks land
+          mbar_wait_cluster(&p_ready[c], ph);
           tc_fence_after();
-          issue_acc(i, C::DV_COL, C::R1, C::OFF_GD, h);
+          issue_acc(i, C::DV_COL, C::R1, C::OFF_GD, c);
         }
         if (i + 1 < nsteps) {
           mbar_wait_cluster(&qd_full[(i + 1) % C::STAGES], ((i + 1) / C::STAGES) & 1);
@@ -634,8 +726,8 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         mbar_wait_cluster(ds_ready, ph);
         tc_fence_after();
-        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD, 0);          // dK(i)
-        issue_acc(i, C::DK_COL, C::R2, C::OFF_QD, 1);
+#pragma unroll
+        for (int c = 0; c < kDkvChunks; ++c) issue_acc(i, C::DK_COL, C::R2, C::OFF_QD, c);   // dK(i)
         if (elect_one()) mma2_commit_mc(&qd_empty[i % C::STAGES]);
         __syncwarp();
         if (i + 1 < nsteps) issue_st(i + 1, dv0, C::R2, C::OFF_GQ, dp_full);   // dP^T(i+1)
@@ -664,7 +756,7 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                   [&](int hh) { arrive_pair(&p_ready[hh]); });
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      dkv_phase_b(tl + C::R2 + wg * 64, lds, p.debug, pf, [&]() { arrive_pair(ds_ready); });
+      dkv_phase_b(tl + C::R2 + wg * 64, lds + 512, p.debug, pf, [&]() { arrive_pair(ds_ready); });
     }
     // epilogue (as bwd_dkv_kernel): this CTA's 128 rows, staged in its Q/dO ring
     mbar_wait(dkv_done, 0);
@@ -688,7 +780,7 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (!p.accumulate && p.out_bf16 && p.debug != 4) {
+    if (!p.accumulate && p.out_bf16 && !BWD_DBG(p.debug == 4)) {
       // overwrite in bf16: each 8-lane group packs 64 columns of one row (two
       // staged 32-column chunks) into one full 128-byte line
       __nv_bfloat16* base = static_cast<__nv_bfloat16*>(wg ? p.dk_ptr : p.dv_ptr);
@@ -709,7 +801,7 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                            pack_bf16(b.z, b.w));
         }
       }
-    } else if (!p.accumulate && p.debug != 4) {   // 4: profiling, no drain
+    } else if (!p.accumulate && !BWD_DBG(p.debug == 4)) {   // 4: profiling, no drain
       // overwrite: each 8-lane group stores one full 128-byte row segment
       // (STG.128, whole lines); measured ~5 % faster than TMA tensor stores here
       float* base = static_cast<float*>(wg ? p.dk_ptr : p.dv_ptr);
@@ -726,7 +818,7 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             *reinterpret_cast<float4*>(base + g * hs + (int64_t)grow * rs + c * 32 + q * 4) = val;
         }
       }
-    } else if (p.accumulate && lane == 0 && p.debug != 4) {   // reduce-add in L2
+    } else if (p.accumulate && lane == 0 && !BWD_DBG(p.debug == 4)) {   // reduce-add in L2
       const CUtensorMap* m = wg ? &tmDK : &tmDV;
       const uint64_t pol = l2_evict_first();   // written once, not re-read here
       for (int c = 0; c < D / 32; ++c)
@@ -932,7 +1024,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         uint32_t sv[32];
         tmem_ld32(tl + C::S_COL + wg * 64 + hh * 32, sv);
         tmem_wait_ld();
-        if (p.debug == 1) {
+        if (BWD_DBG(p.debug == 1)) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
           continue;
@@ -970,7 +1062,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         uint32_t gv[32];
         tmem_ld32(tl + C::DP_COL + wg * 64 + hh * 32, gv);
         tmem_wait_ld();
-        if (p.debug == 1) {
+        if (BWD_DBG(p.debug == 1)) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
           continue;
@@ -1309,3 +1401,10 @@ int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
 }
 
 }  // namespace lvx
+
+#ifdef LVX_DKV_TRACE
+extern "C" int lvx_dbg_dkv_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, lvx::g_dkv_trace, sizeof(lvx::g_dkv_trace)) == cudaSuccess ? 0
+                                                                                             : -3;
+}
+#endif

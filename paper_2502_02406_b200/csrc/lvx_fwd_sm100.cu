@@ -66,7 +66,8 @@ struct FwdParams {
   int tiles_per_split;
   int splits;
   float scale_log2;     // scale * log2(e)
-  int variant;          // LVX_FWD_VARIANT (tuning only): 1 = stub exp math, 2 = always two-pass,
+  int variant;          // LVX_FWD_VARIANT, -DLVX_FWD_VARIANTS builds only (tuning): 1 = stub
+                        // exp math, 2 = always two-pass,
                         // 10 = no polynomial exp2
   float* ws_o;          // [splits][hq][rows_q][D]
   float* ws_l;          // [splits][hq][rows_q]
@@ -92,6 +93,11 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LVX_FWD_VARIANTS   // tuning builds only (tools/build_variant.sh)
+  const int kVariant = p.variant;
+#else
+  constexpr int kVariant = 0;
+#endif
   const int pair = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
   const int kv_t0 = split * p.tiles_per_split;
   const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
@@ -246,7 +252,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         // halve the FMA-pipe issue per element.
         bool done = false, fast_failed = false;
         float rs = 0.f;
-        if (j > 0 && p.variant != 1 && p.variant != 2) {
+        if (j > 0 && kVariant != 1 && kVariant != 2) {
           uint32_t pk[4][16];
           float2 rsc[4];
           const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
@@ -289,7 +295,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
           using I = std::integral_constant<int, 0>;
           if (nvalid < kBN)
             pass(std::true_type{}, I{});
-          else if (p.variant == 0)
+          else if (kVariant == 0)
             pass(std::false_type{}, std::integral_constant<int, kPolyPairs>{});
           else
             pass(std::false_type{}, I{});
@@ -348,7 +354,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             uint32_t sv[32], pk[16];
             tmem_ld32(sa + c * 32, sv);
             tmem_wait_ld();
-            if (p.variant == 1) {
+            if (kVariant == 1) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) pk[e] = sv[2 * e];
             } else {
