@@ -46,6 +46,25 @@ constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
 constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
+#ifndef LVX_FWD_LD_ALL
+#define LVX_FWD_LD_ALL 0
+#endif
+
+// LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
+// stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
+#ifdef LVX_FWD_TRACE
+__device__ long long g_fwd_trace[4][128][4];
+#define FWD_STAMP(role, j, ev)                                                              \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && blockIdx.y == LVX_FWD_TRACE && blockIdx.z == 0 && (j) < 128 &&   \
+        lane == 0)                                                                          \
+      g_fwd_trace[role][j][ev] = clock64();                                                 \
+  } while (0)
+#else
+#define FWD_STAMP(role, j, ev) \
+  do {                         \
+  } while (0)
+#endif
 
 template <int D>
 struct FwdCfg {
@@ -216,10 +235,13 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       release(0);                                   // K_0 consumed
       for (int j = 0; j < nt; ++j) {
         wait_load(2 * j + 1);                       // V_j
+        FWD_STAMP(2, j, 0);
         if (j + 1 < nt) wait_load(2 * j + 2);       // K_{j+1}
+        FWD_STAMP(2, j, 1);
         for (int t = 0; t < 2; ++t) {
           if (!active[t]) continue;
           mbar_wait(&p_full[t], j & 1);
+          FWD_STAMP(2, j, 2 + t);
           tc_fence_after();
           issue_pv(t, j);
           if (j + 1 < nt) issue_qk(t, j + 1);
@@ -239,6 +261,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j) {
         mbar_wait(&s_full[t], j & 1);   // QK_t(j) done, hence PV_t(j-1) done
+        if (q4 == 0) FWD_STAMP(t, j, 0);
         tc_fence_after();
         const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
         const uint32_t sa = tl + C::S_COL0 + t * kBN;
@@ -282,6 +305,14 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
               }
               rsc[c] = acc;
             };
+#if LVX_FWD_LD_ALL   // all 128 columns in one TMEM round trip
+            uint32_t sv[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(sa + c * 32, sv[c]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) chunk(sv[c], c);
+#else
 #pragma unroll
             for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip
               uint32_t s0[32], s1[32];
@@ -291,6 +322,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
               chunk(s0, 2 * h);
               chunk(s1, 2 * h + 1);
             }
+#endif
           };
           using I = std::integral_constant<int, 0>;
           if (nvalid < kBN)
@@ -378,6 +410,8 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         l += rs;
         tc_fence_before();
         mbar_arrive(&p_full[t]);
+        if (q4 == 0) FWD_STAMP(t, j, 1);
+        if (q4 == 0) FWD_STAMP(t, j, 2 + (int)done);   // 3: single pass accepted
       }
       // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial
       mbar_wait(&o_done[t], (nt - 1) & 1);
@@ -683,3 +717,10 @@ int tc_fwd_finish(const lvx_view* q, const lvx_view* k, const lvx_view* po, cons
 }
 
 }  // namespace lvx
+
+#ifdef LVX_FWD_TRACE
+extern "C" int lvx_dbg_fwd_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, lvx::g_fwd_trace, sizeof(lvx::g_fwd_trace)) == cudaSuccess ? 0
+                                                                                             : -3;
+}
+#endif

@@ -8,10 +8,10 @@ import subprocess
 import sys
 
 KEYS = [
-    ("duration_us", "gpu__time_duration.sum"),
-    ("sm_clock_ghz", "sm__cycles_elapsed.avg.per_second"),
-    ("dram_read_MB", "dram__bytes_read.sum"),
-    ("dram_write_MB", "dram__bytes_write.sum"),
+    ("duration", "gpu__time_duration.sum"),
+    ("sm_clock", "sm__cycles_elapsed.avg.per_second"),
+    ("dram_read", "dram__bytes_read.sum"),
+    ("dram_write", "dram__bytes_write.sum"),
     ("tensor_utchmma_pct_peak", "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"),
     ("tensor_pipe_active_pct", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
     ("issue_active_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
@@ -36,14 +36,14 @@ def main():
         if len(rows) < 3:
             print(f"## {path}: no data")
             continue
-        hdr = rows[0]
+        hdr, units = rows[0], dict(zip(rows[0], rows[1]))   # row 1: ncu's (auto-scaled) units
         for r in rows[2:]:
             d = dict(zip(hdr, r))
             print(f"## {path}\n\n`{d.get('Kernel Name', '?')[:110]}`\n")
-            print("| metric | value |\n|---|---|")
+            print("| metric | value | unit |\n|---|---|---|")
             for name, key in KEYS:
                 if key in d:
-                    print(f"| {name} (`{key}`) | {d[key]} |")
+                    print(f"| {name} (`{key}`) | {d[key]} | {units.get(key, '')} |")
             stalls = sorted(((float(v), k) for k, v in d.items()
                              if k.startswith("smsp__average_warp_latency_issue_stalled_") or
                              (k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"))
