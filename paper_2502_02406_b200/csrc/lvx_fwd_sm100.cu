@@ -46,9 +46,6 @@ constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
 constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
-#ifndef LVX_FWD_LD_ALL
-#define LVX_FWD_LD_ALL 0
-#endif
 
 // LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
 // stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
@@ -305,14 +302,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
               }
               rsc[c] = acc;
             };
-#if LVX_FWD_LD_ALL   // all 128 columns in one TMEM round trip
-            uint32_t sv[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(sa + c * 32, sv[c]);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 4; ++c) chunk(sv[c], c);
-#else
 #pragma unroll
             for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip
               uint32_t s0[32], s1[32];
@@ -322,7 +311,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
               chunk(s0, 2 * h);
               chunk(s1, 2 * h + 1);
             }
-#endif
           };
           using I = std::integral_constant<int, 0>;
           if (nvalid < kBN)
