@@ -54,6 +54,22 @@ constexpr int kDkvArrivals = LVX_DKV_ARRIVALS;   // per hand-off barrier: 256 th
 #define BWD_DBG(cond) false
 #endif
 
+// LVX_DQ_TRACE=<query tile> (profiling builds only, tools/dq_trace.py): the same
+// for one dQ CTA (split 0, head group 0), [role][kv step][event]
+#ifdef LVX_DQ_TRACE
+__device__ long long g_dq_trace[4][128][8];
+#define DQ_STAMP(role, step, ev)                                                       \
+  do {                                                                                 \
+    if (blockIdx.x == LVX_DQ_TRACE && blockIdx.y == 0 && blockIdx.z == 0 &&            \
+        (step) < 128 && lane == 0)                                                     \
+      g_dq_trace[role][step][ev] = clock64();                                          \
+  } while (0)
+#else
+#define DQ_STAMP(role, step, ev) \
+  do {                           \
+  } while (0)
+#endif
+
 // LVX_DKV_TRACE=<cta x> (profiling builds only, tools/dkv_trace.py): clock64
 // stamps of one dK/dV CTA's hand-offs, [role][step][event]
 #ifdef LVX_DKV_TRACE
@@ -923,6 +939,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const int s = j % C::STAGES, u = j / C::STAGES;
         if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
         else if (s == C::QSLOT) mbar_wait(q_ready, 0);   // Q / dO have left this slot
+        DQ_STAMP(3, j, 0);
         uint8_t* slot = sKV + s * C::SLOT;
         mbar_arrive_expect_tx(&kv_full[s], C::SLOT);
         const int kr = (kv_t0 + j) * 128;
@@ -964,18 +981,21 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const uint32_t ph = j & 1;
       if (j + 1 < nt) {
         wait_kv(j + 1);
+        DQ_STAMP(2, j, 0);
         mbar_wait(s_read, ph);
+        DQ_STAMP(2, j, 1);
         tc_fence_after();
         issue_sdp(j + 1, C::Q_COL, C::S_COL, 0, s_full);            // S(j+1)
       }
       mbar_wait(ds_full, ph);
+      DQ_STAMP(2, j, 2);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t b = dkm0 + kslot(j);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)   // dQ += dS K (A = dS packed over dP)
-          mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + kk * 8, b + ((kk * 16 * 128) >> 4),
-                      idQ, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + dkv_a_col(kk),
+                      b + ((kk * 16 * 128) >> 4), idQ, (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&kv_empty[j % C::STAGES]);
       }
       __syncwarp();
@@ -1015,18 +1035,24 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     for (int j = 0; j < nt; ++j) {
       const uint32_t ph = j & 1;
       const int nvalid = min(128, p.rows_kv - (kv_t0 + j) * 128) - wg * 64;
-      // phase A: P = exp2(S*c + nL), packed in registers; S is then free
+      // phase A: P = exp2(S*c + nL) in registers.  S(j) is released as soon as
+      // it is loaded (P never goes back to TMEM here), so S(j+1) overlaps the
+      // exponentials instead of waiting for them.
       mbar_wait(s_full, ph);
+      if (q4 == 0) DQ_STAMP(wg, j, 0);
       tc_fence_after();
+      uint32_t sv[2][32];
+      tmem_ld32(tl + C::S_COL + wg * 64, sv[0]);
+      tmem_ld32(tl + C::S_COL + wg * 64 + 32, sv[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(s_read);
       float2 pf[32];   // P in fp32 until phase B (only dS feeds an MMA here)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sv[32];
-        tmem_ld32(tl + C::S_COL + wg * 64 + hh * 32, sv);
-        tmem_wait_ld();
         if (BWD_DBG(p.debug == 1)) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pf[hh * 16 + e] = u2f2(sv[2 * e], sv[2 * e + 1]);
+          for (int e = 0; e < 16; ++e) pf[hh * 16 + e] = u2f2(sv[hh][2 * e], sv[hh][2 * e + 1]);
           continue;
         }
         // full and ragged KV steps are separate instantiations (otherwise the
@@ -1035,7 +1061,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const int c = hh * 32 + e;
-            float2 x = ffma2(u2f2(sv[e], sv[e + 1]), sc2, nl2);
+            float2 x = ffma2(u2f2(sv[hh][e], sv[hh][e + 1]), sc2, nl2);
             if constexpr (decltype(masked)::value) {
               x.x = c < nvalid ? x.x : -INFINITY;
               x.y = c + 1 < nvalid ? x.y : -INFINITY;
@@ -1051,38 +1077,35 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         else
           pa(std::false_type{});
       }
-      tc_fence_before();
-      mbar_arrive(s_read);
-      // phase B: dS = P (dP + nD), packed over dP
+      if (q4 == 0) DQ_STAMP(wg, j, 1);
+      // phase B: dS = P (dP + nD), packed into the first half of this
+      // warpgroup's own dP columns (the two warpgroups never share columns)
       mbar_wait(dp_full, ph);
+      if (q4 == 0) DQ_STAMP(wg, j, 2);
       tc_fence_after();
-      uint32_t dd[32];
+      uint32_t gv[2][32], dd[32];
+      tmem_ld32(tl + C::DP_COL + wg * 64, gv[0]);
+      tmem_ld32(tl + C::DP_COL + wg * 64 + 32, gv[1]);
+      tmem_wait_ld();
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t gv[32];
-        tmem_ld32(tl + C::DP_COL + wg * 64 + hh * 32, gv);
-        tmem_wait_ld();
         if (BWD_DBG(p.debug == 1)) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[2 * e];
+          for (int e = 0; e < 16; ++e) dd[hh * 16 + e] = gv[hh][2 * e];
           continue;
         }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const int pi = (hh * 32 + e) / 2;
-          const float2 r2 = fmul2(pf[pi], fadd2(u2f2(gv[e], gv[e + 1]), nd2));
+          const float2 r2 = fmul2(pf[pi], fadd2(u2f2(gv[hh][e], gv[hh][e + 1]), nd2));
           dd[pi] = pack_bf16(r2.x, r2.y);
         }
       }
-      // both wgs read dP before either packs over the shared lanes (a one-sided
-      // arrive / sync hand-off measured ~3 % slower here)
-      tc_fence_before();
-      named_sync<1>();
-      tc_fence_after();
-      tmem_st32(tl + C::DP_COL + wg * 32, dd);
+      tmem_st32(tl + C::DP_COL + wg * 64, dd);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(ds_full);
+      if (q4 == 0) DQ_STAMP(wg, j, 3);
     }
     // epilogue: warpgroup w drains dQ columns [w*D/2, (w+1)*D/2) of its rows
     mbar_wait(dq_done, 0);
@@ -1406,5 +1429,11 @@ int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
 extern "C" int lvx_dbg_dkv_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, lvx::g_dkv_trace, sizeof(lvx::g_dkv_trace)) == cudaSuccess ? 0
                                                                                              : -3;
+}
+#endif
+
+#ifdef LVX_DQ_TRACE
+extern "C" int lvx_dbg_dq_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, lvx::g_dq_trace, sizeof(lvx::g_dq_trace)) == cudaSuccess ? 0 : -3;
 }
 #endif
