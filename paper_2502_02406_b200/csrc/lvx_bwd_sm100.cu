@@ -1266,13 +1266,8 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
     return LVX_ECUDA;
   if (accumulate && (!make_tma_f32_3d(&mdk, dk, 32) || !make_tma_f32_3d(&mdv, dvv, 32)))
     return LVX_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DkvCfg<D>::SMEM) != cudaSuccess)
-      return LVX_ECUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(bwd_dkv_kernel<D>, DkvCfg<D>::SMEM, attr_done)) return LVX_ECUDA;
   p.accumulate = accumulate;
   p.dk_ptr = dk->data;
   p.dv_ptr = dvv->data;
@@ -1297,13 +1292,8 @@ int launch_dkv2(const lvx_view* q, const lvx_view* k, const lvx_view* v, const l
     return LVX_ECUDA;
   if (accumulate && (!make_tma_f32_3d(&mdk, dk, 32) || !make_tma_f32_3d(&mdv, dvv, 32)))
     return LVX_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(bwd_dkv2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Dkv2Cfg<128>::SMEM) != cudaSuccess)
-      return LVX_ECUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(bwd_dkv2_kernel<128>, Dkv2Cfg<128>::SMEM, attr_done)) return LVX_ECUDA;
   p.accumulate = accumulate;
   p.dk_ptr = dk->data;
   p.dv_ptr = dvv->data;
@@ -1326,13 +1316,8 @@ int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx
   if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
       !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mv128, v, 128))
     return LVX_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DqCfg<D>::SMEM) != cudaSuccess)
-      return LVX_ECUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(bwd_dq_kernel<D>, DqCfg<D>::SMEM, attr_done)) return LVX_ECUDA;
   bwd_dq_kernel<D><<<dim3(pl.pairs, pl.splits, (unsigned)k->heads), 320, DqCfg<D>::SMEM, st>>>(
       mq128, mk128, mv128, mg128, p);
   note_launch();

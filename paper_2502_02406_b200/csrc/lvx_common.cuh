@@ -125,4 +125,20 @@ int tc_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq, i
 int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
                const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dk,
                const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// Raise a kernel's dynamic shared memory limit once per device: function
+// attributes belong to the device's context, so a process driving several
+// GPUs needs the call on each (bit d of `done` = device d).
+template <typename F>
+inline bool ensure_smem_attr(F* fn, int bytes, std::atomic<unsigned>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const unsigned bit = dev < 32 ? 1u << dev : 0u;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return false;
+  done.fetch_or(bit, std::memory_order_release);
+  return true;
+}
+
 }  // namespace lvx

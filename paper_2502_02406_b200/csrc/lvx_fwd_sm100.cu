@@ -636,13 +636,8 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
   p.ws_o = static_cast<float*>(ws);
   p.ws_l = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.splits * n * D * 4));
   constexpr int smem = FwdCfg<D>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return LVX_ECUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(fwd_kernel<D>, smem, attr_done)) return LVX_ECUDA;
   dim3 grid(pl.pairs, pl.splits, (unsigned)k->heads);
   fwd_kernel<D><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
   note_launch();

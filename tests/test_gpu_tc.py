@@ -290,3 +290,22 @@ def test_dkv_cta_pair_kernel_bit_identical(shape, dt, acc, monkeypatch):
         outs[flag] = (dk, dv)
     assert torch.equal(outs["0"][0], outs["1"][0]), (outs["0"][0] - outs["1"][0]).abs().max()
     assert torch.equal(outs["0"][1], outs["1"][1]), (outs["0"][1] - outs["1"][1]).abs().max()
+
+
+def test_tc_two_devices_one_process():
+    # kernel attributes (227 KB dynamic SMEM) are per device context: one
+    # process driving two GPUs must launch on both (skipped on 1-GPU boxes)
+    import paper_2502_02406_b200 as lvx
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    (q, k, v, g), (Q, K, V, G) = bf16_inputs(4, 1, 256, 1024, 128, seed=5)
+    O, L = orc.blockwise_attention(Q, K, V)
+    for dev in (0, 1, 0):
+        with torch.cuda.device(dev):
+            qd, kd, vd, gd = (t.to(f"cuda:{dev}") for t in (q, k, v, g))
+            st = lvx.blockwise_attention(qd, kd, vd)
+            D = lvx.attention_row_stats(st, gd)
+            grads = lvx.blockwise_attention_backward(qd, kd, vd, st.L, D, gd)
+            torch.cuda.synchronize(dev)
+            assert orc.max_norm_error(st.O.cpu().numpy(), O) <= TOL_BF16
+            assert all(torch.isfinite(t).all() for t in grads)
