@@ -46,11 +46,14 @@ constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
 constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
+#ifndef LVX_FWD_HALVES   // P published in two halves (PV starts on the first)
+#define LVX_FWD_HALVES 1
+#endif
 
 // LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
 // stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
 #ifdef LVX_FWD_TRACE
-__device__ long long g_fwd_trace[4][128][4];
+__device__ long long g_fwd_trace[4][128][6];
 #define FWD_STAMP(role, j, ev)                                                              \
   do {                                                                                      \
     if (blockIdx.x == 0 && blockIdx.y == LVX_FWD_TRACE && blockIdx.z == 0 && (j) < 128 &&   \
@@ -69,7 +72,7 @@ struct FwdCfg {
   static constexpr int Q_BYTES = kBM * D * 2;
   static constexpr int KV_BYTES = kBN * D * 2;
   static constexpr int STAGES = D == 128 ? 5 : 10;
-  static constexpr int NBAR = 1 + 2 * STAGES + 6;
+  static constexpr int NBAR = 1 + 2 * STAGES + 10;
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + STAGES * KV_BYTES + NBAR * 8 + 16;
   static constexpr int S_COL0 = 0;
   static constexpr int O_COL0 = 256;
@@ -104,8 +107,9 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::STAGES;
   uint64_t* s_full = kv_empty + C::STAGES;   // [2]
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_done = p_full + 2;             // [2]
+  uint64_t* p_full = s_full + 2;             // [2 t + h]: half h of P_t (128 each)
+  uint64_t* o_done = p_full + 4;             // [2]
+  uint64_t* pv0_done = o_done + 2;           // [2]: PV_t(j) over the first half
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -135,8 +139,10 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
+      mbar_init(&p_full[2 * t], 128);
+      mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&o_done[t], 1);
+      mbar_init(&pv0_done[t], 1);
     }
     fence_barrier_init();
   }
@@ -209,14 +215,14 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         }
         __syncwarp();
       };
-      auto issue_pv = [&](int t, int j) {
+      auto issue_pv = [&](int t, int j, int kk0, int kk1, uint64_t* bar) {
         if (elect_one()) {
           const uint64_t b = dv0 + ((slot_of(2 * j + 1) * C::KV_BYTES) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
+          for (int kk = kk0; kk < kk1; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
             mma_bf16_ts(tmem + C::O_COL0 + t * D, tmem + C::S_COL0 + t * kBN + kk * 8,
                         b + ((kk * 16 * 128) >> 4), idPV, (j > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&o_done[t]);
+          mma_commit(bar);
         }
         __syncwarp();
       };
@@ -237,10 +243,20 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         FWD_STAMP(2, j, 1);
         for (int t = 0; t < 2; ++t) {
           if (!active[t]) continue;
-          mbar_wait(&p_full[t], j & 1);
+#if LVX_FWD_HALVES
+          mbar_wait(&p_full[2 * t], j & 1);   // PV over kv rows [0, 64) as soon as they land
+          tc_fence_after();
+          issue_pv(t, j, 0, kBN / 32, &pv0_done[t]);
+          mbar_wait(&p_full[2 * t + 1], j & 1);
           FWD_STAMP(2, j, 2 + t);
           tc_fence_after();
-          issue_pv(t, j);
+          issue_pv(t, j, kBN / 32, kBN / 16, &o_done[t]);
+#else
+          mbar_wait(&p_full[2 * t], j & 1);
+          FWD_STAMP(2, j, 2 + t);
+          tc_fence_after();
+          issue_pv(t, j, 0, kBN / 16, &o_done[t]);
+#endif
           if (j + 1 < nt) issue_qk(t, j + 1);
         }
         release(2 * j + 1);                         // V_j consumed
@@ -270,6 +286,129 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         // below when a row's scores grew (rare after the first tiles; that
         // path then moves m_used to the exact row max).  Packed FFMA2/FADD2
         // halve the FMA-pipe issue per element.
+#if LVX_FWD_HALVES
+        // Single pass in two halves of 64 columns (j > 0): a half is final when
+        // no row's partial sum exceeds the bound (every P element of it is then
+        // <= the bound), so it is packed over its own, already read, scores and
+        // published at once — PV_t(j) runs on kv rows [0, 64) while [64, 128)
+        // is exponentiated.  If the first half fails, S is intact and the tile
+        // takes the exact two-pass path.  If only the second fails, the first
+        // half is already in PV: wait for it (pv0_done), rescale O and l to the
+        // new row max and redo the second half from its intact scores.
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        int fail_half = j > 0 ? 2 : 0;   // 2: both halves single-pass
+        if (j > 0) {
+          const float2 nm2 = make_float2(-m_used, -m_used);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t pk[2][16];
+            float2 acc = make_float2(0.f, 0.f);
+            auto half = [&](auto masked, auto poly) {
+              uint32_t s0[32], s1[32];
+              tmem_ld32(sa + h * 64, s0);
+              tmem_ld32(sa + h * 64 + 32, s1);
+              tmem_wait_ld();
+              auto chunk = [&](const uint32_t (&sv)[32], int c) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                  float2 x = ffma2(u2f2(sv[e], sv[e + 1]), sc2, nm2);
+                  if constexpr (decltype(masked)::value) {
+                    const int col = c * 32 + e;
+                    x.x = col < nvalid ? x.x : -INFINITY;
+                    x.y = col + 1 < nvalid ? x.y : -INFINITY;
+                  }
+                  const float2 pp = ((((c * 16 + e / 2) * 3) % 8) < decltype(poly)::value)
+                                        ? ex2_poly2(x)
+                                        : make_float2(ex2(x.x), ex2(x.y));
+                  acc = fadd2(acc, pp);
+                  pk[c & 1][e / 2] = pack_bf16(pp.x, pp.y);
+                }
+              };
+              chunk(s0, 2 * h);
+              chunk(s1, 2 * h + 1);
+            };
+            using I = std::integral_constant<int, 0>;
+            if (nvalid < kBN) half(std::true_type{}, I{});
+            else half(std::false_type{}, std::integral_constant<int, kPolyPairs>{});
+            const float rs = acc.x + acc.y;
+            if (__any_sync(0xffffffffu, !(rs <= kFastBound))) {   // also inf / NaN
+              fail_half = h;
+              break;
+            }
+            tmem_st16(sa + (2 * h) * 16, pk[0]);
+            tmem_st16(sa + (2 * h + 1) * 16, pk[1]);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * t + h]);
+            l += rs;
+          }
+        }
+        if (fail_half < 2) {
+          // exact path over halves h0 .. 1 (h0 = 1: the first half is in PV)
+          const int h0 = fail_half;
+          float mx = -INFINITY;
+          for (int c = 2 * h0; c < 4; ++c) {
+            uint32_t sv[32];
+            tmem_ld32(sa + c * 32, sv);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
+          }
+          mx *= p.scale_log2;
+          // a failed single pass moves to the exact max; the first tile too
+          const bool need = mx > m_used + (j > 0 ? 0.f : kRescaleThreshold);
+          const float alpha = need ? ex2(m_used - mx) : 1.f;
+          if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
+            if (h0 == 1) {   // O must include PV_t(j) over the first half
+              mbar_wait(&pv0_done[t], j & 1);
+              tc_fence_after();
+            }
+#pragma unroll 1
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t ov[32];
+              const uint32_t oa = tl + C::O_COL0 + t * D + c * 32;
+              tmem_ld32(oa, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st32(oa, ov);
+            }
+          }
+          if (need) {
+            l *= alpha;
+            m_used = mx;
+          }
+          for (int h = h0; h < 2; ++h) {
+            float rs = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              const int c = 2 * h + cc;
+              uint32_t sv[32], pk[16];
+              tmem_ld32(sa + c * 32, sv);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const int col = c * 32 + e;
+                float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used));
+                float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used));
+                p0 = col < nvalid ? p0 : 0.f;
+                p1 = col + 1 < nvalid ? p1 : 0.f;
+                rs += p0 + p1;
+                pk[e / 2] = pack_bf16(p0, p1);
+              }
+              tmem_st16(sa + c * 16, pk);   // packed columns [16c, 16c + 16): scores read
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * t + h]);
+            l += rs;
+          }
+        }
+        if (q4 == 0) FWD_STAMP(t, j, 1);
+        if (q4 == 0) FWD_STAMP(t, j, 2 + (int)(fail_half == 2));   // 3: single pass accepted
+        if (q4 == 0 && fail_half == 1) FWD_STAMP(t, j, 4);         // 4: second-half fallback
+#else
         bool done = false, fast_failed = false;
         float rs = 0.f;
         if (j > 0 && kVariant != 1 && kVariant != 2) {
@@ -397,9 +536,10 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         tmem_wait_st();
         l += rs;
         tc_fence_before();
-        mbar_arrive(&p_full[t]);
+        mbar_arrive(&p_full[2 * t]);
         if (q4 == 0) FWD_STAMP(t, j, 1);
         if (q4 == 0) FWD_STAMP(t, j, 2 + (int)done);   // 3: single pass accepted
+#endif
       }
       // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial
       mbar_wait(&o_done[t], (nt - 1) & 1);

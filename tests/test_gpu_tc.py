@@ -292,6 +292,28 @@ def test_dkv_cta_pair_kernel_bit_identical(shape, dt, acc, monkeypatch):
     assert torch.equal(outs["0"][1], outs["1"][1]), (outs["0"][1] - outs["1"][1]).abs().max()
 
 
+@pytest.mark.parametrize("q_scale", [4.0, 8.0])
+def test_tc_forward_second_half_fallback(q_scale):
+    # scores jump only in kv rows [64, 128) of every 128-row tile, x3 per tile:
+    # the forward publishes P in halves, so the first half of a tile is
+    # accepted and already in the PV MMA when the second half fails its bound
+    # — the path that waits for that PV, rescales O / l and redoes the half
+    # (every KV split sees the jump between its consecutive tiles)
+    import paper_2502_02406_b200 as lvx
+    (q, k, v, _), _ = bf16_inputs(2, 1, 200, 1536, 128, seed=33, q_scale=q_scale)
+    rows = torch.arange(1536, device="cuda")
+    scale = torch.where((rows % 128) >= 64, 3.0 ** (rows // 128).float(),
+                        torch.ones_like(rows, dtype=torch.float32))
+    k = (k.float() * scale[None, :, None]).to(torch.bfloat16)
+    Q, K, V = (t.double().cpu().numpy() for t in (q, k, v))
+    st = lvx.blockwise_attention(q, k, v)
+    O, L = orc.blockwise_attention(Q, K, V)
+    eo = orc.max_norm_error(st.O.cpu().numpy(), O)
+    el = orc.max_norm_error(st.L.cpu().numpy(), L)
+    print(f"\nTC fwd second-half fallback q x{q_scale}: O err {eo:.2e}  L err {el:.2e}")
+    assert eo <= TOL_BF16 and el <= TOL_BF16
+
+
 def test_tc_two_devices_one_process():
     # kernel attributes (227 KB dynamic SMEM) are per device context: one
     # process driving two GPUs must launch on both (skipped on 1-GPU boxes)

@@ -39,7 +39,7 @@ def main():
         K.fwd_partial(q, k, v, d ** -0.5, ws)
     torch.cuda.synchronize()
     lib = ctypes.CDLL(os.environ["LVX_B200_LIB"])
-    buf = np.zeros((4, 128, 4), dtype=np.int64)
+    buf = np.zeros((4, 128, 6), dtype=np.int64)
     assert lib.lvx_dbg_fwd_trace(buf.ctypes.data_as(ctypes.c_void_p)) == 0
     s0, s1, mma = buf[0], buf[1], buf[2]
     nt = int((s0[:, 0] != 0).sum())
