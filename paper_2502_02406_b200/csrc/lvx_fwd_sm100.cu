@@ -14,13 +14,16 @@
 //              128B-swizzled ring (10 slots at d=64)
 //   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
 // TMEM (512 columns): S_t = Q_t K_j^T at cols [128t, 128t+128), O_t at
-// [256 + t*D, 256 + (t+1)*D).  The softmax warps read S_t in two passes (row
-// max, then exp2) and write P_t = exp2(S_t*scale*log2e - m) as bf16 pairs
-// back OVER S_t; PV_t is a TS MMA reading P_t from TMEM.  tcgen05.mma runs in
-// issue order, so the stream PV_t(j) -> QK_t(j+1) needs no extra barrier and
-// the commit after QK_t(j) also proves PV_t(j-1) done.  The running max is
+// [256 + t*D, 256 + (t+1)*D).  The softmax warps write P_t =
+// exp2(S_t*scale*log2e - m) as bf16 pairs back OVER S_t, in two published
+// halves (single pass against the running reference max m, a per-half
+// row-sum vote; the exact two-pass path when a vote fails), and PV_t is a TS
+// MMA reading P_t from TMEM, issued per half.  tcgen05.mma runs in issue
+// order, so the stream PV_t(j) -> QK_t(j+1) needs no extra barrier and the
+// commit after QK_t(j) also proves PV_t(j-1) done.  The running max is
 // updated lazily: O in TMEM is rescaled only when the row max grows by more
-// than 2^8, which is exact (P, l and O always share one reference max).
+// than 2^8 (or a vote failed), which is exact (P, l and O always share one
+// reference max).
 // Each split writes a normalised partial (O, L) in fp32 to the workspace;
 // fwd_combine_kernel merges the splits (and the prior ring state) in a fixed
 // order.
@@ -46,9 +49,6 @@ constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
 constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
-#ifndef LVX_FWD_HALVES   // P published in two halves (PV starts on the first)
-#define LVX_FWD_HALVES 1
-#endif
 
 // LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
 // stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
@@ -85,9 +85,6 @@ struct FwdParams {
   int tiles_per_split;
   int splits;
   float scale_log2;     // scale * log2(e)
-  int variant;          // LVX_FWD_VARIANT, -DLVX_FWD_VARIANTS builds only (tuning): 1 = stub
-                        // exp math, 2 = always two-pass,
-                        // 10 = no polynomial exp2
   float* ws_o;          // [splits][hq][rows_q][D]
   float* ws_l;          // [splits][hq][rows_q]
 };
@@ -113,11 +110,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef LVX_FWD_VARIANTS   // tuning builds only (tools/build_variant.sh)
-  const int kVariant = p.variant;
-#else
-  constexpr int kVariant = 0;
-#endif
   const int pair = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
   const int kv_t0 = split * p.tiles_per_split;
   const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
@@ -243,7 +235,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         FWD_STAMP(2, j, 1);
         for (int t = 0; t < 2; ++t) {
           if (!active[t]) continue;
-#if LVX_FWD_HALVES
           mbar_wait(&p_full[2 * t], j & 1);   // PV over kv rows [0, 64) as soon as they land
           tc_fence_after();
           issue_pv(t, j, 0, kBN / 32, &pv0_done[t]);
@@ -251,12 +242,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
           FWD_STAMP(2, j, 2 + t);
           tc_fence_after();
           issue_pv(t, j, kBN / 32, kBN / 16, &o_done[t]);
-#else
-          mbar_wait(&p_full[2 * t], j & 1);
-          FWD_STAMP(2, j, 2 + t);
-          tc_fence_after();
-          issue_pv(t, j, 0, kBN / 16, &o_done[t]);
-#endif
           if (j + 1 < nt) issue_qk(t, j + 1);
         }
         release(2 * j + 1);                         // V_j consumed
@@ -286,7 +271,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         // below when a row's scores grew (rare after the first tiles; that
         // path then moves m_used to the exact row max).  Packed FFMA2/FADD2
         // halve the FMA-pipe issue per element.
-#if LVX_FWD_HALVES
         // Single pass in two halves of 64 columns (j > 0): a half is final when
         // no row's partial sum exceeds the bound (every P element of it is then
         // <= the bound), so it is packed over its own, already read, scores and
@@ -408,138 +392,6 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         if (q4 == 0) FWD_STAMP(t, j, 1);
         if (q4 == 0) FWD_STAMP(t, j, 2 + (int)(fail_half == 2));   // 3: single pass accepted
         if (q4 == 0 && fail_half == 1) FWD_STAMP(t, j, 4);         // 4: second-half fallback
-#else
-        bool done = false, fast_failed = false;
-        float rs = 0.f;
-        if (j > 0 && kVariant != 1 && kVariant != 2) {
-          uint32_t pk[4][16];
-          float2 rsc[4];
-          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-          const float2 nm2 = make_float2(-m_used, -m_used);
-          // full and ragged tiles are separate instantiations: otherwise the
-          // column mask is if-converted into two selects per element everywhere
-          auto pass = [&](auto masked, auto poly) {
-            auto chunk = [&](const uint32_t (&sv)[32], int c) {
-              float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                float2 x = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])),
-                                 sc2, nm2);
-                if constexpr (decltype(masked)::value) {
-                  const int col = c * 32 + e;
-                  x.x = col < nvalid ? x.x : -INFINITY;
-                  x.y = col + 1 < nvalid ? x.y : -INFINITY;
-                }
-                // decltype(poly)::value of every 8 pairs take exp2 on the FMA
-                // pipe: MUFU.EX2 alone would set the pace (2 x 128 per
-                // sub-partition per KV tile ~ the tile's MMA time)
-                const float2 pp = ((((c * 16 + e / 2) * 3) % 8) < decltype(poly)::value)
-                                      ? ex2_poly2(x)
-                                      : make_float2(ex2(x.x), ex2(x.y));
-                acc = fadd2(acc, pp);
-                pk[c][e / 2] = pack_bf16(pp.x, pp.y);
-              }
-              rsc[c] = acc;
-            };
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {   // two chunks per TMEM round trip
-              uint32_t s0[32], s1[32];
-              tmem_ld32(sa + h * 64, s0);
-              tmem_ld32(sa + h * 64 + 32, s1);
-              tmem_wait_ld();
-              chunk(s0, 2 * h);
-              chunk(s1, 2 * h + 1);
-            }
-          };
-          using I = std::integral_constant<int, 0>;
-          if (nvalid < kBN)
-            pass(std::true_type{}, I{});
-          else if (kVariant == 0)
-            pass(std::false_type{}, std::integral_constant<int, kPolyPairs>{});
-          else
-            pass(std::false_type{}, I{});
-          const float2 r2 = fadd2(fadd2(rsc[0], rsc[1]), fadd2(rsc[2], rsc[3]));
-          rs = r2.x + r2.y;
-          // !(rs <= bound) also catches inf / NaN sums
-          if (!__any_sync(0xffffffffu, !(rs <= kFastBound))) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_st16(sa + c * 16, pk[c]);
-            done = true;
-          } else {
-            rs = 0.f;
-            fast_failed = true;
-          }
-        }
-        if (!done) {
-          // pass 1 over TMEM: row max (log2 domain)
-          float mx = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t sv[32];
-            tmem_ld32(sa + c * 32, sv);
-            tmem_wait_ld();
-            if (nvalid == kBN) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
-            } else {
-#pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (c * 32 + e < nvalid) mx = fmaxf(mx, __uint_as_float(sv[e]));
-            }
-          }
-          mx *= p.scale_log2;
-          const bool need = mx > m_used + (fast_failed ? 0.f : kRescaleThreshold);
-          const float alpha = need ? ex2(m_used - mx) : 1.f;
-          if (__any_sync(0xffffffffu, need && j > 0)) {   // lazy rescale of O_t in TMEM
-#pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-              uint32_t ov[32];
-              const uint32_t oa = tl + C::O_COL0 + t * D + c * 32;
-              tmem_ld32(oa, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-              tmem_st32(oa, ov);
-            }
-          }
-          if (need) {
-            l *= alpha;
-            m_used = mx;
-          }
-          // pass 2: P = exp2(S*c - m) -> bf16 pairs written over S_t (chunk c of
-          // S is read before packed columns [16c, 16c+16) are overwritten)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t sv[32], pk[16];
-            tmem_ld32(sa + c * 32, sv);
-            tmem_wait_ld();
-            if (kVariant == 1) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) pk[e] = sv[2 * e];
-            } else {
-#pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const int col = c * 32 + e;
-                float p0 = ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -m_used));
-                float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), p.scale_log2, -m_used));
-                if (nvalid < kBN) {
-                  p0 = col < nvalid ? p0 : 0.f;
-                  p1 = col + 1 < nvalid ? p1 : 0.f;
-                }
-                rs += p0 + p1;
-                pk[e / 2] = pack_bf16(p0, p1);
-              }
-            }
-            tmem_st16(sa + c * 16, pk);
-          }
-        }
-        tmem_wait_st();
-        l += rs;
-        tc_fence_before();
-        mbar_arrive(&p_full[2 * t]);
-        if (q4 == 0) FWD_STAMP(t, j, 1);
-        if (q4 == 0) FWD_STAMP(t, j, 2 + (int)done);   // 3: single pass accepted
-#endif
       }
       // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial
       mbar_wait(&o_done[t], (nt - 1) & 1);
@@ -770,8 +622,6 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
   p.tiles_per_split = pl.tiles_per_split;
   p.splits = pl.splits;
   p.scale_log2 = (float)(scale * 1.4426950408889634);
-  const char* var = getenv("LVX_FWD_VARIANT");
-  p.variant = var ? atoi(var) : 0;
   const size_t n = (size_t)q->heads * q->rows;
   p.ws_o = static_cast<float*>(ws);
   p.ws_l = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.splits * n * D * 4));
