@@ -1,7 +1,10 @@
-# Forward-kernel A/B in one box (same clocks): 0 = default, 1 = stub exp
-# math (tensor-pipe ceiling), 2 = always two-pass softmax, 10 = no
-# polynomial exp2.  Sweep of polynomial pairs per 8 (c2gath, one box):
-# 0: 1365, 1: 1422, 2: 1440, 3: 1450, 4: 1391, 5: 1320 TFLOP/s.
-for i in 1 2; do for v in ${VARIANTS:-0 1 2 10}; do
-LVX_FWD_VARIANT=$v python tools/bench_kernels.py --shape c2gath --iters 5 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('variant $v fwd', round(d['fwd_tflops']))"
-done; done
+# Forward-kernel A/B in one box (same clocks).  Build the two libraries here
+# (nvcc cross-compiles), then run this on the GPU box:
+#   bash tools/build_variant.sh fwd_a "" HEAD      # a git revision
+#   bash tools/build_variant.sh fwd_b ""           # the working tree (or "-D..." flags)
+#   gpurun -- bash tools/ab_fwd.sh
+# Historical sweep of polynomial exp2 pairs per 8 (c2gath, one box, round 1):
+# 0: 1365, 1: 1422, 2: 1440, 3: 1450, 4: 1391, 5: 1320 TFLOP/s -> kPolyPairs = 3.
+for shape in ${SHAPES:-c2gath c2round}; do
+  LIBS="${LIBS:-build/ab/fwd_a.so build/ab/fwd_b.so}" SHAPE=$shape bash tools/ab_libs.sh
+done
