@@ -312,17 +312,19 @@ def native_arm(args):
     kflops, kdur = kernels[kname]
     burst, sust, hbm, pk_kind, sust_mhz = peaks()
     achieved = kflops / kdur / 1e12
-    # The sustained peak is cuBLAS under the power cap (MEASURED_PEAKS
-    # clocks_under_load).  A kernel whose SM clock in the timed region sits well
-    # above that clock was not power-capped (smaller per-GPU work at N > 1):
-    # its denominator is the burst peak.
+    # The sustained peak is cuBLAS under the power cap at the SM clock in
+    # MEASURED_PEAKS clocks_under_load; tensor throughput scales with the SM
+    # clock, so the denominator is that peak at the clock sampled in THIS timed
+    # region, never above the burst peak (an uncapped N > 1 run at ~1.7 GHz is
+    # measured against burst).
     run_mhz = (clocks or {}).get("sm_mhz")
-    capped = not (run_mhz and sust_mhz and run_mhz > 1.15 * sust_mhz)
-    peak = sust if capped else burst
-    peak_kind = (f"{pk_kind} bf16 sustained (kernel timed inside a long, power-capped step: "
-                 f"SM {run_mhz} MHz vs {sust_mhz} MHz for the sustained GEMM)" if capped else
-                 f"{pk_kind} bf16 burst (SM {run_mhz} MHz in the timed region, well above the "
-                 f"{sust_mhz} MHz of the power-capped sustained GEMM)")
+    if run_mhz and sust_mhz:
+        peak = min(burst, sust * run_mhz / sust_mhz)
+        peak_kind = (f"{pk_kind} bf16 sustained {sust} TFLOP/s at {sust_mhz} MHz, scaled to the "
+                     f"{run_mhz} MHz SM clock of this timed region (capped at burst {burst})")
+    else:
+        peak = sust
+        peak_kind = f"{pk_kind} bf16 sustained (kernel timed inside a long step)"
     traffic, traffic_src = None, None
     tj = ROOT / "profiles" / "r01b_traffic.json"
     if world == 1 and args.strategy == "lvx" and args.skv == CFG["s_kv"] and tj.exists():
