@@ -36,8 +36,18 @@ using namespace sm100;
 
 constexpr int kStep = 64;      // q rows per step (dkv kernel) / kv rows per step (dq kernel)
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kPolyPairs = 3;   // of every 8 column pairs, exp2 by polynomial (FMA pipe)
-constexpr int kPolyPairsDkv = 2; // the same for the dK/dV kernel's phase A
+// Polynomial exp2 shares, tuned in the power-capped bench step
+// (tools/ab_bench.sh): dQ 1/8 (3/8 was best isolated at ~1.8 GHz; at the
+// bench's ~1.4 GHz cap 1/8 measured +0.2-0.7 %), dK/dV 2/8 (1/8: -0.4 %, 0/8:
+// -1.7 %); the forward keeps 3/8 (2/8 even, 1/8 -0.4 %)
+#ifndef LVX_DQ_POLY
+#define LVX_DQ_POLY 1
+#endif
+#ifndef LVX_DKV_POLY
+#define LVX_DKV_POLY 2
+#endif
+constexpr int kPolyPairs = LVX_DQ_POLY;     // of every 8 column pairs, exp2 by polynomial (FMA pipe)
+constexpr int kPolyPairsDkv = LVX_DKV_POLY; // the same for the dK/dV kernel's phase A
 #ifndef LVX_DKV_CHUNKS
 #define LVX_DKV_CHUNKS 2
 #endif

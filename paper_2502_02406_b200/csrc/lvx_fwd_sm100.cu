@@ -48,7 +48,10 @@ constexpr int kBN = 128;   // kv rows per tile
 constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
-constexpr int kPolyPairs = 3;              // of every 8 column pairs, exp2 by polynomial
+#ifndef LVX_FWD_POLY
+#define LVX_FWD_POLY 3
+#endif
+constexpr int kPolyPairs = LVX_FWD_POLY;   // of every 8 column pairs, exp2 by polynomial
 
 // LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
 // stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
