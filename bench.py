@@ -314,14 +314,17 @@ def native_arm(args):
     achieved = kflops / kdur / 1e12
     # The sustained peak is cuBLAS under the power cap at the SM clock in
     # MEASURED_PEAKS clocks_under_load; tensor throughput scales with the SM
-    # clock, so the denominator is that peak at the clock sampled in THIS timed
-    # region, never above the burst peak (an uncapped N > 1 run at ~1.7 GHz is
-    # measured against burst).
+    # clock, so a timed region that ran faster (less work per GPU at N > 1) is
+    # measured against that peak scaled up to its clock, never above burst.
+    # Never scaled DOWN: the clock is a median over the whole step, not the
+    # dominant kernel's own clock, and the measured sustained figure is what a
+    # capped B200 delivers.
     run_mhz = (clocks or {}).get("sm_mhz")
     if run_mhz and sust_mhz:
-        peak = min(burst, sust * run_mhz / sust_mhz)
-        peak_kind = (f"{pk_kind} bf16 sustained {sust} TFLOP/s at {sust_mhz} MHz, scaled to the "
-                     f"{run_mhz} MHz SM clock of this timed region (capped at burst {burst})")
+        peak = min(burst, max(sust, sust * run_mhz / sust_mhz))
+        peak_kind = (f"{pk_kind} bf16 sustained {sust} TFLOP/s at {sust_mhz} MHz, scaled up to "
+                     f"the {run_mhz} MHz SM clock of this timed region when higher (capped at "
+                     f"burst {burst})")
     else:
         peak = sust
         peak_kind = f"{pk_kind} bf16 sustained (kernel timed inside a long step)"
