@@ -230,17 +230,6 @@ __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
 }
 
-// Named barriers over the two softmax warpgroups (256 threads): producers of
-// a hand-off arrive without waiting, consumers sync.
-template <int ID>
-__device__ __forceinline__ void named_arrive() {
-  asm volatile("bar.arrive %0, 256;" ::"n"(ID) : "memory");
-}
-template <int ID>
-__device__ __forceinline__ void named_sync() {
-  asm volatile("bar.sync %0, 256;" ::"n"(ID) : "memory");
-}
-
 // ---- CTA pairs (cta_group::2): the leader (cluster rank 0) issues the MMAs of
 // the pair; operands split as cute's SM100_MMA_F16BF16_2x1SM_{SS,TS}: A by M
 // (each CTA its 128 rows / TMEM lanes), B by N (each CTA N/2).  Verified by
