@@ -7,7 +7,9 @@
 //
 // One CTA = one kv head g, two 128-row query tiles of that head's GQA group
 // (so each K/V tile fetched into shared memory feeds 256 query rows), and one
-// split of the resident KV block.  Warp roles (320 threads):
+// split of the resident KV block.  With a single query tile per kv head (MHA,
+// <= 128 rows; KVP instantiation) the two tiles are the same Q against the
+// even / odd KV tiles of the split, each writing its own split partial.  Warp roles (320 threads):
 //   warps 0-3  softmax for query tile 0 (TMEM lanes 0-127, one row per thread)
 //   warps 4-7  softmax for query tile 1
 //   warp  8    TMA producer: Q tiles once, then K_j / V_j into a 5-slot
@@ -86,13 +88,15 @@ struct FwdParams {
   int tpq;              // 128-row tiles per query head
   int n_tiles;          // 128-row kv tiles in the block
   int tiles_per_split;
-  int splits;
+  int splits;           // workspace partials (2 per CTA split in kv_pair mode)
+  int kv_pair;          // one query tile per kv head: the CTA's two tiles take the
+                        // even / odd KV tiles of its split with the same Q
   float scale_log2;     // scale * log2(e)
   float* ws_o;          // [splits][hq][rows_q][D]
   float* ws_l;          // [splits][hq][rows_q]
 };
 
-template <int D>
+template <int D, bool KVP>
 __global__ void __launch_bounds__(kThreads, 1)
 fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
@@ -125,6 +129,18 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     qh[t] = g * p.G + tt / p.tpq;
     row0[t] = (tt % p.tpq) * kBM;
   }
+  // kv_pair: tile t runs over KV tiles kv_t0 + 2 j + t (nt is even), one Q
+  constexpr bool kvp = KVP;   // == p.kv_pair (a separate instantiation: no cost to the normal path)
+  if (kvp) {
+    active[1] = active[0];
+    qh[1] = qh[0];
+    row0[1] = row0[0];
+  }
+  const int ns = kvp ? nt / 2 : nt;   // KV steps per query tile
+  // load index L of the K / V tile QK_t(j) / PV_t(j) reads: (K_j, V_j)
+  // pairs, or (K_2j, K_2j+1, V_2j, V_2j+1) quads in kv_pair mode
+  auto k_load = [&](int t, int j) { return kvp ? 4 * j + t : 2 * j; };
+  auto v_load = [&](int t, int j) { return kvp ? 4 * j + 2 + t : 2 * j + 1; };
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -156,9 +172,9 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      const uint32_t qbytes = (active[0] + active[1]) * C::Q_BYTES;
+      const uint32_t qbytes = (kvp ? active[0] : active[0] + active[1]) * C::Q_BYTES;
       mbar_arrive_expect_tx(q_full, qbytes);
-      for (int t = 0; t < 2; ++t)
+      for (int t = 0; t < (kvp ? 1 : 2); ++t)
         if (active[t])
           for (int pn = 0; pn < C::PANELS; ++pn)
             tma_load_3d(sQ + t * C::Q_BYTES + pn * kBM * 128, &tmQ, q_full, pn * 64, row0[t],
@@ -166,12 +182,13 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       for (int L = 0; L < 2 * nt; ++L) {
         const int s = L % C::STAGES, u = L / C::STAGES;
         if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
-        const int j = L >> 1;
-        const CUtensorMap* m = (L & 1) ? &tmV : &tmK;
+        const bool is_v = kvp ? (L & 3) >= 2 : (L & 1);
+        const int kvt = kvp ? 2 * (L >> 2) + (L & 1) : L >> 1;
+        const CUtensorMap* m = is_v ? &tmV : &tmK;
         mbar_arrive_expect_tx(&kv_full[s], C::KV_BYTES);
         for (int pn = 0; pn < C::PANELS; ++pn)
           tma_load_3d(sKV + s * C::KV_BYTES + pn * kBN * 128, m, &kv_full[s], pn * 64,
-                      (kv_t0 + j) * kBN, g);
+                      (kv_t0 + kvt) * kBN, g);
       }
     }
   } else if (warp == 9) {
@@ -198,8 +215,8 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       };
       auto issue_qk = [&](int t, int j) {
         if (elect_one()) {
-          const uint64_t a = dq0 + ((t * C::Q_BYTES) >> 4);
-          const uint64_t b = dkv0 + ((slot_of(2 * j) * C::KV_BYTES) >> 4);
+          const uint64_t a = dq0 + (((kvp ? 0 : t) * C::Q_BYTES) >> 4);
+          const uint64_t b = dkv0 + ((slot_of(k_load(t, j)) * C::KV_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t ao = ((kk >> 2) * (kBM * 128) + (kk & 3) * 32) >> 4;
@@ -212,7 +229,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       };
       auto issue_pv = [&](int t, int j, int kk0, int kk1, uint64_t* bar) {
         if (elect_one()) {
-          const uint64_t b = dv0 + ((slot_of(2 * j + 1) * C::KV_BYTES) >> 4);
+          const uint64_t b = dv0 + ((slot_of(v_load(t, j)) * C::KV_BYTES) >> 4);
 #pragma unroll
           for (int kk = kk0; kk < kk1; ++kk)   // A = P_t in TMEM (bf16, 8 cols per K=16)
             mma_bf16_ts(tmem + C::O_COL0 + t * D, tmem + C::S_COL0 + t * kBN + kk * 8,
@@ -227,14 +244,16 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
       };
       mbar_wait(q_full, 0);
       tc_fence_after();
-      wait_load(0);
+      const int nk = kvp ? 2 : 1;   // K (and V) loads per step and tile pair
+      for (int t = 0; t < nk; ++t) wait_load(k_load(t, 0));
       for (int t = 0; t < 2; ++t)
         if (active[t]) issue_qk(t, 0);
-      release(0);                                   // K_0 consumed
-      for (int j = 0; j < nt; ++j) {
-        wait_load(2 * j + 1);                       // V_j
+      for (int t = 0; t < nk; ++t) release(k_load(t, 0));   // K_0 consumed
+      for (int j = 0; j < ns; ++j) {
+        for (int t = 0; t < nk; ++t) wait_load(v_load(t, j));     // V_j
         FWD_STAMP(2, j, 0);
-        if (j + 1 < nt) wait_load(2 * j + 2);       // K_{j+1}
+        if (j + 1 < ns)
+          for (int t = 0; t < nk; ++t) wait_load(k_load(t, j + 1));   // K_{j+1}
         FWD_STAMP(2, j, 1);
         for (int t = 0; t < 2; ++t) {
           if (!active[t]) continue;
@@ -245,10 +264,11 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
           FWD_STAMP(2, j, 2 + t);
           tc_fence_after();
           issue_pv(t, j, kBN / 32, kBN / 16, &o_done[t]);
-          if (j + 1 < nt) issue_qk(t, j + 1);
+          if (j + 1 < ns) issue_qk(t, j + 1);
         }
-        release(2 * j + 1);                         // V_j consumed
-        if (j + 1 < nt) release(2 * j + 2);         // K_{j+1} consumed
+        for (int t = 0; t < nk; ++t) release(v_load(t, j));       // V_j consumed
+        if (j + 1 < ns)
+          for (int t = 0; t < nk; ++t) release(k_load(t, j + 1));   // K_{j+1} consumed
       }
     }
   } else if (warp >= 10) {
@@ -260,11 +280,11 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
     if (active[t]) {
       const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < nt; ++j) {
+      for (int j = 0; j < ns; ++j) {
         mbar_wait(&s_full[t], j & 1);   // QK_t(j) done, hence PV_t(j-1) done
         if (q4 == 0) FWD_STAMP(t, j, 0);
         tc_fence_after();
-        const int nvalid = min(kBN, p.rows_kv - (kv_t0 + j) * kBN);
+        const int nvalid = min(kBN, p.rows_kv - (kv_t0 + (kvp ? 2 * j + t : j)) * kBN);
         const uint32_t sa = tl + C::S_COL0 + t * kBN;
         // Single pass (j > 0): exponentiate against the current reference max
         // m_used without looking for the row max first.  The row sum bounds
@@ -397,12 +417,13 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         if (q4 == 0 && fail_half == 1) FWD_STAMP(t, j, 4);         // 4: second-half fallback
       }
       // epilogue: O / l and L = (m + log2 l) ln 2 into this split's partial
-      mbar_wait(&o_done[t], (nt - 1) & 1);
+      mbar_wait(&o_done[t], (ns - 1) & 1);
       tc_fence_after();
       const int row = row0[t] + r;
       const bool valid = row < p.rows_q;
       const float inv = 1.f / l;
-      const size_t slot = ((size_t)split * p.hq + qh[t]) * p.rows_q + row;
+      const int ws_split = kvp ? 2 * split + t : split;   // this tile's partial
+      const size_t slot = ((size_t)ws_split * p.hq + qh[t]) * p.rows_q + row;
       float* dst = p.ws_o + slot * D;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
@@ -573,7 +594,10 @@ bool tma_view_ok(const lvx_view* v) {
 namespace {
 
 struct FwdPlan {
-  int tpq, pairs, n_tiles, tiles_per_split, splits;
+  int tpq, pairs, n_tiles, tiles_per_split;
+  int grid_splits;   // CTA splits of the KV block
+  int splits;        // workspace partials: grid_splits, x2 in kv_pair mode
+  bool kv_pair;
 };
 
 FwdPlan plan_fwd(const lvx_view* q, const lvx_view* k) {
@@ -582,14 +606,18 @@ FwdPlan plan_fwd(const lvx_view* q, const lvx_view* k) {
   pl.tpq = (int)ceil_div(q->rows, kBM);
   pl.pairs = (int)ceil_div((int64_t)G * pl.tpq, 2);
   pl.n_tiles = (int)ceil_div(k->rows, kBN);
+  // one query tile per kv head (MHA rounds with <= 128 query rows): pair the
+  // KV tiles of each split instead, so both softmax warpgroups ping-pong
+  pl.kv_pair = G * pl.tpq == 1 && pl.n_tiles >= 2 && pl.n_tiles % 2 == 0;
   const int64_t units0 = (int64_t)pl.pairs * k->heads;
   const int sms = device_sms();
   // maximise modelled throughput: wave efficiency / (1 + partial-state traffic)
-  int best = 1;
+  int best_tps = pl.n_tiles;
   double best_score = -1.0;
   const int max_s = (int)std::max<int64_t>(1, std::min<int64_t>(64, pl.n_tiles / 2));
   for (int s = 1; s <= max_s; ++s) {
-    const int tps = (int)ceil_div(pl.n_tiles, s);
+    int tps = (int)ceil_div(pl.n_tiles, s);
+    if (pl.kv_pair) tps += tps & 1;   // even tile counts in every split
     const int real_s = (int)ceil_div(pl.n_tiles, tps);
     const int64_t units = units0 * real_s;
     const int64_t waves = ceil_div(units, sms);
@@ -597,11 +625,12 @@ FwdPlan plan_fwd(const lvx_view* q, const lvx_view* k) {
     const double score = eff / (1.0 + 2.4 * real_s / pl.n_tiles);
     if (score > best_score + 1e-9) {
       best_score = score;
-      best = s;
+      best_tps = tps;
     }
   }
-  pl.tiles_per_split = (int)ceil_div(pl.n_tiles, best);
-  pl.splits = (int)ceil_div(pl.n_tiles, pl.tiles_per_split);
+  pl.tiles_per_split = best_tps;
+  pl.grid_splits = (int)ceil_div(pl.n_tiles, pl.tiles_per_split);
+  pl.splits = pl.grid_splits * (pl.kv_pair ? 2 : 1);
   return pl;
 }
 
@@ -624,15 +653,22 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
   p.n_tiles = pl.n_tiles;
   p.tiles_per_split = pl.tiles_per_split;
   p.splits = pl.splits;
+  p.kv_pair = pl.kv_pair ? 1 : 0;
   p.scale_log2 = (float)(scale * 1.4426950408889634);
   const size_t n = (size_t)q->heads * q->rows;
   p.ws_o = static_cast<float*>(ws);
   p.ws_l = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(pl.splits * n * D * 4));
+  dim3 grid(pl.pairs, pl.grid_splits, (unsigned)k->heads);
   constexpr int smem = FwdCfg<D>::SMEM;
-  static std::atomic<unsigned> attr_done{0};
-  if (!ensure_smem_attr(fwd_kernel<D>, smem, attr_done)) return LVX_ECUDA;
-  dim3 grid(pl.pairs, pl.splits, (unsigned)k->heads);
-  fwd_kernel<D><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  if (pl.kv_pair) {
+    static std::atomic<unsigned> attr_done{0};
+    if (!ensure_smem_attr(fwd_kernel<D, true>, smem, attr_done)) return LVX_ECUDA;
+    fwd_kernel<D, true><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  } else {
+    static std::atomic<unsigned> attr_done{0};
+    if (!ensure_smem_attr(fwd_kernel<D, false>, smem, attr_done)) return LVX_ECUDA;
+    fwd_kernel<D, false><<<grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  }
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }

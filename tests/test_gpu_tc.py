@@ -33,7 +33,10 @@ def bf16_inputs(hq, hkv, sq, skv, d, seed, q_scale=1.0):
 
 SHAPES = [  # hq, hkv, sq, skv, d
     (1, 1, 128, 128, 128), (2, 2, 200, 1000, 128), (8, 2, 77, 515, 64), (4, 1, 256, 4096, 128),
-    (8, 8, 128, 4096, 64), (3, 3, 5, 7, 128), (32, 8, 64, 640, 128), (2, 1, 300, 129, 64)]
+    (8, 8, 128, 4096, 64), (3, 3, 5, 7, 128), (32, 8, 64, 640, 128), (2, 1, 300, 129, 64),
+    # one query tile per kv head -> KV-pair mode (even KV tile counts): ragged
+    # last tile, one step per tile; and an odd count that stays in normal mode
+    (4, 4, 100, 2000, 128), (2, 2, 128, 256, 64), (2, 2, 64, 384, 128)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
