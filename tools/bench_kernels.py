@@ -21,6 +21,7 @@ SHAPES = {  # hq, hkv, rows_q, rows_kv, d
     "c3round": (28, 4, 690, 65536, 128),      # Owl3 256K, n=4 (ragged rows)
     "c2gath": (32, 8, 2048, 131072, 128),     # Llama-3-V n=8: batched dK/dV over all blocks
     "c2gath_q2": (32, 8, 4096, 65536, 128),   # same work, 2x query steps per dK/dV CTA
+    "c4gath": (8, 8, 1024, 65536, 64),        # OpenFlamingo n=8: the batched dK/dV launch
 }
 
 
