@@ -6,7 +6,8 @@
  * `lvxattn` (reference: /root/reference/pkg/src/lvxattn/kernels.py).  The
  * ring-exchange scheduler that calls them (lvx_forward / lvx_backward /
  * ring_forward / ring_backward / run_distributed) lives in the Python host
- * layer `paper_2502_02406_b200.strategies`, one process per GPU over NCCL.
+ * layer `paper_2502_02406_b200.strategies`, one process per GPU; the ring
+ * hops run on the copy engines through the lvx_peer_* transport below.
  *
  * Conventions:
  *   - Tensors are strided [heads, rows, d] views with the last dim
@@ -22,10 +23,8 @@
  *     F32/BF16 inputs and F64 for F64 inputs.
  *   - Every call is asynchronous on the caller's cudaStream_t, never
  *     synchronises the host, allocates nothing (scratch comes from the
- *     caller's workspace) and keeps no global mutable state -- except two
- *     documented process-wide items: the planner's SM reserve
- *     (lvx_set_sm_reserve) and the cached per-device cuBLAS handle of the
- *     three projection calls (which also use cuBLAS's own workspace).
+ *     caller's workspace; the transport's arena from lvx_peer_create) and
+ *     keeps no global mutable state beyond the launch counter.
  *   - Return value: LVX_OK (0) or a negative lvx_status.  The Python shim
  *     maps LVX_EINVAL/LVX_EDTYPE to ValueError with the reference messages
  *     (kernels.py:62-73) and LVX_ECUDA to RuntimeError.
@@ -159,11 +158,10 @@ int lvx_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v,
 /* ---- utilities ---------------------------------------------------------
  * empty_state (kernels.py:48-53): O = 0, L = -inf. */
 int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream);
-/* Process-wide planner setting: the split / grid planners size their waves
- * for (SM count - sms) SMs, leaving room for NCCL's send/recv CTAs that run
- * beside the ring-round kernels (one process per GPU).  Returns the previous
- * value; 0 (the default) plans for the whole device. */
-int lvx_set_sm_reserve(int sms);
+/* dst += src for F32/F64 state tensors of one shape (the Ring baseline adds
+ * a round's dK/dV contribution to the partial that arrived over the ring,
+ * strategies.py:330-350). */
+int lvx_accumulate(const lvx_view* src, const lvx_view* dst, void* stream);
 /* dst = src converted (F32/F64/BF16 <-> F32/F64/BF16), strided views. */
 int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
 
@@ -193,6 +191,42 @@ int lvx_project_bwd(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* do
  * (head_stride == d) it is ONE GEMM y @ [W_K | W_V]. */
 int lvx_kv_recompute(const lvx_matrix* y, const lvx_matrix* w_k, const lvx_matrix* w_v,
                      const lvx_view* k_out, const lvx_view* v_out, void* stream);
+
+/* ---- ring transport (copy engines over NVLink, no SMs) -----------------
+ * Replaces the reference's in-process mailboxes: Cluster.send / recv
+ * (cluster.py:173-220) and WorkerContext.send / recv / ring_shift
+ * (cluster.py:227-272).  Each rank owns an "arena" (device memory allocated
+ * and zeroed by _create) laid out identically on every rank; a message is
+ * copied by the sender's copy engine into the same offset of the receiver's
+ * arena, followed by a 32-bit flag write the receiver's stream waits on.
+ * All calls are asynchronous on the given stream and never block the host.
+ *   _create / _destroy   per-rank arena of `bytes` + peer map (rank in
+ *                        [0, n), n <= LVX_MAX_PEERS); _base is its address
+ *   _export / _open      CUDA IPC mapping of a peer process's arena
+ *                        (handle of lvx_peer_handle_bytes() bytes)
+ *   _attach              a peer arena in the same process (thread ranks)
+ *   _put                 2-D copy (height rows of width bytes) from local
+ *                        memory into peer's arena at dst_off
+ *   _signal              peer's u32 at flag_off <- value, after prior work
+ *                        on the stream (fenced)
+ *   _wait                stream waits until (int32)(own u32 at flag_off -
+ *                        value) >= 0
+ */
+#define LVX_MAX_PEERS 16
+typedef struct lvx_peer_map lvx_peer_map;
+int lvx_peer_create(uint64_t bytes, int rank, int n, lvx_peer_map** out);
+int lvx_peer_destroy(lvx_peer_map* m);
+void* lvx_peer_base(const lvx_peer_map* m);
+uint64_t lvx_peer_handle_bytes(void);
+int lvx_peer_export(const lvx_peer_map* m, void* handle);
+int lvx_peer_open(lvx_peer_map* m, int peer, const void* handle);
+int lvx_peer_attach(lvx_peer_map* m, int peer, const lvx_peer_map* other);
+int lvx_peer_put(const lvx_peer_map* m, int peer, uint64_t dst_off, uint64_t dst_pitch,
+                 const void* src, uint64_t src_pitch, uint64_t width, uint64_t height,
+                 void* stream);
+int lvx_peer_signal(const lvx_peer_map* m, int peer, uint64_t flag_off, uint32_t value,
+                    void* stream);
+int lvx_peer_wait(const lvx_peer_map* m, uint64_t flag_off, uint32_t value, void* stream);
 
 #ifdef __cplusplus
 }

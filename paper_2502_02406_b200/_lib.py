@@ -24,7 +24,9 @@ EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eli
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
            "lvx_fill_empty_state", "lvx_convert", "lvx_bwd_workspace", "lvx_bwd_dq_partial",
            "lvx_bwd_dq_finish", "lvx_bwd_dkv", "lvx_project", "lvx_project_bwd",
-           "lvx_kv_recompute", "lvx_set_sm_reserve")
+           "lvx_kv_recompute", "lvx_accumulate", "lvx_peer_create", "lvx_peer_destroy",
+           "lvx_peer_base", "lvx_peer_handle_bytes", "lvx_peer_export", "lvx_peer_open",
+           "lvx_peer_attach", "lvx_peer_put", "lvx_peer_signal", "lvx_peer_wait")
 
 
 class LvxView(ctypes.Structure):
@@ -63,6 +65,7 @@ def load() -> ctypes.CDLL:
     P = ctypes.POINTER(LvxView)
     M = ctypes.POINTER(LvxMatrix)
     vp, sz, dbl, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double, ctypes.c_int
+    u64 = ctypes.c_uint64
     proto = {
         "lvx_abi_version": (i32, []),
         "lvx_kernel_launches": (ctypes.c_ulonglong, []),
@@ -85,7 +88,17 @@ def load() -> ctypes.CDLL:
         "lvx_project": (i32, [M, M, P, vp]),
         "lvx_project_bwd": (i32, [M, M, P, M, M, vp]),
         "lvx_kv_recompute": (i32, [M, M, M, P, P, vp]),
-        "lvx_set_sm_reserve": (i32, [i32]),
+        "lvx_accumulate": (i32, [P, P, vp]),
+        "lvx_peer_create": (i32, [u64, i32, i32, ctypes.POINTER(vp)]),
+        "lvx_peer_destroy": (i32, [vp]),
+        "lvx_peer_base": (vp, [vp]),
+        "lvx_peer_handle_bytes": (u64, []),
+        "lvx_peer_export": (i32, [vp, vp]),
+        "lvx_peer_open": (i32, [vp, i32, vp]),
+        "lvx_peer_attach": (i32, [vp, i32, vp]),
+        "lvx_peer_put": (i32, [vp, i32, u64, u64, vp, u64, u64, u64, vp]),
+        "lvx_peer_signal": (i32, [vp, i32, u64, ctypes.c_uint32, vp]),
+        "lvx_peer_wait": (i32, [vp, u64, ctypes.c_uint32, vp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

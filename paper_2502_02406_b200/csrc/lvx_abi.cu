@@ -276,9 +276,11 @@ int lvx_fill_empty_state(const lvx_view* o, const lvx_view* l, void* stream) {
   return fill_empty(o, l, static_cast<cudaStream_t>(stream));
 }
 
-int lvx_set_sm_reserve(int sms) {
-  if (sms < 0) return LVX_EINVAL;
-  return g_sm_reserve.exchange(sms);
+int lvx_accumulate(const lvx_view* src, const lvx_view* dst, void* stream) {
+  if (!valid_view(src) || !valid_view(dst) || !same_hr(src, dst) || src->d != dst->d)
+    return LVX_EINVAL;
+  if (src->dtype != dst->dtype || src->dtype == LVX_BF16) return LVX_EDTYPE;
+  return accumulate_into(src, dst, 1, static_cast<cudaStream_t>(stream));
 }
 
 int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream) {

@@ -567,6 +567,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
   }
 }
 
+#ifdef LVX_DKV2_PROBE   // CTA-pair variant: measured 19 % slower, not in the product build
 // ================================================================ dK / dV on CTA pairs
 // The same algorithm as bwd_dkv_kernel on cta_group::2 (M = 256 KV rows per
 // pair, 128 per CTA): the leader issues S^T = K Q^T, dP^T = V dO^T (SS) and
@@ -861,6 +862,8 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tmem_dealloc2(tmem, 512);
   }
 }
+
+#endif  // LVX_DKV2_PROBE
 
 // ================================================================ dQ kernel
 // Q-parallel, one 128-row query tile per CTA, split over the KV block in
@@ -1245,8 +1248,10 @@ void fill_params(BwdParams& p, const BwdPlan& pl, const lvx_view* q, const lvx_v
   p.splits = pl.splits;
   p.scale = (float)scale;
   p.scale_log2 = (float)(scale * 1.4426950408889634);
+#ifdef LVX_BWD_DEBUG_MODES
   const char* dbg = getenv("LVX_BWD_DEBUG");
   p.debug = dbg ? atoi(dbg) : 0;
+#endif
   char* w = static_cast<char*>(ws);
   const size_t lp_bytes = align256((size_t)p.hq * p.rows_pad * 4);
   p.Lp = reinterpret_cast<float*>(w);
@@ -1292,6 +1297,7 @@ int launch_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
+#ifdef LVX_DKV2_PROBE
 int launch_dkv2(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
                 BwdParams p, const lvx_view* dk, const lvx_view* dvv, int accumulate,
                 cudaStream_t st) {
@@ -1319,6 +1325,8 @@ int launch_dkv2(const lvx_view* q, const lvx_view* k, const lvx_view* v, const l
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
+#endif  // LVX_DKV2_PROBE
+
 template <int D>
 int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
               const BwdParams& p, const BwdPlan& pl, cudaStream_t st) {
@@ -1337,7 +1345,6 @@ int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx
 }  // namespace
 
 bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
-  if (getenv("LVX_DISABLE_TC")) return false;
   if (q->dtype != LVX_BF16 || (q->d != 64 && q->d != 128)) return false;
   if (!tma_view_ok(q) || !tma_view_ok(k) || !tma_view_ok(v)) return false;
   if (k->heads == 0 || q->heads % k->heads) return false;
@@ -1406,14 +1413,16 @@ int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lv
   fill_params(p, pl, q, k, scale, ws);
   int s = launch_prep(p, L, D, st);
   if (s) return s;
-  // CTA-pair kernel (d = 128), opt-in: bit-identical to the 1-CTA kernel and
-  // equal with the softmax stubbed (1423 vs 1457 TFLOP/s at c2gath), but 19 %
-  // slower with real math (1008-1013 vs 1242-1251 at c2full): the pair's two
-  // tensor cores wait for the slower CTA's softmax at both hand-offs of every
-  // step, and those hand-offs, not SMEM bandwidth, are the critical path.
+#ifdef LVX_DKV2_PROBE
+  // CTA-pair kernel (d = 128), probe builds only: bit-identical to the 1-CTA
+  // kernel and equal with the softmax stubbed (1423 vs 1457 TFLOP/s at
+  // c2gath), but 19 % slower with real math (1008-1013 vs 1242-1251 at
+  // c2full): the pair's two tensor cores wait for the slower CTA's softmax at
+  // both hand-offs of every step.
   const char* two = getenv("LVX_DKV_2CTA");
   if (q->d == 128 && two && atoi(two) == 1)
     return launch_dkv2(q, k, v, dO, p, dk, dv, accumulate, st);
+#endif
   return q->d == 128 ? launch_dkv<128>(q, k, v, dO, p, dk, dv, accumulate, st)
                      : launch_dkv<64>(q, k, v, dO, p, dk, dv, accumulate, st);
 }

@@ -97,7 +97,6 @@ int simt_bwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_
              const lvx_view* dk, const lvx_view* dv, int accumulate, cudaStream_t st);
 // zero an F32/F64 view
 int fill_empty_zero(const lvx_view* a, cudaStream_t st);
-extern std::atomic<int> g_sm_reserve;   // lvx_set_sm_reserve (planner SM budget)
 // dst (+)= src, state dtypes, same shapes
 int accumulate_into(const lvx_view* src, const lvx_view* dst, int accumulate, cudaStream_t st);
 int merge(const lvx_view* oa, const lvx_view* la, const lvx_view* ob, const lvx_view* lb,

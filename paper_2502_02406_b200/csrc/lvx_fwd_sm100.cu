@@ -553,21 +553,18 @@ bool make_tma_f32_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
   return r == CUDA_SUCCESS;
 }
 
-// SMs the grid planners leave free (lvx_set_sm_reserve): NCCL's send/recv
-// CTAs share the GPU with the ring-round kernels, and a plan that fills every
-// SM in whole waves then spills a straggler wave.
-std::atomic<int> g_sm_reserve{0};
-
+// SM count of the current device.  The grid plans depend only on this and the
+// shapes, so a workspace query, _partial and _finish always agree (the ring
+// hops run on copy engines and take no SM, so the plans use all of them).
 int device_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
   }
-  const int r = g_sm_reserve.load(std::memory_order_relaxed);
-  return r > 0 && r < sms ? sms - r : sms;
+  return sms;
 }
 
 bool is_sm100() {
@@ -676,7 +673,6 @@ int launch_fwd(const lvx_view* q, const lvx_view* k, const lvx_view* v, double s
 }  // namespace
 
 bool tc_fwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
-  if (getenv("LVX_DISABLE_TC")) return false;
   if (q->dtype != LVX_BF16 || (q->d != 64 && q->d != 128)) return false;
   if (!tma_view_ok(q) || !tma_view_ok(k) || !tma_view_ok(v)) return false;
   if (k->heads == 0 || q->heads % k->heads) return false;

@@ -22,12 +22,6 @@ class CudaOps:
         return K.state_dtype(dt)
 
     @staticmethod
-    def set_sm_reserve(sms: int) -> int:
-        """SMs the kernel planners leave to NCCL (lvx_set_sm_reserve)."""
-        from . import _lib
-        return int(_lib.load().lvx_set_sm_reserve(int(sms)))
-
-    @staticmethod
     def grad_dtype(dt: torch.dtype) -> torch.dtype:
         """Gradients come back in the input dtype (the reference's convention);
         dK/dV are written in it directly by the tensor-core epilogue."""
@@ -74,7 +68,12 @@ class CudaOps:
             K.bwd_dkv(q, k, v, L, D, d_o, scale, dk, dv, accumulate,
                       ws=self.bwd_workspace(q, k, slot=2))
 
-    # -- device timing (CUDA events on the compute stream) -----------------
+    def accumulate(self, src, dst) -> None:
+        """dst += src (state dtype; the Ring baseline's dK/dV partials)."""
+        if dst.numel():
+            K._lib.check("lvx_accumulate", K._lib.load().lvx_accumulate(
+                K._lib.view(src), K._lib.view(dst), K._lib.stream_ptr(dst.device)))
+
     def kv_recompute(self, y, w_k, w_v, k_out, v_out) -> None:
         """k_out / v_out ([hkv, S, d] views) = project(y, W_K / W_V) (lvx_kv_recompute)."""
         if y.shape[0]:
@@ -87,6 +86,7 @@ class CudaOps:
         """dx = dOut_flat W^T, dw = x^T dOut_flat for a [heads, S, d] view (lvx_project_bwd)."""
         K.project_backward_into(x, W, d_out, dx, dw)
 
+    # -- device timing (CUDA events on the compute stream) -----------------
     @staticmethod
     def event():
         e = torch.cuda.Event(enable_timing=True)

@@ -178,28 +178,30 @@ def _expect(got, want, what: str) -> None:
         raise ClusterError(f"{what}: expected block {want}, got {got}")
 
 
-class _Flat:
-    """Double-buffered contiguous storage for rotating blocks of varying rows."""
-
-    def __init__(self, heads: int, max_rows: int, d: int | None, dtype, device, count: int = 2):
-        # d=None: a row statistic [heads, rows] (L, D)
-        self.h, self.d = heads, d
-        self.bufs = [torch.empty(max(heads * max_rows * (d or 1), 1), dtype=dtype, device=device)
-                     for _ in range(count)]
-
-    def view(self, idx: int, rows: int) -> torch.Tensor:
-        t = self.bufs[idx][:self.h * rows * (self.d or 1)]
-        return t.view(self.h, rows) if self.d is None else t.view(self.h, rows, self.d)
+def _shaped(flat: torch.Tensor, h: int, rows: int, d: int | None = None) -> torch.Tensor:
+    """[h, rows, d] (or [h, rows] for d=None) view of the prefix of a flat
+    buffer: a block of any row count has the same layout on every rank, so a
+    record sent as a whole lands exactly where the receiver reads it."""
+    t = flat[:h * rows * (d or 1)]
+    return t.view(h, rows) if d is None else t.view(h, rows, d)
 
 
-def _dev_copy(t: torch.Tensor, buf: torch.Tensor) -> torch.Tensor:
-    buf.copy_(t)
-    return buf
+def _slot_value(ctx: DeviceContext, m: int) -> int:
+    """Flag value released for message m of a slot channel in this call."""
+    return (ctx.epoch * 4096 + m + 1) & 0xFFFFFFFF
 
 
-# ---------------------------------------------------------------------------
-# LV-XAttn query rotation
-# ---------------------------------------------------------------------------
+def _after(ctx: DeviceContext, chan: int, m: int, slots: int):
+    """Message m of channel ``chan`` reuses slot m % slots: wait until the
+    receiver released message m - slots (earlier calls: the epoch fence)."""
+    if m < slots:
+        return None
+    return (chan * 16 + m % slots, _slot_value(ctx, m - slots))
+
+
+def _release(ctx: DeviceContext, chan: int, m: int, slots: int) -> None:
+    ctx.release(chan * 16 + m % slots, _slot_value(ctx, m))
+
 
 @dataclass
 class KVStream:
@@ -216,6 +218,45 @@ class KVStream:
     dkv_done: object = None
 
 
+def _attend_merge(ops, q, k_block, v_block, scale, o, l, hop, kv_stream, first, prior):
+    """One round's attention of q against the resident KV block merged into
+    (o, l): the main loop runs before the hop is waited on, the split combine
+    + merge after it.  ``prior``: (o, l) hold a state to merge with (the
+    received one) — else they are overwritten.  Round 0 of a streamed block
+    consumes K/V chunk by chunk.  Returns the events (t1, t2) around the wait."""
+    t1 = t2 = None
+    if first and kv_stream is not None and len(kv_stream.bounds) > 1:
+        for c, (a, b) in enumerate(kv_stream.bounds):
+            if kv_stream.wait_chunk is not None:
+                kv_stream.wait_chunk(c)
+            kc, vc = k_block[:, a:b], v_block[:, a:b]
+            ws = ops.fwd_workspace(q, kc)
+            ops.fwd_partial(q, kc, vc, scale, ws)
+            if c == 0:
+                t1 = ops.event()
+                if hop is not None:
+                    hop.wait()
+                t2 = ops.event()
+            merge = prior or c > 0
+            ops.fwd_finish(q, kc, ws, o, l, o if merge else None, l if merge else None)
+        return t1, t2
+    if kv_stream is not None and kv_stream.wait_chunk is not None:
+        for c in range(len(kv_stream.bounds)):
+            kv_stream.wait_chunk(c)
+    ws = ops.fwd_workspace(q, k_block)
+    ops.fwd_partial(q, k_block, v_block, scale, ws)
+    t1 = ops.event()
+    if hop is not None:
+        hop.wait()
+    t2 = ops.event()
+    ops.fwd_finish(q, k_block, ws, o, l, o if prior else None, l if prior else None)
+    return t1, t2
+
+
+# ---------------------------------------------------------------------------
+# LV-XAttn query rotation
+# ---------------------------------------------------------------------------
+
 def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                 scale: float, tile_rows: int = DEFAULT_TILE_ROWS,
                 trace: RoundTrace | None = None,
@@ -225,76 +266,72 @@ def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block
     (block i-r+1; round 0 ships the empty state) plus Q of block i-r to the
     successor, run block i-r's attention against the resident K/V, receive
     the predecessor's state and Q, merge.  After n rounds an epilogue hop
-    sends each completed state home."""
+    sends each completed state home.
+
+    Buffers: round r's message lands in record r of the call's arena
+    ([O | L | Q], one record per round, so no slot is ever reused inside the
+    call); from round 1 on the record received last round is forwarded whole
+    — one copy-engine transfer per hop."""
     n, i, ops = ctx.n, ctx.rank, ctx.ops
     h, _, d = q_block.shape
     dev = q_block.device
     sd = ops.state_dtype(q_block.dtype)
     qs = shards.q_sizes
     mq = max(qs) if qs else 0
-    O = _Flat(h, mq, d, sd, dev)
-    Lb = _Flat(h, mq, None, sd, dev)
-    Qb = _Flat(h, mq, d, q_block.dtype, dev)
+    with ctx.call() as call:
+        if n == 1:   # loopback (cluster.py:178-180): the empty state merges to nothing
+            out_o = torch.empty((h, qs[0], d), dtype=sd, device=dev)
+            out_l = torch.empty((h, qs[0]), dtype=sd, device=dev)
+            t0 = ops.event() if trace is not None else None
+            t1, t2 = _attend_merge(ops, q_block, k_block, v_block, scale, out_o, out_l, None,
+                                   kv_stream, True, False)
+            if trace is not None:
+                t3 = ops.event()
+                trace._add_timed(ops, t0, t1, t2, {"O": 0, "L": 0, "Q": 0})
+                trace.section("fwd_kernel", ops, t0, t1)
+                trace.section("fwd_finish", ops, t2, t3)
+                trace.section("wait", ops, t1, t2)
+                trace.epilogue_bytes_by_class = {"O": 0, "L": 0}
+            return AttentionState(O=out_o, L=out_l)
+        buf = call.alloc({"rec": (n, [("O", h * mq * d, sd), ("L", h * mq, sd),
+                                      ("Q", h * mq * d, q_block.dtype)]),
+                          "home": (1, [("O", h * mq * d, sd), ("L", h * mq, sd)])})
+        R, home = buf["rec"], buf["home"][0]
+        send_block, q_block_id = (i + 1) % n, i
+        o_s = torch.empty((h, qs[send_block], d), dtype=sd, device=dev)
+        l_s = torch.empty((h, qs[send_block]), dtype=sd, device=dev)
+        ops.fill_empty(o_s, l_s)
+        send = [o_s, l_s, q_block]
+        q_cur = q_block
+        for r in range(n):
+            j, j_next = (i - r) % n, (i - r - 1) % n
+            _expect(q_block_id, j, f"worker {i} round {r} query")
+            _expect(send_block, (j + 1) % n, f"worker {i} round {r} state")
+            rec = R[r]
+            recv = [_shaped(rec["O"], h, qs[j], d), _shaped(rec["L"], h, qs[j]),
+                    _shaped(rec["Q"], h, qs[j_next], d)]
+            dst = [_shaped(rec["O"], h, qs[send_block], d), _shaped(rec["L"], h, qs[send_block]),
+                   _shaped(rec["Q"], h, qs[j], d)]
+            t0 = ops.event() if trace is not None else None
+            hop, sent = ctx.shift(send, recv, ["O", "L", "Q"], dst=dst)
+            t1, t2 = _attend_merge(ops, q_cur, k_block, v_block, scale, recv[0], recv[1], hop,
+                                   kv_stream, r == 0, True)      # merge(recv, delta)
+            if trace is not None:
+                t3 = ops.event()
+                trace._add_timed(ops, t0, t1, t2, sent)
+                trace.section("fwd_kernel", ops, t0, t1)
+                trace.section("fwd_finish", ops, t2, t3)
+                trace.section("wait", ops, t1, t2)
+            send, q_cur = recv, recv[2]
+            send_block, q_block_id = j, j_next
 
-    cur = 0
-    send_block = (i + 1) % n
-    o_s, l_s = O.view(cur, qs[send_block]), Lb.view(cur, qs[send_block])
-    ops.fill_empty(o_s, l_s)
-    q_cur = _dev_copy(q_block, Qb.view(cur, qs[i]))
-    q_block_id = i
-    for r in range(n):
-        j, j_next = (i - r) % n, (i - r - 1) % n
-        _expect(q_block_id, j, f"worker {i} round {r} query")
-        _expect(send_block, (j + 1) % n, f"worker {i} round {r} state")
-        o_r, l_r = O.view(1 - cur, qs[j]), Lb.view(1 - cur, qs[j])
-        q_r = Qb.view(1 - cur, qs[j_next])
-        if n == 1:  # loopback (cluster.py:178-180): the sent state comes straight back
-            o_r, l_r, q_r = o_s, l_s, q_cur
-        t0 = ops.event() if trace is not None else None
-        hop, sent = ctx.shift([o_s, l_s, q_cur], [o_r, l_r, q_r], ["O", "L", "Q"])
-        if r == 0 and kv_stream is not None and len(kv_stream.bounds) > 1:
-            # K/V still streaming in: one partial + merge per resident chunk
-            for c, (a, b) in enumerate(kv_stream.bounds):
-                if kv_stream.wait_chunk is not None:
-                    kv_stream.wait_chunk(c)
-                kc, vc = k_block[:, a:b], v_block[:, a:b]
-                ws = ops.fwd_workspace(q_cur, kc)
-                ops.fwd_partial(q_cur, kc, vc, scale, ws)
-                if c == 0:
-                    t1 = ops.event() if trace is not None else None
-                    hop.wait()
-                    t2 = ops.event() if trace is not None else None
-                ops.fwd_finish(q_cur, kc, ws, o_r, l_r, o_r, l_r)
-        else:
-            if kv_stream is not None and kv_stream.wait_chunk is not None:
-                for c in range(len(kv_stream.bounds)):
-                    kv_stream.wait_chunk(c)
-            ws = ops.fwd_workspace(q_cur, k_block)
-            ops.fwd_partial(q_cur, k_block, v_block, scale, ws)
-            t1 = ops.event() if trace is not None else None
-            hop.wait()
-            t2 = ops.event() if trace is not None else None
-            ops.fwd_finish(q_cur, k_block, ws, o_r, l_r, o_r, l_r)   # merge(recv, delta)
-        if trace is not None:
-            t3 = ops.event()
-            trace._add_timed(ops, t0, t1, t2, sent)
-            trace.section("fwd_kernel", ops, t0, t1)
-            trace.section("fwd_finish", ops, t2, t3)
-            trace.section("wait", ops, t1, t2)
-        o_s, l_s, q_cur = o_r, l_r, q_r
-        send_block, q_block_id, cur = j, j_next, 1 - cur
-
-    # epilogue: the completed state of block i+1 goes home (strategies.py:220-231)
-    out_o = torch.empty((h, qs[i], d), dtype=sd, device=dev)
-    out_l = torch.empty((h, qs[i]), dtype=sd, device=dev)
-    if n == 1:
-        out_o.copy_(o_s)
-        out_l.copy_(l_s)
-        epi = {"O": 0, "L": 0}
-    else:
-        hop, epi = ctx.shift([o_s, l_s], [out_o, out_l], ["O", "L"])
+        # epilogue: the completed state of block i+1 goes home (strategies.py:220-231)
+        _expect(send_block, (i + 1) % n, f"worker {i} epilogue")
+        recv = [_shaped(home["O"], h, qs[i], d), _shaped(home["L"], h, qs[i])]
+        dst = [_shaped(home["O"], h, qs[send_block], d), _shaped(home["L"], h, qs[send_block])]
+        hop, epi = ctx.shift(send[:2], recv, ["O", "L"], dst=dst)
         hop.wait()
-    _expect(send_block, (i + 1) % n, f"worker {i} epilogue")
+        out_o, out_l = recv[0].clone(), recv[1].clone()
     if trace is not None:
         trace.epilogue_bytes_by_class = epi
     return AttentionState(O=out_o, L=out_l)
@@ -310,112 +347,91 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     reference's convention): everything is computed and carried in the fp32
     state dtype and the batched dK/dV pass writes bf16 gradients directly.
 
-    B200 schedule (same messages and bytes per rank as the reference; see
-    DESIGN.md §5):
+    B200 schedule (same bytes per rank as the reference):
       * the immutable part (Q, dO, L, D) of block j is sent at the START of
-        round r, overlapping this round's dQ kernel, instead of after it;
+        round r, overlapping this round's dQ kernel, instead of after it; it
+        lands at block j's rows of the receiver's gather buffers, so every
+        rank ends the ring holding every block's rows with no extra copy;
       * dQ lags one hop: round r sends the dQ of block j+1 finished in round
         r-1, and the received dQ of block j is folded in by the dQ finish
-        kernel after the local contribution is computed;
-      * every block's (Q, dO, L, D) passes through every rank anyway, so dK_i
-        and dV_i (the sum over rounds at strategies.py:261-262) are computed
-        ONCE after the ring over all gathered query rows — one tensor-core
-        pass with dK/dV in TMEM and a single write, instead of n passes with
-        an fp32 read-modify-write each.
+        kernel after the local contribution is computed; the epilogue hop
+        takes the last one home;
+      * dK_i and dV_i (the sum over rounds at strategies.py:261-262) are
+        computed ONCE after the ring over the gathered query rows — one
+        tensor-core pass with dK/dV in TMEM and a single write, instead of n
+        passes with an fp32 read-modify-write each.
     """
     n, i, ops = ctx.n, ctx.rank, ctx.ops
     h, _, d = q_block.shape
     dev = q_block.device
     sd = ops.state_dtype(q_block.dtype)
+    gd = _grad_dtype(ops, q_block.dtype)
     qs, qr = shards.q_sizes, shards.q_ranges
     mq = max(qs) if qs else 0
-    Qb = _Flat(h, mq, d, q_block.dtype, dev)
-    Gb = _Flat(h, mq, d, q_block.dtype, dev)
-    Lb = _Flat(h, mq, None, sd, dev)
-    Db = _Flat(h, mq, None, sd, dev)
-    dQb = _Flat(h, mq, d, sd, dev)
-    if n > 1:   # gather of every block's immutable rows for the batched dK/dV
-        s_tot = sum(qs)
-        Qg = torch.empty((h, s_tot, d), dtype=q_block.dtype, device=dev)
-        Gg = torch.empty((h, s_tot, d), dtype=q_block.dtype, device=dev)
-        Lg = torch.empty((h, s_tot), dtype=sd, device=dev)
-        Dg = torch.empty((h, s_tot), dtype=sd, device=dev)
-
-    cur = 0
-    q_j = _dev_copy(q_block, Qb.view(cur, qs[i]))
-    do_j = _dev_copy(do_block, Gb.view(cur, qs[i]))
-    l_j = _dev_copy(state.L, Lb.view(cur, qs[i]))
-    d_j = Db.view(cur, qs[i])
-    ops.row_stats(state.O, do_block, d_j)             # strategies.py:247
-    gd = _grad_dtype(ops, q_block.dtype)
     dk = torch.empty(k_block.shape, dtype=gd, device=dev)   # written once, in gd
     dv = torch.empty(v_block.shape, dtype=gd, device=dev)
-    early_dkv = n == 1 and kv_stream is not None and kv_stream.dkv_done is not None
-    if early_dkv:   # n = 1: the rows are all local, so dK/dV first and their chunks
-        # leave the GPU while the dQ kernel runs
-        t4 = ops.event() if trace is not None else None
-        _dkv_chunks(ops, kv_stream, q_j, k_block, v_block, l_j, d_j, do_j, scale, dk, dv)
-        if trace is not None:
-            trace.section("dkv_kernel", ops, t4, ops.event())
-    dq_prev = None
-    blk = i
-    for r in range(n):
-        j, nxt = (i - r) % n, (i - r - 1) % n
-        _expect(blk, j, f"worker {i} backward round {r}")
-        send = [q_j, do_j, l_j, d_j]
-        recv = [Qb.view(1 - cur, qs[nxt]), Gb.view(1 - cur, qs[nxt]),
-                Lb.view(1 - cur, qs[nxt]), Db.view(1 - cur, qs[nxt])]
-        classes = ["Q", "dO", "L", "D"]
-        dq_in = None
-        if r >= 1:   # dQ of block j+1 (finished last round) out, dQ of block j in
-            dq_in = dQb.view(r % 2, qs[j])
-            send.append(dq_prev)
-            recv.append(dq_in)
-            classes.append("dQ")
+    with ctx.call() as call:
         if n == 1:
-            recv = send
-        t0 = ops.event() if trace is not None else None
-        hop, sent = ctx.shift(send, recv, classes)
-        ws = ops.bwd_workspace(q_j, k_block)
-        ops.bwd_dq_partial(q_j, k_block, v_block, l_j, d_j, do_j, scale, ws)
-        t1 = ops.event() if trace is not None else None
-        if n > 1:
-            a, b = qr[j]
-            Qg[:, a:b].copy_(q_j)
-            Gg[:, a:b].copy_(do_j)
-            Lg[:, a:b].copy_(l_j)
-            Dg[:, a:b].copy_(d_j)
-        else:
-            Qg, Gg, Lg, Dg = q_j, do_j, l_j, d_j
-        hop.wait()
-        t2 = ops.event() if trace is not None else None
-        if dq_in is None:
-            dq_acc = dQb.view(0, qs[j])
-            ops.bwd_dq_finish(q_j, k_block, ws, dq_acc, accumulate=False)
-        else:
-            ops.bwd_dq_finish(q_j, k_block, ws, dq_in, accumulate=True)
-            dq_acc = dq_in
-        if trace is not None:
-            t3 = ops.event()
-            trace._add_timed(ops, t0, t1, t2, sent)
-            trace.section("dq_kernel", ops, t0, t1)
-            trace.section("gather+wait", ops, t1, t2)
-            trace.section("dq_finish", ops, t2, t3)
-        dq_prev = dq_acc
-        if n > 1:
-            q_j, do_j, l_j, d_j = recv[:4]
-        blk, cur = nxt, 1 - cur
-    _expect(blk, i, f"worker {i} backward homecoming")
-    # the dQ of block i+1 goes home; this rank's own dQ_i arrives
-    dq_out = torch.empty((h, qs[i], d), dtype=sd, device=dev)
-    if n == 1:
-        dq_out.copy_(dq_prev)
-    else:
-        hop, epi = ctx.shift([dq_prev], [dq_out], ["dQ"])
-        hop.wait()
+            return _lvx_backward_local(ops, q_block, k_block, v_block, state, do_block, scale,
+                                       trace, kv_stream, dk, dv, sd, gd)
+        s_tot = sum(qs)
+        buf = call.alloc({"Qg": (h * s_tot * d, q_block.dtype), "Gg": (h * s_tot * d, q_block.dtype),
+                          "Lg": (h * s_tot, sd), "Dg": (h * s_tot, sd),
+                          "dq": (n, [("dQ", h * mq * d, sd)]),
+                          "home": (1, [("dQ", h * mq * d, sd)])})
+        Qg, Gg = buf["Qg"].view(h, s_tot, d), buf["Gg"].view(h, s_tot, d)
+        Lg, Dg = buf["Lg"].view(h, s_tot), buf["Dg"].view(h, s_tot)
+        DQ = [rec["dQ"] for rec in buf["dq"]]
+        a, b = qr[i]
+        Qg[:, a:b].copy_(q_block)
+        Gg[:, a:b].copy_(do_block)
+        Lg[:, a:b].copy_(state.L)
+        ops.row_stats(state.O, do_block, Dg[:, a:b])          # strategies.py:247
+        dq_prev, blk = None, i
+        for r in range(n):
+            j, nxt = (i - r) % n, (i - r - 1) % n
+            _expect(blk, j, f"worker {i} backward round {r}")
+            (a, b), (an, bn) = qr[j], qr[nxt]
+            q_j, do_j, l_j, d_j = Qg[:, a:b], Gg[:, a:b], Lg[:, a:b], Dg[:, a:b]
+            send = [q_j, do_j, l_j, d_j]
+            dst = list(send)        # block j's rows: the same offsets on the successor
+            recv = [Qg[:, an:bn], Gg[:, an:bn], Lg[:, an:bn], Dg[:, an:bn]]
+            classes = ["Q", "dO", "L", "D"]
+            dq_in = None
+            if r >= 1:   # dQ of block j+1 (finished last round) out, dQ of block j in
+                dq_in = _shaped(DQ[r], h, qs[j], d)
+                send.append(dq_prev)
+                dst.append(_shaped(DQ[r], h, qs[(j + 1) % n], d))
+                recv.append(dq_in)
+                classes.append("dQ")
+            t0 = ops.event() if trace is not None else None
+            hop, sent = ctx.shift(send, recv, classes, dst=dst)
+            ws = ops.bwd_workspace(q_j, k_block)
+            ops.bwd_dq_partial(q_j, k_block, v_block, l_j, d_j, do_j, scale, ws)
+            t1 = ops.event() if trace is not None else None
+            hop.wait()
+            t2 = ops.event() if trace is not None else None
+            if dq_in is None:
+                dq_acc = _shaped(DQ[0], h, qs[j], d)
+                ops.bwd_dq_finish(q_j, k_block, ws, dq_acc, accumulate=False)
+            else:
+                ops.bwd_dq_finish(q_j, k_block, ws, dq_in, accumulate=True)
+                dq_acc = dq_in
+            if trace is not None:
+                t3 = ops.event()
+                trace._add_timed(ops, t0, t1, t2, sent)
+                trace.section("dq_kernel", ops, t0, t1)
+                trace.section("wait", ops, t1, t2)
+                trace.section("dq_finish", ops, t2, t3)
+            dq_prev, blk = dq_acc, nxt
+        _expect(blk, i, f"worker {i} backward homecoming")
+        # the dQ of block i+1 goes home; this rank's own dQ_i arrives
+        home = buf["home"][0]["dQ"]
+        dq_home = _shaped(home, h, qs[i], d)
+        hop, epi = ctx.shift([dq_prev], [dq_home], ["dQ"],
+                             dst=[_shaped(home, h, qs[(i + 1) % n], d)])
         if trace is not None:
             trace.epilogue_bytes_by_class = epi
-    if not early_dkv:
         t4 = ops.event() if trace is not None else None
         if kv_stream is not None and kv_stream.dkv_done is not None:
             _dkv_chunks(ops, kv_stream, Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv)
@@ -423,7 +439,46 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
             ops.bwd_dkv(Qg, k_block, v_block, Lg, Dg, Gg, scale, dk, dv, accumulate=False)
         if trace is not None:
             trace.section("dkv_kernel", ops, t4, ops.event())
-    return dq_out.to(gd), dk, dv
+        hop.wait()
+        dq_out = dq_home.to(gd, copy=True)
+    return dq_out, dk, dv
+
+
+def _lvx_backward_local(ops, q_block, k_block, v_block, state, do_block, scale, trace,
+                        kv_stream, dk, dv, sd, gd):
+    """n = 1: the one round of lvx_backward on the resident block (loopback
+    hops are free and carry nothing)."""
+    h, rows, d = q_block.shape
+    dev = q_block.device
+    D = torch.empty((h, rows), dtype=sd, device=dev)
+    ops.row_stats(state.O, do_block, D)                      # strategies.py:247
+    streamed = kv_stream is not None and kv_stream.dkv_done is not None
+    if streamed:   # dK/dV first, so their chunks leave the GPU while dQ runs
+        t4 = ops.event() if trace is not None else None
+        _dkv_chunks(ops, kv_stream, q_block, k_block, v_block, state.L, D, do_block, scale,
+                    dk, dv)
+        if trace is not None:
+            trace.section("dkv_kernel", ops, t4, ops.event())
+    dq = torch.empty((h, rows, d), dtype=sd, device=dev)
+    t0 = ops.event() if trace is not None else None
+    ws = ops.bwd_workspace(q_block, k_block)
+    ops.bwd_dq_partial(q_block, k_block, v_block, state.L, D, do_block, scale, ws)
+    t1 = ops.event() if trace is not None else None
+    ops.bwd_dq_finish(q_block, k_block, ws, dq, accumulate=False)
+    if trace is not None:
+        t3 = ops.event()
+        trace._add_timed(ops, t0, t1, t1, {"Q": 0, "dO": 0, "L": 0, "D": 0})
+        trace.section("dq_kernel", ops, t0, t1)
+        trace.section("wait", ops, t1, t1)
+        trace.section("dq_finish", ops, t1, t3)
+        trace.epilogue_bytes_by_class = {"dQ": 0}
+    if not streamed:
+        t4 = ops.event() if trace is not None else None
+        ops.bwd_dkv(q_block, k_block, v_block, state.L, D, do_block, scale, dk, dv,
+                    accumulate=False)
+        if trace is not None:
+            trace.section("dkv_kernel", ops, t4, ops.event())
+    return (dq if gd == sd else dq.to(gd)), dk, dv
 
 
 def _grad_dtype(ops, dt):
@@ -443,12 +498,17 @@ def _dkv_chunks(ops, kv_stream: KVStream, q, k_block, v_block, L, D, g, scale, d
 # Ring Attention KV rotation (the baseline)
 # ---------------------------------------------------------------------------
 
+RING_SLOTS = 3   # receive slots per rotating class (K/V, dK/dV partials)
+
+
 def ring_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                  scale: float, tile_rows: int = DEFAULT_TILE_ROWS,
                  trace: RoundTrace | None = None) -> AttentionState:
     """KV-rotation forward (strategies.py:279-311): Q/O/L stay resident and
-    (K, V) shift n-1 times, each shift overlapping the attention on the block
-    in hand."""
+    (K, V) shift n-1 times, each shift (sent at the start of the round)
+    overlapping the attention on the block in hand.  Blocks land in
+    RING_SLOTS reusable slots; a slot is released to the sender once the
+    round that computed on it (and forwarded it) is done."""
     n, i, ops = ctx.n, ctx.rank, ctx.ops
     h, rows, d = q_block.shape
     hk = k_block.shape[0]
@@ -456,99 +516,153 @@ def ring_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     sd = ops.state_dtype(q_block.dtype)
     ks = shards.kv_sizes
     mk = max(ks) if ks else 0
+    S = max(1, min(RING_SLOTS, n - 1))
     O = torch.empty((h, rows, d), dtype=sd, device=dev)
     L = torch.empty((h, rows), dtype=sd, device=dev)
-    ops.fill_empty(O, L)
-    if n > 1:
-        Kb = _Flat(hk, mk, d, k_block.dtype, dev)
-        Vb = _Flat(hk, mk, d, v_block.dtype, dev)
-        k_cur = _dev_copy(k_block, Kb.view(0, ks[i]))
-        v_cur = _dev_copy(v_block, Vb.view(0, ks[i]))
-    else:
-        k_cur, v_cur = k_block, v_block
-    cur, blk = 0, i
-    for r in range(n):
-        hop, sent = None, {}
-        nxt = (i - r - 1) % n
-        if r < n - 1:
-            hop, sent = ctx.shift([k_cur, v_cur], [Kb.view(1 - cur, ks[nxt]),
-                                                   Vb.view(1 - cur, ks[nxt])], ["K", "V"])
-        t0 = ops.event() if trace is not None else None
-        ws = ops.fwd_workspace(q_block, k_cur)
-        ops.fwd_partial(q_block, k_cur, v_cur, scale, ws)
-        ops.fwd_finish(q_block, k_cur, ws, O, L, O, L)       # merge(state, delta)
-        t1 = ops.event() if trace is not None else None
-        if trace is not None:
-            trace.section("fwd_kernel", ops, t0, t1)
-        if hop is not None:
-            hop.wait()
-            k_cur, v_cur = Kb.view(1 - cur, ks[nxt]), Vb.view(1 - cur, ks[nxt])
-            blk, cur = nxt, 1 - cur
-        t2 = ops.event() if trace is not None else None
-        if trace is not None:
-            trace._add_timed(ops, t0, t1, t2, sent)
+    with ctx.call() as call:
+        R = call.alloc({"kv": (S, [("K", hk * mk * d, k_block.dtype),
+                                   ("V", hk * mk * d, v_block.dtype)])})["kv"] if n > 1 else None
+        k_cur, v_cur, blk = k_block, v_block, i
+        for r in range(n):
+            _expect(blk, (i - r) % n, f"worker {i} ring round {r}")
+            hop, sent = None, {}
+            nxt = (i - r - 1) % n
+            if r < n - 1:
+                s = R[r % S]
+                recv = [_shaped(s["K"], hk, ks[nxt], d), _shaped(s["V"], hk, ks[nxt], d)]
+                dst = [_shaped(s["K"], hk, ks[blk], d), _shaped(s["V"], hk, ks[blk], d)]
+                hop, sent = ctx.shift([k_cur, v_cur], recv, ["K", "V"], dst=dst,
+                                      after=_after(ctx, 0, r, S))
+            t0 = ops.event() if trace is not None else None
+            if ks[blk]:
+                ws = ops.fwd_workspace(q_block, k_cur)
+                ops.fwd_partial(q_block, k_cur, v_cur, scale, ws)
+                ops.fwd_finish(q_block, k_cur, ws, O, L, O if r else None, L if r else None)
+            elif r == 0:
+                ops.fill_empty(O, L)
+            t1 = ops.event() if trace is not None else None
+            if trace is not None:
+                trace.section("fwd_kernel", ops, t0, t1)
+            if r >= 1:   # the slot this round computed on (message r-1) is free
+                _release(ctx, 0, r - 1, S)
+            if hop is not None:
+                hop.wait()
+                k_cur, v_cur, blk = recv[0], recv[1], nxt
+            t2 = ops.event() if trace is not None else None
+            if trace is not None:
+                trace._add_timed(ops, t0, t1, t2, sent)
     return AttentionState(O=O, L=L)
 
 
 def ring_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                   state: AttentionState, do_block, scale: float,
                   trace: RoundTrace | None = None):
-    """KV-rotation backward (strategies.py:314-361): (K, V, dK, dV) rotate
-    n-1 times while dQ accumulates locally; an epilogue hop returns each
-    (dK, dV) pair to its owner."""
+    """KV-rotation backward (strategies.py:314-361): (K, V) rotate n-1 times
+    while dQ accumulates locally, and each block's dK/dV partial follows its
+    K/V around the ring; an epilogue hop returns each (dK, dV) to its owner.
+
+    Overlapped schedule (same bytes per rank as the reference, K/V and dK/dV
+    as separate messages): K/V of the next round are sent at the START of the
+    round; this round's dK/dV contribution is computed into a local fp32
+    buffer while the partial of the same block is still in flight from the
+    predecessor, then added to it (``accumulate``) and forwarded — the
+    partials lag one hop behind the K/V they belong to."""
     n, i, ops = ctx.n, ctx.rank, ctx.ops
     h, rows, d = q_block.shape
     hk = k_block.shape[0]
     dev = q_block.device
     sd = ops.state_dtype(q_block.dtype)
+    gd = _grad_dtype(ops, q_block.dtype)
     ks = shards.kv_sizes
     mk = max(ks) if ks else 0
+    S = max(1, min(RING_SLOTS, n - 1))
     D = torch.empty((h, rows), dtype=sd, device=dev)
     ops.row_stats(state.O, do_block, D)
     L = state.L
     dq = torch.zeros((h, rows, d), dtype=sd, device=dev)
-    Kb = _Flat(hk, mk, d, k_block.dtype, dev)
-    Vb = _Flat(hk, mk, d, v_block.dtype, dev)
-    dKb = _Flat(hk, mk, d, sd, dev)
-    dVb = _Flat(hk, mk, d, sd, dev)
-    cur = 0
-    k_cur = _dev_copy(k_block, Kb.view(0, ks[i]))
-    v_cur = _dev_copy(v_block, Vb.view(0, ks[i]))
-    dk_cur, dv_cur = dKb.view(0, ks[i]), dVb.view(0, ks[i])
-    dk_cur.zero_()
-    dv_cur.zero_()
-    blk = i
-    for r in range(n):
-        t0 = ops.event() if trace is not None else None
-        ops.bwd_accumulate(q_block, k_cur, v_cur, L, D, do_block, scale, dq, dk_cur, dv_cur)
-        t1 = ops.event() if trace is not None else None
-        sent = {}
-        if r < n - 1:
+    with ctx.call() as call:
+        if n == 1:
+            dk = torch.empty(k_block.shape, dtype=sd, device=dev)
+            dv = torch.empty(v_block.shape, dtype=sd, device=dev)
+            t0 = ops.event() if trace is not None else None
+            ws = ops.bwd_workspace(q_block, k_block)
+            ops.bwd_dq_partial(q_block, k_block, v_block, L, D, do_block, scale, ws)
+            ops.bwd_dq_finish(q_block, k_block, ws, dq, accumulate=False)
+            ops.bwd_dkv(q_block, k_block, v_block, L, D, do_block, scale, dk, dv, accumulate=False)
+            if trace is not None:
+                t1 = ops.event()
+                trace._add_timed(ops, t0, t1, t1, {})
+                trace.epilogue_bytes_by_class = {"dK": 0, "dV": 0}
+            return _cast(dq, gd), _cast(dk, gd), _cast(dv, gd)
+        buf = call.alloc({"kv": (S, [("K", hk * mk * d, k_block.dtype),
+                                     ("V", hk * mk * d, v_block.dtype)]),
+                          "part": (S, [("dK", hk * mk * d, sd), ("dV", hk * mk * d, sd)]),
+                          "home": (1, [("dK", hk * mk * d, sd), ("dV", hk * mk * d, sd)])})
+        R, P, home = buf["kv"], buf["part"], buf["home"][0]
+        own_k = torch.empty((hk, ks[i], d), dtype=sd, device=dev)   # round 0's partial
+        own_v = torch.empty((hk, ks[i], d), dtype=sd, device=dev)
+        tmp_k = torch.empty((hk * mk * d,), dtype=sd, device=dev)
+        tmp_v = torch.empty((hk * mk * d,), dtype=sd, device=dev)
+        k_cur, v_cur, blk = k_block, v_block, i
+        hop_p = recv_p = None
+        for r in range(n):
+            _expect(blk, (i - r) % n, f"worker {i} ring backward round {r}")
             nxt = (i - r - 1) % n
-            recv = [Kb.view(1 - cur, ks[nxt]), Vb.view(1 - cur, ks[nxt]),
-                    dKb.view(1 - cur, ks[nxt]), dVb.view(1 - cur, ks[nxt])]
-            hop, sent = ctx.shift([k_cur, v_cur, dk_cur, dv_cur], recv, ["K", "V", "dK", "dV"])
-            hop.wait()
-            k_cur, v_cur, dk_cur, dv_cur = recv
-            blk, cur = nxt, 1 - cur
-        t2 = ops.event() if trace is not None else None
-        if trace is not None:
-            trace._add_timed(ops, t0, t1, t2, sent)
-    # dk_cur / dv_cur now belong to block i+1: send them home
-    dk = torch.empty((hk, ks[i], d), dtype=sd, device=dev)
-    dv = torch.empty((hk, ks[i], d), dtype=sd, device=dev)
-    if n == 1:
-        dk.copy_(dk_cur)
-        dv.copy_(dv_cur)
-        epi = {"dK": 0, "dV": 0}
-    else:
-        hop, epi = ctx.shift([dk_cur, dv_cur], [dk, dv], ["dK", "dV"])
-        hop.wait()
-    _expect(blk, (i + 1) % n, f"worker {i} backward epilogue")
+            hop_kv, sent = None, {}
+            if r < n - 1:
+                s = R[r % S]
+                recv_kv = [_shaped(s["K"], hk, ks[nxt], d), _shaped(s["V"], hk, ks[nxt], d)]
+                dst = [_shaped(s["K"], hk, ks[blk], d), _shaped(s["V"], hk, ks[blk], d)]
+                hop_kv, sent = ctx.shift([k_cur, v_cur], recv_kv, ["K", "V"], dst=dst,
+                                         after=_after(ctx, 0, r, S))
+            t0 = ops.event() if trace is not None else None
+            ws = ops.bwd_workspace(q_block, k_cur)
+            ops.bwd_dq_partial(q_block, k_cur, v_cur, L, D, do_block, scale, ws)
+            ops.bwd_dq_finish(q_block, k_cur, ws, dq, accumulate=True)
+            if r == 0:
+                acc_k, acc_v = own_k, own_v
+                ops.bwd_dkv(q_block, k_cur, v_cur, L, D, do_block, scale, acc_k, acc_v,
+                            accumulate=False)
+            else:
+                tk, tv = _shaped(tmp_k, hk, ks[blk], d), _shaped(tmp_v, hk, ks[blk], d)
+                ops.bwd_dkv(q_block, k_cur, v_cur, L, D, do_block, scale, tk, tv,
+                            accumulate=False)
+                hop_p.wait()                 # the partial of this block from upstream
+                acc_k, acc_v = recv_p
+                ops.accumulate(tk, acc_k)
+                ops.accumulate(tv, acc_v)
+            t1 = ops.event() if trace is not None else None
+            if r >= 1:
+                _release(ctx, 0, r - 1, S)   # K/V slot computed on this round
+            if r < n - 1:                    # the partial follows its block downstream
+                s = P[r % S]
+                recv_p = [_shaped(s["dK"], hk, ks[nxt], d), _shaped(s["dV"], hk, ks[nxt], d)]
+                dst = [_shaped(s["dK"], hk, ks[blk], d), _shaped(s["dV"], hk, ks[blk], d)]
+                hop_p, sent_p = ctx.shift([acc_k, acc_v], recv_p, ["dK", "dV"], dst=dst,
+                                          after=_after(ctx, 1, r, S))
+                sent = {**sent, **sent_p}
+            else:                            # block i+1 is complete: send it home
+                _expect(blk, (i + 1) % n, f"worker {i} backward epilogue")
+                recv_h = [_shaped(home["dK"], hk, ks[i], d), _shaped(home["dV"], hk, ks[i], d)]
+                dst = [_shaped(home["dK"], hk, ks[blk], d), _shaped(home["dV"], hk, ks[blk], d)]
+                hop_h, epi = ctx.shift([acc_k, acc_v], recv_h, ["dK", "dV"], dst=dst)
+            if r >= 1:
+                _release(ctx, 1, r - 1, S)   # partial slot added into and forwarded
+            if hop_kv is not None:
+                hop_kv.wait()
+                k_cur, v_cur, blk = recv_kv[0], recv_kv[1], nxt
+            t2 = ops.event() if trace is not None else None
+            if trace is not None:
+                trace._add_timed(ops, t0, t1, t2, sent)
+        hop_h.wait()
+        dk, dv = recv_h[0].to(gd, copy=True), recv_h[1].to(gd, copy=True)
     if trace is not None:
         trace.epilogue_bytes_by_class = epi
-    gd = _grad_dtype(ctx.ops, q_block.dtype)
-    return dq.to(gd), dk.to(gd), dv.to(gd)
+    return _cast(dq, gd), dk, dv
+
+
+def _cast(t: torch.Tensor, dt) -> torch.Tensor:
+    return t if t.dtype == dt else t.to(dt)
 
 
 # ---------------------------------------------------------------------------
@@ -577,42 +691,49 @@ def head_parallel_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_bloc
     dev = q_block.device
     sd = ops.state_dtype(q_block.dtype)
     qs, ks = shards.q_sizes, shards.kv_sizes
+    mq, mk = max(qs), max(ks)
     s_q, s_kv = sum(qs), sum(ks)
     q_full = torch.empty((hpw, s_q, d), dtype=q_block.dtype, device=dev)
     k_full = torch.empty((kpw, s_kv, d), dtype=k_block.dtype, device=dev)
     v_full = torch.empty((kpw, s_kv, d), dtype=v_block.dtype, device=dev)
-    chunks = [[q_block[w * hpw:(w + 1) * hpw].contiguous(),
-               k_block[w * kpw:(w + 1) * kpw].contiguous(),
-               v_block[w * kpw:(w + 1) * kpw].contiguous()] for w in range(n)]
-    recv = [[torch.empty((hpw, qs[w], d), dtype=q_block.dtype, device=dev),
-             torch.empty((kpw, ks[w], d), dtype=k_block.dtype, device=dev),
-             torch.empty((kpw, ks[w], d), dtype=v_block.dtype, device=dev)] for w in range(n)]
-    t0 = ops.event() if trace is not None else None
-    hop, g_sent = ctx.all_to_all(chunks, recv, ["Q", "K", "V"])
-    hop.wait()
-    for w in range(n):
-        (qa, qb), (ka, kb) = shards.q_ranges[w], shards.kv_ranges[w]
-        q_full[:, qa:qb].copy_(recv[w][0])
-        k_full[:, ka:kb].copy_(recv[w][1])
-        v_full[:, ka:kb].copy_(recv[w][2])
-    t1 = ops.event() if trace is not None else None
     O = torch.empty((hpw, s_q, d), dtype=sd, device=dev)
     L = torch.empty((hpw, s_q), dtype=sd, device=dev)
-    if s_kv == 0:
-        ops.fill_empty(O, L)
-    else:
-        ws = ops.fwd_workspace(q_full, k_full)
-        ops.fwd_partial(q_full, k_full, v_full, scale, ws)
-        ops.fwd_finish(q_full, k_full, ws, O, L)
-    t2 = ops.event() if trace is not None else None
-    out_chunks = [[O[:, qa:qb].contiguous(), L[:, qa:qb].contiguous()]
-                  for qa, qb in shards.q_ranges]
-    back = [[torch.empty((hpw, qs[i], d), dtype=sd, device=dev),
-             torch.empty((hpw, qs[i]), dtype=sd, device=dev)] for _ in range(n)]
-    hop, s_sent = ctx.all_to_all(out_chunks, back, ["O", "L"])
-    hop.wait()
-    o_i = torch.cat([b[0] for b in back], dim=0)
-    l_i = torch.cat([b[1] for b in back], dim=0)
+    with ctx.call() as call:
+        buf = call.alloc({"g": (n, [("Q", hpw * mq * d, q_block.dtype),
+                                    ("K", kpw * mk * d, k_block.dtype),
+                                    ("V", kpw * mk * d, v_block.dtype)]),
+                          "s": (n, [("O", hpw * mq * d, sd), ("L", hpw * mq, sd)])})
+        G, Sc = buf["g"], buf["s"]
+        chunks = [[q_block[w * hpw:(w + 1) * hpw], k_block[w * kpw:(w + 1) * kpw],
+                   v_block[w * kpw:(w + 1) * kpw]] for w in range(n)]
+        recv = [[_shaped(G[w]["Q"], hpw, qs[w], d), _shaped(G[w]["K"], kpw, ks[w], d),
+                 _shaped(G[w]["V"], kpw, ks[w], d)] for w in range(n)]
+        t0 = ops.event() if trace is not None else None
+        hop, g_sent = ctx.all_to_all(chunks, recv, ["Q", "K", "V"])
+        hop.wait()
+        for w in range(n):
+            (qa, qb), (ka, kb) = shards.q_ranges[w], shards.kv_ranges[w]
+            q_full[:, qa:qb].copy_(recv[w][0])
+            k_full[:, ka:kb].copy_(recv[w][1])
+            v_full[:, ka:kb].copy_(recv[w][2])
+        t1 = ops.event() if trace is not None else None
+        if s_kv == 0:
+            ops.fill_empty(O, L)
+        else:
+            ws = ops.fwd_workspace(q_full, k_full)
+            ops.fwd_partial(q_full, k_full, v_full, scale, ws)
+            ops.fwd_finish(q_full, k_full, ws, O, L)
+        t2 = ops.event() if trace is not None else None
+        out_chunks = [[O[:, qa:qb], L[:, qa:qb]] for qa, qb in shards.q_ranges]
+        back = [[_shaped(Sc[w]["O"], hpw, qs[i], d), _shaped(Sc[w]["L"], hpw, qs[i])]
+                for w in range(n)]
+        # rank w keeps our block in its record i, sized by ITS rows
+        dst = [[_shaped(Sc[i]["O"], hpw, qs[w], d), _shaped(Sc[i]["L"], hpw, qs[w])]
+               for w in range(n)]
+        hop, s_sent = ctx.all_to_all(out_chunks, back, ["O", "L"], dst=dst)
+        hop.wait()
+        o_i = torch.cat([b[0] for b in back], dim=0)
+        l_i = torch.cat([b[1] for b in back], dim=0)
     if trace is not None:
         t3 = ops.event()
         trace._add_timed(ops, t1, t2, t3, {"QKV_gather": sum(g_sent.values()),
@@ -633,43 +754,51 @@ def head_parallel_backward(ctx: DeviceContext, shards: ShardSpec, saved, do_bloc
     dev = q_full.device
     sd = ops.state_dtype(q_full.dtype)
     qs, ks = shards.q_sizes, shards.kv_sizes
-    chunks = [[do_block[w * hpw:(w + 1) * hpw].contiguous()] for w in range(n)]
-    recv = [[torch.empty((hpw, qs[w], d), dtype=do_block.dtype, device=dev)] for w in range(n)]
-    t0 = ops.event() if trace is not None else None
-    hop, g_sent = ctx.all_to_all(chunks, recv, ["dO"])
-    hop.wait()
+    mq, mk = max(qs), max(ks)
     do_full = torch.empty((hpw, s_q, d), dtype=do_block.dtype, device=dev)
-    for w in range(n):
-        qa, qb = shards.q_ranges[w]
-        do_full[:, qa:qb].copy_(recv[w][0])
-    t1 = ops.event() if trace is not None else None
     D = torch.empty((hpw, s_q), dtype=sd, device=dev)
-    ops.row_stats(st.O, do_full, D)
     dq = torch.empty((hpw, s_q, d), dtype=sd, device=dev)
     dk = torch.empty((kpw, s_kv, d), dtype=sd, device=dev)
     dv = torch.empty((kpw, s_kv, d), dtype=sd, device=dev)
-    ws = ops.bwd_workspace(q_full, k_full)
-    ops.bwd_dq_partial(q_full, k_full, v_full, st.L, D, do_full, scale, ws)
-    ops.bwd_dq_finish(q_full, k_full, ws, dq, accumulate=False)
-    ops.bwd_dkv(q_full, k_full, v_full, st.L, D, do_full, scale, dk, dv, accumulate=False)
-    t2 = ops.event() if trace is not None else None
-    out = [[dq[:, qa:qb].contiguous(), dk[:, ka:kb].contiguous(), dv[:, ka:kb].contiguous()]
-           for (qa, qb), (ka, kb) in zip(shards.q_ranges, shards.kv_ranges)]
-    back = [[torch.empty((hpw, qs[i], d), dtype=sd, device=dev),
-             torch.empty((kpw, ks[i], d), dtype=sd, device=dev),
-             torch.empty((kpw, ks[i], d), dtype=sd, device=dev)] for _ in range(n)]
-    hop, s_sent = ctx.all_to_all(out, back, ["dQ", "dK", "dV"])
-    hop.wait()
+    gd = _grad_dtype(ops, do_block.dtype)
+    with ctx.call() as call:
+        buf = call.alloc({"g": (n, [("dO", hpw * mq * d, do_block.dtype)]),
+                          "s": (n, [("dQ", hpw * mq * d, sd), ("dK", kpw * mk * d, sd),
+                                    ("dV", kpw * mk * d, sd)])})
+        G, Sc = buf["g"], buf["s"]
+        chunks = [[do_block[w * hpw:(w + 1) * hpw]] for w in range(n)]
+        recv = [[_shaped(G[w]["dO"], hpw, qs[w], d)] for w in range(n)]
+        t0 = ops.event() if trace is not None else None
+        hop, g_sent = ctx.all_to_all(chunks, recv, ["dO"])
+        hop.wait()
+        for w in range(n):
+            qa, qb = shards.q_ranges[w]
+            do_full[:, qa:qb].copy_(recv[w][0])
+        t1 = ops.event() if trace is not None else None
+        ops.row_stats(st.O, do_full, D)
+        ws = ops.bwd_workspace(q_full, k_full)
+        ops.bwd_dq_partial(q_full, k_full, v_full, st.L, D, do_full, scale, ws)
+        ops.bwd_dq_finish(q_full, k_full, ws, dq, accumulate=False)
+        ops.bwd_dkv(q_full, k_full, v_full, st.L, D, do_full, scale, dk, dv, accumulate=False)
+        t2 = ops.event() if trace is not None else None
+        out = [[dq[:, qa:qb], dk[:, ka:kb], dv[:, ka:kb]]
+               for (qa, qb), (ka, kb) in zip(shards.q_ranges, shards.kv_ranges)]
+        back = [[_shaped(Sc[w]["dQ"], hpw, qs[i], d), _shaped(Sc[w]["dK"], kpw, ks[i], d),
+                 _shaped(Sc[w]["dV"], kpw, ks[i], d)] for w in range(n)]
+        dst = [[_shaped(Sc[i]["dQ"], hpw, qs[w], d), _shaped(Sc[i]["dK"], kpw, ks[w], d),
+                _shaped(Sc[i]["dV"], kpw, ks[w], d)] for w in range(n)]
+        hop, s_sent = ctx.all_to_all(out, back, ["dQ", "dK", "dV"], dst=dst)
+        hop.wait()
+        res = (torch.cat([b[0] for b in back], dim=0).to(gd),
+               torch.cat([b[1] for b in back], dim=0).to(gd),
+               torch.cat([b[2] for b in back], dim=0).to(gd))
     if trace is not None:
         t3 = ops.event()
         trace._add_timed(ops, t1, t2, t3, {"dO_gather": sum(g_sent.values()),
                                            "grad_scatter": sum(s_sent.values())})
         trace.section("bwd_kernel", ops, t1, t2)
         trace.section("all_to_all", ops, t0, t1)
-    gd = _grad_dtype(ops, do_block.dtype)
-    return (torch.cat([b[0] for b in back], dim=0).to(gd),
-            torch.cat([b[1] for b in back], dim=0).to(gd),
-            torch.cat([b[2] for b in back], dim=0).to(gd))
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -730,7 +859,8 @@ def _to_torch(x) -> tuple[torch.Tensor, str]:
 
 def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
                     scale: float | None = None, tile_rows: int = DEFAULT_TILE_ROWS,
-                    timeout: float | None = None, *, group=None, ops=None) -> RunResult:
+                    timeout: float | None = None, *, group=None, ops=None,
+                    ranks: str = "auto") -> RunResult:
     """Scatter Q/K/V by rows, run the strategy collectively, gather the full
     O, L (and gradients when dO is given) with transport stats and traces
     (strategies.py:454-551).
@@ -739,7 +869,12 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
     ranks (torchrun, one GPU each) every rank calls this with the same full
     inputs, uploads only its own shard, and all ranks return the gathered
     result.  Without a process group, n = 1 runs on the current GPU and
-    n > 1 spawns n processes on n local GPUs (``launch.spawn_run``).
+    n > 1 runs ``ranks``: "processes" (n processes on n local GPUs,
+    ``launch.spawn_run``), "threads" (n thread ranks sharing the current
+    device, the reference's own worker model, ``launch.spawn_ranks``), or
+    "auto" (processes when n GPUs are visible, else threads).  ``timeout``
+    (else $LVX_TIMEOUT_SECS, else 30 s) bounds every wait on a peer; the
+    first failing rank is raised as ``WorkerFailed`` (cluster.py:300-335).
     Output dtype = input dtype (O, L, grads), as the reference."""
     strategy = StrategyKind(strategy)
     validate_qkv(Q, K, V)
@@ -749,33 +884,67 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
         raise ValueError(f"dO shape {tuple(dO.shape)} != Q shape {tuple(Q.shape)}")
     scale = default_scale(d) if scale is None else scale
     n_req = spec.n if spec is not None else None
+    if strategy is StrategyKind.SINGLE and (n_req or 1) != 1:
+        raise ValueError("single-worker strategy requires n=1")
+    if strategy is StrategyKind.HEAD_PARALLEL and n_req:
+        _check_heads(h, K.shape[0], n_req)
     if dist.is_initialized() and (group is not None or n_req is None or n_req > 1 or
-                                  dist.get_world_size(group) == 1):
+                                  dist.get_world_size(group) == 1) and ranks != "threads":
         n = dist.get_world_size(group)
         rank = dist.get_rank(group)
         if n_req is not None and n_req != n:
             raise ValueError(f"spec.n={n_req} but the process group has {n} ranks")
-    else:
-        n = n_req or 1
-        rank = 0
-        if n > 1:
-            from .launch import spawn_run
-            return spawn_run(strategy.value, Q, K, V, dO, n, scale, tile_rows)
-    if strategy is StrategyKind.SINGLE and n != 1:
-        raise ValueError("single-worker strategy requires n=1")
-    if strategy is StrategyKind.HEAD_PARALLEL:
-        _check_heads(h, K.shape[0], n)
-    shards = ShardSpec.balanced(s_q, s_kv, n)
+        if strategy is StrategyKind.SINGLE and n != 1:
+            raise ValueError("single-worker strategy requires n=1")
+        if strategy is StrategyKind.HEAD_PARALLEL:
+            _check_heads(h, K.shape[0], n)
+        dev = _device_for(ops)
+        ctx = DeviceContext(rank, n, group=group if n > 1 else None, device=dev, ops=ops,
+                            timeout=timeout)
+        try:
+            return rank_body(strategy, ctx, Q, K, V, dO, scale, tile_rows)
+        finally:
+            ctx.close()
+    n = n_req or 1
+    if n == 1:
+        ctx = DeviceContext(0, 1, device=_device_for(ops), ops=ops, timeout=timeout)
+        return rank_body(strategy, ctx, Q, K, V, dO, scale, tile_rows)
+    from . import launch
+    if ranks not in ("auto", "threads", "processes"):
+        raise ValueError(f"ranks must be 'auto', 'threads' or 'processes', got {ranks!r}")
+    gpus = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if ranks == "processes" or (ranks == "auto" and ops is None and gpus >= n):
+        return launch.spawn_run(strategy.value, Q, K, V, dO, n, scale, tile_rows, timeout)
+    dev = _device_for(ops)
 
-    (Qt, kind), (Kt, _), (Vt, _) = _to_torch(Q), _to_torch(K), _to_torch(V)
-    dt = torch.promote_types(torch.promote_types(Qt.dtype, Kt.dtype), Vt.dtype)
+    def body(ctx):
+        return rank_body(strategy, ctx, Q, K, V, dO, scale, tile_rows)
+    res = launch.spawn_ranks(ClusterSpec(n), body, timeout=timeout, device=dev,
+                             ops_factory=(type(ops) if ops is not None else None))
+    return res.results[0]
+
+
+def _device_for(ops) -> torch.device:
     if ops is None:
         if not torch.cuda.is_available():
             raise RuntimeError("run_distributed needs a CUDA device (no CPU fallback)")
-        dev = torch.device("cuda", torch.cuda.current_device())
-    else:
-        dev = torch.device(getattr(ops, "device", "cuda"))
-    ctx = DeviceContext(rank, n, group=group if n > 1 else None, device=dev, ops=ops)
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(getattr(ops, "device", "cuda"))
+
+
+def rank_body(strategy, ctx: DeviceContext, Q, K, V, dO, scale: float,
+              tile_rows: int = DEFAULT_TILE_ROWS) -> RunResult:
+    """One rank of run_distributed on full host (or device) inputs: upload
+    this rank's shard, run the strategy, wait with the context's deadline,
+    gather O / L / grads by row range and the stats / traces of every rank
+    (strategies.py:475-551).  Every rank returns the same RunResult."""
+    strategy = StrategyKind(strategy)
+    n, rank, dev = ctx.n, ctx.rank, ctx.device
+    h, s_q, d = Q.shape
+    s_kv = K.shape[1]
+    shards = ShardSpec.balanced(s_q, s_kv, n)
+    (Qt, kind), (Kt, _), (Vt, _) = _to_torch(Q), _to_torch(K), _to_torch(V)
+    dt = torch.promote_types(torch.promote_types(Qt.dtype, Kt.dtype), Vt.dtype)
     qa, qb = shards.q_ranges[rank]
     ka, kb = shards.kv_ranges[rank]
     q_i = Qt[:, qa:qb].to(dev).to(dt).contiguous()
@@ -785,8 +954,7 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
     if dO is not None:
         do_i = _to_torch(dO)[0][:, qa:qb].to(dev).to(dt).contiguous()
     st, grads, tf, tb = run_rank(strategy, ctx, shards, q_i, k_i, v_i, do_i, scale, tile_rows)
-    if dev.type == "cuda":
-        torch.cuda.synchronize(dev)
+    ctx.synchronize()          # CollectiveTimeout if a hop never arrives
     tf.resolve()
     if tb is not None:
         tb.resolve()
@@ -800,8 +968,7 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
         full = torch.zeros(full_shape, dtype=dtype, device=dev)
         if local.numel():
             full[:, rng[0]:rng[1]] = local.to(dtype)
-        if n > 1:
-            dist.all_reduce(full, group=group)
+        ctx.all_reduce_sum_(full)
         return full
 
     O = gather(st.O, (h, s_q, d), shards.q_ranges[rank], out_dt)
@@ -814,8 +981,7 @@ def run_distributed(strategy, Q, K, V, dO=None, spec: ClusterSpec | None = None,
     stats = ctx.stats
     traces_f, traces_b = [tf], [tb] if tb is not None else None
     if n > 1:
-        objs = [None] * n
-        dist.all_gather_object(objs, (ctx.stats, tf, tb), group=group)
+        objs = ctx.all_gather_object((ctx.stats, tf, tb))
         stats = TransportStats()
         for s, _, _ in objs:
             stats.merge(s)

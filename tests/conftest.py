@@ -4,6 +4,9 @@ from pathlib import Path
 
 import pytest
 
+# thread ranks sharing one GPU put 2 streams per rank behind stream-side
+# waits: give every stream its own hardware queue (set before CUDA init)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 GOLDEN = ROOT / "tests" / "golden"

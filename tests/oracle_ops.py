@@ -108,6 +108,9 @@ class OracleOps:
             dk.copy_(gk)
             dv.copy_(gv)
 
+    def accumulate(self, src, dst):
+        dst += src
+
     def kv_recompute(self, y, w_k, w_v, k_out, v_out):
         h = k_out.shape[0]
         for w, out in ((w_k, k_out), (w_v, v_out)):
