@@ -36,7 +36,21 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CFG = dict(workload="llama3v-cross-attn-C2", s_q=2048, s_kv=1 << 20, hq=32, hkv=8, d=128)
+# BASELINE.json configs[1..4]; C2 is the headline (the driver's default run)
+WORKLOADS = {
+    "c2": dict(workload="llama3v-cross-attn-C2", s_q=2048, s_kv=1 << 20, hq=32, hkv=8, d=128),
+    # mPLUG-Owl3: Lkv sweep 256K..4M (headline point 1M)
+    "c3": dict(workload="owl3-cross-attn-C3", s_q=5514, s_kv=1 << 20, hq=28, hkv=4, d=128,
+               sweep=[1 << 18, 1 << 19, 1 << 20, 1 << 21, 1 << 22]),
+    # OpenFlamingo gated cross-attn: L layers sharing one visual-token copy y,
+    # K/V recomputed from y in the backward (d_embed 2048, OpenFlamingo-3B-like)
+    "c4": dict(workload="openflamingo-xattn-C4", s_q=1024, s_kv=1 << 19, hq=8, hkv=8, d=64,
+               layers=4, d_embed=2048),
+    # scaling sweep, Llama-3-V heads: Lkv 64K..15M, LV-XAttn vs Ring
+    "c5": dict(workload="lkv-sweep-C5", s_q=2048, s_kv=1 << 20, hq=32, hkv=8, d=128,
+               sweep=[1 << 16, 1 << 18, 1 << 20, 1 << 22, 15_000_000]),
+}
+CFG = dict(WORKLOADS["c2"])
 METRIC = "cross-attn fwd+bwd ms/layer & TFLOP/s at 1/2/4/8 B200; overhead vs no-comm bound"
 
 
@@ -50,8 +64,26 @@ def parse():
     ap.add_argument("--no-ring-compare", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--skv", type=int, default=CFG["s_kv"], help="(dev) override Lkv")
-    return ap.parse_args()
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
+                    help="BASELINE config (c2 = the headline; c3 / c5 sweep Lkv, c4 = layers "
+                         "with K/V recompute)")
+    ap.add_argument("--skv", type=int, default=None, help="Lkv (default: the workload's)")
+    ap.add_argument("--sweep", default=None,
+                    help="comma-separated Lkv list (default: the workload's sweep, if any)")
+    a = ap.parse_args()
+    wl = WORKLOADS[a.workload]
+    CFG.clear()
+    CFG.update({k: v for k, v in wl.items() if k != "sweep"})
+    if a.skv is not None:
+        CFG["s_kv"] = a.skv
+    if a.sweep:
+        a.points = [int(float(x)) for x in a.sweep.split(",")]
+    elif a.skv is None and "sweep" in wl:
+        a.points = list(wl["sweep"])
+    else:
+        a.points = [CFG["s_kv"]]
+    a.skv = CFG["s_kv"]
+    return a
 
 
 # ---------------------------------------------------------------- helpers
@@ -189,36 +221,100 @@ def reference_arm(args):
 
 # ---------------------------------------------------------------- native arm
 
+class Env:
+    """Per-process run context shared by the measurement legs."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={self.world}; "
+                             "launch N>1 with torchrun")
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.group = None
+        if self.world > 1:
+            # the process group carries only setup, barriers and the timing
+            # reduction; the ring hops are copy-engine transfers (comm.py)
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.group = dist.group.WORLD
+        from paper_2502_02406_b200 import build
+        if self.rank == 0 and not build.LIB.exists():
+            build.build()
+        if self.world > 1:
+            dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], device=self.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+
+
 def native_arm(args):
     import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    group = None
-    if world > 1:
-        # the ring hop's NCCL kernel becomes ready exactly when the next
-        # attention grid launches; high-priority NCCL streams let it take the
-        # first SM that frees instead of queueing behind the whole grid
-        os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
-        dist.init_process_group("nccl", device_id=dev)
-        group = dist.group.WORLD
-    from paper_2502_02406_b200 import build
-    if rank == 0 and not build.LIB.exists():
-        build.build()
-    if world > 1:
+    env = Env(args)
+    if args.workload == "c4":
+        out = layer_arm(args, env)
+    else:
+        import paper_2502_02406_b200 as lvx
+        ctx = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev)
+        ctx_nc = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev,
+                                   comm_enabled=False)
+        head_skv = CFG["s_kv"] if CFG["s_kv"] in args.points else args.points[-1]
+        lines = []
+        for skv in args.points:
+            lines.append(measure_point(args, env, ctx, ctx_nc, skv, head=(skv == head_skv)))
+            torch.cuda.empty_cache()
+        out = next(ln for ln, skv in zip(lines, args.points) if skv == head_skv)
+        if len(lines) > 1:
+            out["sweep"] = [_summary(ln) for ln in lines]
+    if env.rank == 0 and env.world == 1 and not args.no_cpu:
+        v, sample, threads = cpu_reference_rate()
+        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                               "sample": sample + " (TFLOP/s on a sample, not the full workload)",
+                               "c1": cpu_c1_timing()}
+    if env.rank == 0:
+        print(json.dumps(out), flush=True)
+    if env.world > 1:
+        import torch.distributed as dist
         dist.barrier()
-    import paper_2502_02406_b200 as lvx
+        dist.destroy_process_group()
+
+
+def _summary(line: dict) -> dict:
+    keep = ("value", "ms_per_step", "overhead_vs_no_comm", "no_comm_ms_per_step")
+    out = {"s_kv": line["config"]["s_kv"], **{k: line.get(k) for k in keep}}
+    out["roofline_frac"] = line["roofline"]["frac"]
+    out["fwd_tflops"] = line["roofline"]["fwd_tflops"]
+    out["bwd_tflops"] = line["roofline"]["bwd_tflops"]
+    if "ring_baseline" in line:
+        out["ring_ms_per_step"] = line["ring_baseline"]["ms_per_step"]
+        out["speedup_lvx_over_ring"] = line["ring_baseline"]["speedup_lvx_over_ring"]
+    return out
+
+
+def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
+    """One (workload, Lkv) point: the timed lvx (or ring) fwd+bwd steps, the
+    dominant kernel's roofline, the no-comm A/B and the Ring baseline at
+    N > 1, and (``head``) the end-to-end host-buffer leg."""
+    import torch
     from paper_2502_02406_b200 import _lib, volumes
     from paper_2502_02406_b200.strategies import (RoundTrace, ShardSpec, lvx_backward,
                                                   lvx_forward, ring_backward, ring_forward)
-
-    s_q, s_kv, hq, hkv, d = CFG["s_q"], args.skv, CFG["hq"], CFG["hkv"], CFG["d"]
+    world, rank, local, dev = env.world, env.rank, env.local, env.dev
+    s_q, hq, hkv, d = CFG["s_q"], CFG["hq"], CFG["hkv"], CFG["d"]
     scale = 1.0 / d ** 0.5
     shards = ShardSpec.balanced(s_q, s_kv, world)
     qa, qb = shards.q_ranges[rank]
@@ -231,8 +327,6 @@ def native_arm(args):
 
     q_i, k_i, v_i, do_i = rnd(hq, qb - qa, d), rnd(hkv, kb - ka, d), rnd(hkv, kb - ka, d), \
         rnd(hq, qb - qa, d)
-    ctx = lvx.DeviceContext(rank, world, group=group, device=dev)
-    ctx_nc = lvx.DeviceContext(rank, world, group=group, device=dev, comm_enabled=False)
     fwd, bwd = (lvx_forward, lvx_backward) if args.strategy == "lvx" else \
         (ring_forward, ring_backward)
 
@@ -253,8 +347,7 @@ def native_arm(args):
         for _ in range(warm):
             step(c, strategy=strategy)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        env.barrier()
         traces = []
         launches0 = _lib.load().lvx_kernel_launches()
         w0 = time.time()
@@ -268,18 +361,13 @@ def native_arm(args):
             cs.mark(w0, time.time())
             time.sleep(0.15)
             cs.__exit__()
-        if world > 1:
-            dist.barrier()
+        env.barrier()
         launches = _lib.load().lvx_kernel_launches() - launches0
         ms = e0.elapsed_time(e1) / steps
         for tf, tb in traces:
             tf.resolve()
             tb.resolve()
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
-        return ms, traces, launches, (cs.summary() if cs else None)
+        return env.max_over_ranks(ms), traces, launches, (cs.summary() if cs else None)
 
     ms, traces, launches, clocks = timed(ctx, args.steps, args.warmup, sampler=True)
     flops = volumes.attention_flops(s_q, s_kv, hq, d)
@@ -295,7 +383,7 @@ def native_arm(args):
     unit = qrows * kvrows * hq * d                      # one (q block, kv shard) pair
     phases = {"fwd_kernel": sec(tfs, "fwd_kernel"), "fwd_finish": sec(tfs, "fwd_finish"),
               "fwd_wait": sec(tfs, "wait"), "dq_kernel": sec(tbs, "dq_kernel"),
-              "dq_finish": sec(tbs, "dq_finish"), "bwd_gather_wait": sec(tbs, "gather+wait"),
+              "dq_finish": sec(tbs, "dq_finish"), "bwd_wait": sec(tbs, "wait"),
               "dkv_kernel": sec(tbs, "dkv_kernel")}
     # algorithmic FLOP per launch (PAPER.md:67 split by product): fwd 4 units per
     # round; dQ kernel 2 (dS K) + the S, dP it recomputes are counted in dkv;
@@ -330,7 +418,8 @@ def native_arm(args):
         peak_kind = f"{pk_kind} bf16 sustained (kernel timed inside a long step)"
     traffic, traffic_src = None, None
     tj = ROOT / "profiles" / "r01b_traffic.json"
-    if world == 1 and args.strategy == "lvx" and args.skv == CFG["s_kv"] and tj.exists():
+    if world == 1 and args.strategy == "lvx" and args.workload == "c2" and \
+            s_kv == WORKLOADS["c2"]["s_kv"] and tj.exists():
         # ncu DRAM bytes per launch of this kernel at this exact launch shape
         rec = json.loads(tj.read_text())["per_launch"].get(kname)
         if rec:
@@ -354,11 +443,11 @@ def native_arm(args):
     w = volumes.Wire.b200(hq, hkv, d, 2)
     model = (volumes.bytes_by_worker(args.strategy, "forward", shards.q_sizes, shards.kv_sizes, w)[rank]
              + volumes.bytes_by_worker(args.strategy, "backward", shards.q_sizes, shards.kv_sizes, w)[rank])
-    comm = {"bytes_per_step_rank0": sent, "closed_form_rank0": model,
+    comm = {"transport": ctx.transport_kind,
+            "bytes_per_step_rank0": sent, "closed_form_rank0": model,
             "paper_q_plus_o_hop_bytes_bf16": volumes.paper_hop_bytes(s_q, world, hq, d, 2),
             "measured_fwd_hop_bytes": (tf0.rounds[0].sent_bytes if world > 1 else 0),
             "exposed_comm_ms_per_step": sum(r.comm_seconds for r in tf0.rounds + tb0.rounds) * 1e3}
-    out_phases_nc = None
 
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_layer": ms,
@@ -367,29 +456,27 @@ def native_arm(args):
            "config": {**CFG, "s_kv": s_kv, "strategy": args.strategy,
                       "parallelism": f"kv-seq-parallel x{world} (query rotation)"
                       if args.strategy == "lvx" else f"kv-rotation x{world}",
-                      "l2": "inputs larger than L2 (K/V shard >= 512 MiB per rank)"},
+                      "l2": "inputs larger than L2 (K/V shard >= 16 MiB per rank and the "
+                            "step touches > 126 MB)"},
            "roofline": roofline, "comm": comm, "clocks": clocks,
            "gpu_launches": int(launches)}
 
     # --- no-communication arm and the Ring baseline
     if world > 1:
-        # no-communication arm: the identical schedule with every
-        # hop skipped.  Measured as interleaved A/B step pairs so power-cap and
-        # clock drift hit both arms equally; also reported from a separate block.
+        # the identical schedule with every hop skipped, measured as interleaved
+        # A/B step pairs so power-cap and clock drift hit both arms equally
         pairs = max(3, args.steps)
         a_ms, b_ms = [], []
         for _ in range(pairs):
             for c, acc in ((ctx, a_ms), (ctx_nc, b_ms)):
                 torch.cuda.synchronize()
-                dist.barrier()
+                env.barrier()
                 ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ea.record()
                 step(c)
                 eb.record()
                 torch.cuda.synchronize()
-                t = torch.tensor([ea.elapsed_time(eb)], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                acc.append(t.item())
+                acc.append(env.max_over_ranks(ea.elapsed_time(eb)))
         ms_a, ms_b = statistics.median(a_ms), statistics.median(b_ms)
         out["no_comm_ms_per_step"] = ms_b
         out["overhead_vs_no_comm"] = ms_a / ms_b - 1.0
@@ -407,6 +494,8 @@ def native_arm(args):
             out["ring_baseline"] = {"ms_per_step": ms_ring,
                                     "value": flops / (ms_ring * 1e-3) / 1e12,
                                     "speedup_lvx_over_ring": ms_ring / ms,
+                                    "schedule": "K/V sent at the start of each round, dK/dV "
+                                                "partials one hop behind (overlapped)",
                                     "bytes_per_step_rank0": rtr[0][0].total_sent_bytes()
                                     + rtr[0][1].total_sent_bytes()}
     else:
@@ -414,20 +503,125 @@ def native_arm(args):
         out["overhead_vs_no_comm"] = 0.0
 
     # --- end to end through the host-buffer API (pinned host -> HBM -> host)
-    if not args.no_e2e:
+    if head and not args.no_e2e:
         out["e2e"] = e2e_arm(args, ctx, shards, (q_i, k_i, v_i, do_i), scale, fwd, bwd, flops,
                              world, dev)
+    return out
 
-    # --- CPU reference on the host cores (rank 0, N=1 only)
-    if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample, threads = cpu_reference_rate()
-        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": threads,
-                               "kind": "port", "sample": sample}
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+
+def cpu_c1_timing(reps: int = 3) -> dict:
+    """BASELINE configs[0] exactly (Lq 128, Lkv 4096, 8 heads, d 64, fp32,
+    simulated world_size 2): the oracle port of lvx fwd+bwd at 1 BLAS
+    thread and at all host threads, best of ``reps`` each."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import lvx_oracle as orc
+    Q, K, V, dO = (t.astype(np.float32) for t in orc.make_inputs(128, 4096, 8, 64, seed=1))
+    out = {"config": "C1: Lq 128, Lkv 4096, h 8, d 64, fp32, n 2 (oracle port of the "
+                     "reference's lvx fwd+bwd)", "cpu_count": os.cpu_count()}
+    for key, threads in (("ms_1_thread", 1), ("ms_all_threads", os.cpu_count())):
+        with threadpool_limits(limits=threads, user_api="blas"):
+            best = float("inf")
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                orc.simulate("lvx", Q, K, V, dO, n=2)
+                best = min(best, time.perf_counter() - t0)
+        out[key] = best * 1e3
+    return out
+
+
+def layer_arm(args, env):
+    """C4: ``layers`` OpenFlamingo cross-attention layers sharing ONE copy of
+    the visual tokens y, RECOMPUTE_KV (K/V re-projected from y in the
+    backward), lvx over the ranks.  A step = forward through all layers, then
+    backward through them in reverse.  value = algorithmic TFLOP/s of the
+    whole step: attention (14 Lq Lkv hq d per layer) + every projection GEMM
+    (Q, K/V, O forward; the K/V recompute; dX, dY and weight gradients)."""
+    import torch
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import _lib, volumes
+    from paper_2502_02406_b200.recompute import (ActivationPolicy, CrossAttentionWeights,
+                                                 OpCounter, ca_backward, ca_forward)
+    world, rank, dev = env.world, env.rank, env.dev
+    s_q, s_kv, hq, hkv, d = CFG["s_q"], CFG["s_kv"], CFG["hq"], CFG["hkv"], CFG["d"]
+    e, nl = CFG["d_embed"], CFG["layers"]
+    sh = lvx.ShardSpec.balanced(s_q, s_kv, world)
+    (qa, qb), (ka, kb) = sh.q_ranges[rank], sh.kv_ranges[rank]
+    g = torch.Generator(device=dev).manual_seed(77)
+
+    def r(*shape, sc=1.0):
+        return ((torch.rand(*shape, device=dev, generator=g) * 2 - 1) * sc).bfloat16()
+    ws = 0.5 / e ** 0.5
+    layers = [CrossAttentionWeights(r(e, hq * d, sc=ws), r(e, hkv * d, sc=ws),
+                                    r(e, hkv * d, sc=ws), r(hq * d, e, sc=ws), hq, hkv)
+              for _ in range(nl)]
+    x0, y, go = r(qb - qa, e), r(kb - ka, e), r(qb - qa, e)
+    ctx = lvx.DeviceContext(rank, world, group=env.group, device=dev)
+
+    def step(policy, counter=None):
+        x, saved = x0, []
+        for w in layers:
+            x, sv = ca_forward(ctx, sh, x, y, w, policy)
+            saved.append(sv)
+        gx, dy = go, torch.zeros_like(y, dtype=torch.float32)
+        for w, sv in zip(reversed(layers), reversed(saved)):
+            gr = ca_backward(ctx, sh, gx, sv, y, w, counter=counter, group=env.group)
+            gx = gr.d_x
+            dy += gr.d_y
+        return gx, dy
+
+    def timed(policy, steps, warm, sampler=False):
+        for _ in range(warm):
+            step(policy)
+        torch.cuda.synchronize()
+        env.barrier()
+        cs = ClockSampler(env.local).__enter__() if sampler else None
+        l0 = _lib.load().lvx_kernel_launches()
+        w0 = time.time()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step(policy)
+        e1.record()
+        torch.cuda.synchronize()
+        if cs:
+            cs.mark(w0, time.time())
+            time.sleep(0.15)
+            cs.__exit__()
+        env.barrier()
+        return env.max_over_ranks(e0.elapsed_time(e1) / steps), \
+            _lib.load().lvx_kernel_launches() - l0, (cs.summary() if cs else None)
+
+    cnt = OpCounter()
+    step(ActivationPolicy.RECOMPUTE_KV, cnt)       # counts the recompute FLOP (per rank)
+    ms, launches, clocks = timed(ActivationPolicy.RECOMPUTE_KV, args.steps, args.warmup, True)
+    ms_store, _, _ = timed(ActivationPolicy.STORE_KV, max(2, args.steps // 2), 1)
+    att = volumes.attention_flops(s_q, s_kv, hq, d) * nl
+    # projections per layer: fwd Q (2 sq e hq d), K+V (2 * 2 skv e hkv d), O
+    # (2 sq hq d e); bwd: recompute K+V, Q re-projection, dX / dW for Q, K, V, O
+    proj_fwd = 2 * s_q * e * hq * d * 2 + 2 * 2 * s_kv * e * hkv * d
+    proj_bwd = (2 * 2 * s_kv * e * hkv * d + 2 * s_q * e * hq * d      # recompute K/V, Q
+                + 2 * (2 * 2 * s_q * e * hq * d)                         # dX, dW of Q and O
+                + 2 * (2 * 2 * s_kv * e * hkv * d))                      # dY, dW of K and V
+    total = att + nl * (proj_fwd + proj_bwd)
+    burst, sust, hbm, pk_kind, _ = peaks()
+    value = total / (ms * 1e-3) / 1e12
+    return {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_layer": ms / nl, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (uniform[-1,1] activations, U[+-0.5/sqrt(e)] weights)",
+            "config": {**CFG, "policy": "recompute", "parallelism": f"kv-seq-parallel x{world}",
+                       "l2": "y shard + K/V larger than L2"},
+            "attention_tflops": att / (ms * 1e-3) / 1e12,
+            "flop_split": {"attention": att, "projections": nl * (proj_fwd + proj_bwd),
+                           "recompute_counted_per_rank": cnt.projection_flops},
+            "store_kv_ms_per_step": ms_store, "recompute_overhead": ms / ms_store - 1.0,
+            "roofline": {"kernel": "whole step (attention + projection GEMMs)",
+                         "bound": "tensor", "achieved": value, "peak": sust,
+                         "unit": "TFLOP/s", "frac": value / sust, "traffic": None,
+                         "peak_kind": f"{pk_kind} bf16 sustained"},
+            "clocks": clocks, "gpu_launches": int(launches)}
 
 
 def _bwd_is_tc(q, k):

@@ -166,16 +166,25 @@ int lvx_accumulate(const lvx_view* src, const lvx_view* dst, void* stream);
 int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
 
 /* ---- projections (SURVEY.md §8(b) lvx_kv_recompute / lvx_project_bwd) --
- * Plain GEMMs on cuBLAS (bf16 in / fp32 accumulate; f32 without TF32; f64).
- * Row-major matrices; strides in elements; all operands one dtype.  These
- * entry points keep one cuBLAS handle per device (created on first use,
- * calls serialised by a mutex) and use cuBLAS's own workspace. */
+ * GEMMs on the library's own tcgen05 kernel (bf16 in, fp32 accumulate, bf16
+ * out; row strides multiple of 8 elements, 16-byte aligned bases) or its
+ * exact SIMT kernel (f32 / f64, and bf16 views TMA cannot describe).
+ * Row-major matrices; strides in elements; all operands one dtype.  Tall-K
+ * products with few output tiles split K across the SMs and reduce in fp32
+ * scratch from the stream-ordered allocator (cudaMallocAsync on `stream`). */
 typedef struct lvx_matrix {
   void* data;
   int64_t rows, cols, row_stride;
   int32_t dtype, _pad;
 } lvx_matrix;
 
+/* General GEMM of the layer's projections: c (+)= op(a) op(b), row-major
+ * matrices, op = transpose when ta / tb.  bf16 runs on the tcgen05 kernel
+ * (fp32 accumulate), f32 / f64 on an exact SIMT kernel.  Used for the output
+ * projection W_O of the cross-attention block (mllm.py:297-301 forward,
+ * :343-351 backward); the three calls below are special cases of it. */
+int lvx_gemm(const lvx_matrix* a, int ta, const lvx_matrix* b, int tb, const lvx_matrix* c,
+             int accumulate, void* stream);
 /* project (kernels.py:227-235): out[h] = x [S, e] @ w[:, h*d:(h+1)*d] for every
  * head of the [heads, S, d] view out.  out->head_stride == d (heads are column
  * blocks of one [S, heads*d] matrix) is one GEMM; any other head stride one

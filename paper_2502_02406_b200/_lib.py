@@ -24,7 +24,7 @@ EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eli
            "lvx_row_stats", "lvx_blockwise_bwd_workspace", "lvx_blockwise_bwd",
            "lvx_fill_empty_state", "lvx_convert", "lvx_bwd_workspace", "lvx_bwd_dq_partial",
            "lvx_bwd_dq_finish", "lvx_bwd_dkv", "lvx_project", "lvx_project_bwd",
-           "lvx_kv_recompute", "lvx_accumulate", "lvx_peer_create", "lvx_peer_destroy",
+           "lvx_kv_recompute", "lvx_gemm", "lvx_accumulate", "lvx_peer_create", "lvx_peer_destroy",
            "lvx_peer_base", "lvx_peer_handle_bytes", "lvx_peer_export", "lvx_peer_open",
            "lvx_peer_attach", "lvx_peer_put", "lvx_peer_signal", "lvx_peer_wait")
 
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "lvx_project": (i32, [M, M, P, vp]),
         "lvx_project_bwd": (i32, [M, M, P, M, M, vp]),
         "lvx_kv_recompute": (i32, [M, M, M, P, P, vp]),
+        "lvx_gemm": (i32, [M, i32, M, i32, M, i32, vp]),
         "lvx_accumulate": (i32, [P, P, vp]),
         "lvx_peer_create": (i32, [u64, i32, i32, ctypes.POINTER(vp)]),
         "lvx_peer_destroy": (i32, [vp]),

@@ -67,7 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     (BUILD / "ptxas.log").write_text("\n".join(log))
     tmp = LIB.with_suffix(".so.tmp")
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
-            *[str(o) for _, o, _ in results], "-cudart", "static", "-lcublas"]
+            *[str(o) for _, o, _ in results], "-cudart", "static"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stderr)

@@ -218,11 +218,11 @@ class ThreadGroup:
     def rank(self, r: int) -> "ThreadRank":
         return ThreadRank(self, r)
 
-    def _wait(self, rank: int) -> None:
+    def _wait(self, rank: int, timeout: float | None = None) -> None:
         if self.first_failure is not None:
             raise ClusterAborted(f"worker {rank}: group aborted")
         try:
-            self._barrier.wait(timeout=self.timeout)
+            self._barrier.wait(timeout=self.timeout if timeout is None else timeout)
         except threading.BrokenBarrierError:
             if self.first_failure is not None:
                 raise ClusterAborted(f"worker {rank}: group aborted") from None
@@ -253,11 +253,11 @@ class _Coll:
     def threaded(self) -> bool:
         return isinstance(self.group, ThreadRank)
 
-    def barrier(self) -> None:
+    def barrier(self, timeout: float | None = None) -> None:
         if self.n == 1:
             return
         if self.threaded:
-            self.group.group._wait(self.rank)
+            self.group.group._wait(self.rank, timeout)
         else:
             dist.barrier(group=self.group)
 

@@ -2,6 +2,8 @@
 // conversion and warp reductions.  sm_100a only.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <atomic>
 #include <cuda_bf16.h>
@@ -124,6 +126,25 @@ int tc_bwd_dq_finish(const lvx_view* q, const lvx_view* k, const lvx_view* dq, i
 int tc_bwd_dkv(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* L,
                const lvx_view* D, const lvx_view* dO, double scale, const lvx_view* dk,
                const lvx_view* dv, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// GEMMs (lvx_gemm_sm100.cu): C[M, N] (+)= op(A) op(B), row-major storage;
+// op(A) = A^T when ta (A stored [K, M]), op(B) = B^T when tb (B stored [N, K]).
+struct GemmCall {
+  int32_t dtype;
+  int64_t M, N, K;
+  const void* a;
+  int64_t lda;
+  bool ta;
+  const void* b;
+  int64_t ldb;
+  bool tb;
+  void* c;
+  int64_t ldc;
+  bool accumulate;
+};
+int gemm(const GemmCall& g, cudaStream_t st);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (null if absent)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 
 // Raise a kernel's dynamic shared memory limit once per device: function
 // attributes belong to the device's context, so a process driving several

@@ -520,6 +520,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
+
 // bf16 [heads, rows, d] view -> 3-D TMA map with a (64, 128, 1) box, 128B swizzle.
 bool make_tma_3d(CUtensorMap* m, const lvx_view* v, int box_rows) {
   auto fn = encode_fn();

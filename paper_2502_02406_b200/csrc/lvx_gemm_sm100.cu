@@ -1,0 +1,372 @@
+// GEMMs of the cross-attention layer's projections on B200: the K/V
+// recompute from the shared visual tokens (mllm.py:296-300, :358-360), the
+// Q / O projections and their backward (kernels.py:227-254).
+//
+//   C[M, N] (+)= op(A)[M, K] op(B)[K, N]   row-major storage, bf16 in,
+//                                          fp32 accumulate, bf16 out
+//
+// tcgen05 kernel (bf16): persistent, one CTA per SM, 128 x 256 output tiles,
+// 64-deep K blocks in a 4-stage TMA ring (48 KB per stage, 128-byte swizzle),
+// fp32 accumulators double-buffered in TMEM (2 x 256 columns) so the
+// epilogue of tile t overlaps the main loop of tile t+1.  Warp roles:
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMA-fed MMA issuer, M = 128, N = 256, K = 16 per instruction
+//   warps 2-5   epilogue: tcgen05.ld of their 32-lane quadrant, bf16 pack,
+//               16-byte stores (or fp32 reduce-adds for split-K partials)
+// Operand majors come from the transposes, so no operand is ever copied:
+//   A not transposed: stored [M, K] -> K-major tile (one 128 x 64 box)
+//   A transposed:     stored [K, M] -> MN-major tile (two 64 x 64 boxes)
+//   B not transposed: stored [K, N] -> MN-major tile (four 64 x 64 boxes)
+//   B transposed:     stored [N, K] -> K-major tile (one 256 x 64 box)
+// Tall-K products with few output tiles (weight gradients x^T dOut over the
+// rank's visual rows) split K so every SM gets work; the partials are
+// reduce-added in fp32 (red.global.add.v4.f32) into stream-ordered scratch
+// and converted once.
+//
+// Exact SIMT kernel for f32 / f64 (and bf16 views TMA cannot describe): one
+// output element per thread, accumulated in fp32 (bf16, f32) or f64.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "lvx_common.cuh"
+#include "lvx_sm100.cuh"
+
+namespace lvx {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+
+struct GemmParams {
+  int M, N, K;
+  int m_tiles, n_tiles, kb_total, kb_per_split, splits, units;
+  __nv_bfloat16* C;
+  int64_t ldc;
+  float* Cf;          // split-K fp32 partial sums ([M, N], ld N), else null
+  int accumulate;     // bf16 C += A B
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto decode = [&](int u, int& m0, int& n0, int& kb0, int& kb1) {
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int split = u / tiles, t = u % tiles;
+    m0 = (t / p.n_tiles) * BM;       // N fastest: one A row band meets every B tile in L2
+    n0 = (t % p.n_tiles) * BN;
+    kb0 = split * p.kb_per_split;
+    kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      int it = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int m0, n0, kb0, kb1;
+        decode(u, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint8_t* sa = sm + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_3d(sa, &tmA, &full[s], k0, m0, 0);
+          } else {
+            tma_load_3d(sa, &tmA, &full[s], m0, k0, 0);
+            tma_load_3d(sa + 8192, &tmA, &full[s], m0 + 64, k0, 0);
+          }
+          if (!B_MN) {
+            tma_load_3d(sb, &tmB, &full[s], k0, n0, 0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, k0, 0);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    const uint32_t base = smem_u32(sm);
+    int it = 0, lt = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+      int m0, n0, kb0, kb1;
+      decode(u, m0, n0, kb0, kb1);
+      const int buf = lt & 1;
+      if (lt >= 2) mbar_wait(&acc_empty[buf], ((lt >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + buf * BN;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = base + s * STAGE_BYTES, sb = sa + A_BYTES;
+          const uint64_t da = A_MN ? umma_desc_sw128(sa, 8192, 1024) : umma_desc_sw128(sa, 0, 1024);
+          const uint64_t db = B_MN ? umma_desc_sw128(sb, 8192, 1024) : umma_desc_sw128(sb, 0, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major: 16 elements = 32 bytes along the swizzled row;
+            // MN-major: 16 K rows of 128 bytes
+            const uint64_t oa = A_MN ? (uint64_t)((kk * 16 * 128) >> 4) : (uint64_t)((kk * 32) >> 4);
+            const uint64_t ob = B_MN ? (uint64_t)((kk * 16 * 128) >> 4) : (uint64_t)((kk * 32) >> 4);
+            mma_bf16_ss(acc, da + oa, db + ob, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          if (kb + 1 == kb1) mma_commit(&acc_full[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;                  // TMEM lane quadrant of this warp
+    int lt = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++lt) {
+      int m0, n0, kb0, kb1;
+      decode(u, m0, n0, kb0, kb1);
+      const int buf = lt & 1;
+      mbar_wait(&acc_full[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_wait_ld();
+        const int col0 = n0 + c * 32;
+        if (row >= p.M || col0 >= p.N) continue;
+        if (p.Cf) {
+          float* dst = p.Cf + (int64_t)row * p.N + col0;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (col0 + 4 * g < p.N)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
+                           "f"(__uint_as_float(r[4 * g])), "f"(__uint_as_float(r[4 * g + 1])),
+                           "f"(__uint_as_float(r[4 * g + 2])), "f"(__uint_as_float(r[4 * g + 3]))
+                           : "memory");
+        } else {
+          __nv_bfloat16* dst = p.C + (int64_t)row * p.ldc + col0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (col0 + 8 * g >= p.N) break;
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * g + e]);
+            uint4* d4 = reinterpret_cast<uint4*>(dst + 8 * g);
+            if (p.accumulate) {
+              const uint4 old = *d4;
+              const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+                v[2 * e] += __bfloat162float(o2.x);
+                v[2 * e + 1] += __bfloat162float(o2.y);
+              }
+            }
+            *d4 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                             pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// split-K finish: C (+)= bf16(Cf)
+__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
+                                     __nv_bfloat16* __restrict__ C, int64_t ldc, int accumulate) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int64_t r = i / N, c = i % N;
+  float v = Cf[i];
+  if (accumulate) v += __bfloat162float(C[r * ldc + c]);
+  C[r * ldc + c] = __float2bfloat16_rn(v);
+}
+
+// ---------------------------------------------------------------- SIMT
+// One output element per thread; op(A)[m, k] = A[m * lda + k] or A[k * lda + m].
+template <typename T, typename Acc>
+__global__ void gemm_simt_kernel(const T* __restrict__ A, int64_t lda, bool ta,
+                                 const T* __restrict__ B, int64_t ldb, bool tb, T* __restrict__ C,
+                                 int64_t ldc, int64_t M, int64_t N, int64_t K, bool accumulate) {
+  constexpr int TS = 16;
+  __shared__ Acc sa[TS][TS + 1], sb[TS][TS + 1];
+  const int64_t m = (int64_t)blockIdx.y * TS + threadIdx.y;
+  const int64_t n = (int64_t)blockIdx.x * TS + threadIdx.x;
+  Acc acc = 0;
+  for (int64_t k0 = 0; k0 < K; k0 += TS) {
+    const int64_t ka = k0 + threadIdx.x, kb = k0 + threadIdx.y;
+    const int64_t mA = (int64_t)blockIdx.y * TS + threadIdx.y;
+    sa[threadIdx.y][threadIdx.x] =
+        (mA < M && ka < K) ? to_acc<Acc>(ta ? A[ka * lda + mA] : A[mA * lda + ka]) : Acc(0);
+    sb[threadIdx.y][threadIdx.x] =
+        (n < N && kb < K) ? to_acc<Acc>(tb ? B[n * ldb + kb] : B[kb * ldb + n]) : Acc(0);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < TS; ++k) acc += sa[threadIdx.y][k] * sb[k][threadIdx.x];
+    __syncthreads();
+  }
+  if (m < M && n < N) {
+    T* c = C + m * ldc + n;
+    *c = from_acc<T>(accumulate ? acc + to_acc<Acc>(*c) : acc);
+  }
+}
+
+template <typename T, typename Acc>
+int launch_simt(const GemmCall& g, cudaStream_t st) {
+  dim3 block(16, 16), grid((unsigned)((g.N + 15) / 16), (unsigned)((g.M + 15) / 16));
+  if (grid.y > 65535) return LVX_EUNSUPPORTED;
+  gemm_simt_kernel<T, Acc><<<grid, block, 0, st>>>(
+      static_cast<const T*>(g.a), g.lda, g.ta, static_cast<const T*>(g.b), g.ldb, g.tb,
+      static_cast<T*>(g.c), g.ldc, g.M, g.N, g.K, g.accumulate);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+// 2-D bf16 map of a row-major [rows, cols] matrix (leading dimension ld),
+// box (64 columns, box_rows rows), 128-byte swizzle
+bool map2d(CUtensorMap* m, const void* p, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  auto fn = tensor_map_encoder();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * (cuuint64_t)rows};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(p), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tc_ok(const GemmCall& g) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return g.dtype == LVX_BF16 && is_sm100() && g.M > 0 && g.N > 0 && g.K > 0 && al16(g.a) &&
+         al16(g.b) && al16(g.c) && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0 &&
+         g.N % 8 == 0 && g.M < (1ll << 31) && g.N < (1ll << 31) && g.K < (1ll << 31);
+}
+
+template <bool A_MN, bool B_MN>
+int launch_tc(const GemmCall& g, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  // A: [M, K] K-major box 128 rows; [K, M] MN-major boxes of 64 K rows
+  const bool okA = A_MN ? map2d(&ta, g.a, g.K, g.M, g.lda, 64) : map2d(&ta, g.a, g.M, g.K, g.lda, 128);
+  const bool okB = B_MN ? map2d(&tb, g.b, g.K, g.N, g.ldb, 64) : map2d(&tb, g.b, g.N, g.K, g.ldb, 256);
+  if (!okA || !okB) return LVX_ECUDA;
+  GemmParams p{};
+  p.M = (int)g.M;
+  p.N = (int)g.N;
+  p.K = (int)g.K;
+  p.m_tiles = (int)((g.M + BM - 1) / BM);
+  p.n_tiles = (int)((g.N + BN - 1) / BN);
+  p.kb_total = (int)((g.K + BK - 1) / BK);
+  const int sms = device_sms();
+  const int tiles = p.m_tiles * p.n_tiles;
+  int splits = 1;
+  if (tiles < sms && p.kb_total >= 32)   // tall-K, few tiles: split K over the idle SMs
+    splits = std::min((2 * sms + tiles - 1) / tiles, p.kb_total / 16);
+  splits = std::max(1, splits);
+  p.kb_per_split = (p.kb_total + splits - 1) / splits;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.units = tiles * p.splits;
+  p.C = static_cast<__nv_bfloat16*>(g.c);
+  p.ldc = g.ldc;
+  p.accumulate = g.accumulate ? 1 : 0;
+  float* scratch = nullptr;
+  if (p.splits > 1) {
+    const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
+      return LVX_ECUDA;
+    if (cudaMemsetAsync(scratch, 0, bytes, st) != cudaSuccess) return LVX_ECUDA;
+    p.Cf = scratch;
+  }
+  auto kern = gemm_bf16_kernel<A_MN, B_MN>;
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(kern, GEMM_SMEM, attr_done)) return LVX_ECUDA;
+  kern<<<std::min(p.units, sms), GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+  note_launch();
+  if (scratch) {
+    const int64_t n = g.M * g.N;
+    splitk_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(scratch, p.M, p.N, p.C,
+                                                                      g.ldc, p.accumulate);
+    note_launch();
+    cudaFreeAsync(scratch, st);
+  }
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+}  // namespace
+
+int gemm(const GemmCall& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return LVX_OK;
+  if (g.K <= 0) {   // empty contraction: C = 0, or unchanged when accumulating
+    if (g.accumulate) return LVX_OK;
+    const size_t es = g.dtype == LVX_F64 ? 8 : (g.dtype == LVX_F32 ? 4 : 2);
+    return cudaMemset2DAsync(g.c, g.ldc * es, 0, g.N * es, g.M, st) == cudaSuccess ? LVX_OK
+                                                                                    : LVX_ECUDA;
+  }
+  if (tc_ok(g)) {
+    if (!g.ta && !g.tb) return launch_tc<false, true>(g, st);
+    if (!g.ta && g.tb) return launch_tc<false, false>(g, st);
+    if (g.ta && !g.tb) return launch_tc<true, true>(g, st);
+    return launch_tc<true, false>(g, st);
+  }
+  switch (g.dtype) {
+    case LVX_BF16: return launch_simt<__nv_bfloat16, float>(g, st);
+    case LVX_F32: return launch_simt<float, float>(g, st);
+    case LVX_F64: return launch_simt<double, double>(g, st);
+    default: return LVX_EDTYPE;
+  }
+}
+
+}  // namespace lvx

@@ -2,89 +2,38 @@
 // (reference kernels.py:227-254) and the MLLM K/V recompute from the shared
 // visual tokens (mllm.py:296-300 forward, :358-360 backward).
 //
-// These are plain GEMMs and run on cuBLAS (bf16 in, fp32 accumulate; f32 and
-// f64 without TF32).  The head layout is folded into the GEMM's leading
-// dimensions and batch strides, so [heads, S, d] outputs that are column
-// blocks of one [S, heads*d] matrix (head_stride == d: the layout the
-// recompute layer keeps) take ONE GEMM with N = heads*d, and any other
-// head stride takes one strided-batched GEMM over heads.  No copies.
-#include <cublas_v2.h>
+// The GEMMs run on the hand-written tcgen05 kernel of lvx_gemm_sm100.cu (bf16
+// in, fp32 accumulate) or its exact SIMT sibling (f32 / f64).  The head
+// layout is folded into the GEMM's leading dimensions, so [heads, S, d]
+// outputs that are column blocks of one [S, heads*d] matrix (head_stride == d:
+// the layout the recompute layer keeps) take ONE GEMM with N = heads*d; any
+// other head stride one GEMM per head.  No copies.
 #include <cuda_runtime.h>
-
-#include <mutex>
 
 #include "lvx_common.cuh"
 
 namespace lvx {
 namespace {
 
-constexpr int kMaxDevices = 64;
-
-// One cuBLAS handle per device, created on first use; calls are serialised
-// because a handle's stream binding is shared state.
-std::mutex g_mu;
-cublasHandle_t g_handle[kMaxDevices] = {};
-
-cublasHandle_t handle_for_current_device() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
-  if (!g_handle[dev]) {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    g_handle[dev] = h;
-  }
-  return g_handle[dev];
-}
-
-bool gemm_types(int32_t dt, cudaDataType_t* t, cublasComputeType_t* c) {
-  switch (dt) {
-    case LVX_BF16: *t = CUDA_R_16BF; *c = CUBLAS_COMPUTE_32F; return true;
-    case LVX_F32: *t = CUDA_R_32F; *c = CUBLAS_COMPUTE_32F_PEDANTIC; return true;
-    case LVX_F64: *t = CUDA_R_64F; *c = CUBLAS_COMPUTE_64F; return true;
-    default: return false;
-  }
-}
-
 size_t esize(int32_t dt) { return dt == LVX_F64 ? 8 : (dt == LVX_F32 ? 4 : 2); }
 
-// Row-major C[M,N] (ldc) = op(A)[M,K] op(B)[K,N] + beta C, batched with element
-// strides sA / sB / sC (batch 1 = plain GEMM).  Column-major cuBLAS sees the
-// transposes: C^T = op(B)^T op(A)^T.
-int gemm_rm(cublasHandle_t h, int32_t dt, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
+// Row-major C[M,N] (ldc) = op(A)[M,K] op(B)[K,N] (+ C), batched over `batch`
+// operand / output element strides sA / sB / sC (one launch per batch entry:
+// only views whose heads are not column blocks of one matrix get here).
+int gemm_rm(cudaStream_t st, int32_t dt, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
             const void* A, int64_t lda, int64_t sA, const void* B, int64_t ldb, int64_t sB,
             void* C, int64_t ldc, int64_t sC, int batch, bool accumulate) {
-  cudaDataType_t t;
-  cublasComputeType_t ct;
-  if (!gemm_types(dt, &t, &ct)) return LVX_EDTYPE;
-  if (M <= 0 || N <= 0 || batch <= 0) return LVX_OK;
-  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || lda > INT32_MAX || ldb > INT32_MAX ||
-      ldc > INT32_MAX)
-    return LVX_EUNSUPPORTED;
-  const float a32 = 1.f, b32 = accumulate ? 1.f : 0.f;
-  const double a64 = 1.0, b64 = accumulate ? 1.0 : 0.0;
-  const void* alpha = dt == LVX_F64 ? static_cast<const void*>(&a64) : &a32;
-  const void* beta = dt == LVX_F64 ? static_cast<const void*>(&b64) : &b32;
-  const cublasOperation_t opB = tb ? CUBLAS_OP_T : CUBLAS_OP_N;
-  const cublasOperation_t opA = ta ? CUBLAS_OP_T : CUBLAS_OP_N;
-  if (K == 0) {   // empty contraction: C = 0 (or unchanged when accumulating)
-    if (accumulate) return LVX_OK;
-    cudaStream_t st = nullptr;
-    cublasGetStream(h, &st);
-    for (int b = 0; b < batch; ++b)
-      if (cudaMemset2DAsync(static_cast<char*>(C) + (int64_t)b * sC * (int64_t)esize(dt),
-                            ldc * esize(dt), 0, N * esize(dt), M, st) != cudaSuccess)
-        return LVX_ECUDA;
-    return LVX_OK;
+  if (dt != LVX_BF16 && dt != LVX_F32 && dt != LVX_F64) return LVX_EDTYPE;
+  const int64_t es = (int64_t)esize(dt);
+  for (int b = 0; b < batch; ++b) {
+    GemmCall g{dt, M, N, K,
+               static_cast<const char*>(A) + b * sA * es, lda, ta,
+               static_cast<const char*>(B) + b * sB * es, ldb, tb,
+               static_cast<char*>(C) + b * sC * es, ldc, accumulate};
+    const int s = gemm(g, st);
+    if (s) return s;
   }
-  cublasStatus_t s;
-  if (batch == 1)
-    s = cublasGemmEx(h, opB, opA, (int)N, (int)M, (int)K, alpha, B, t, (int)ldb, A, t, (int)lda,
-                     beta, C, t, (int)ldc, ct, CUBLAS_GEMM_DEFAULT);
-  else
-    s = cublasGemmStridedBatchedEx(h, opB, opA, (int)N, (int)M, (int)K, alpha, B, t, (int)ldb,
-                                   sB, A, t, (int)lda, sA, beta, C, t, (int)ldc, sC, batch, ct,
-                                   CUBLAS_GEMM_DEFAULT);
-  return s == CUBLAS_STATUS_SUCCESS ? LVX_OK : LVX_ECUDA;
+  return LVX_OK;
 }
 
 bool mat_ok(const lvx_matrix* m) {
@@ -96,7 +45,7 @@ const char* at(const void* p, int64_t elems, int32_t dt) {
   return static_cast<const char*>(p) + elems * (int64_t)esize(dt);
 }
 
-int project_impl(cublasHandle_t h, const lvx_matrix* x, const lvx_matrix* w, const lvx_view* out) {
+int project_impl(cudaStream_t h, const lvx_matrix* x, const lvx_matrix* w, const lvx_view* out) {
   const int64_t heads = out->heads, S = x->rows, e = x->cols, d = out->d;
   if (w->rows != e || w->cols != heads * d || out->rows != S) return LVX_EINVAL;
   if (out->head_stride == d || heads == 1)   // [S, heads*d] column blocks: one GEMM
@@ -117,10 +66,7 @@ extern "C" {
 int lvx_project(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* out, void* stream) {
   if (!mat_ok(x) || !mat_ok(w) || !out || out->heads < 1 || out->d < 1) return LVX_EINVAL;
   if (x->dtype != w->dtype || x->dtype != out->dtype) return LVX_EDTYPE;
-  std::lock_guard<std::mutex> lk(g_mu);
-  cublasHandle_t h = handle_for_current_device();
-  if (!h || cublasSetStream(h, static_cast<cudaStream_t>(stream)) != CUBLAS_STATUS_SUCCESS)
-    return LVX_ECUDA;
+  cudaStream_t h = static_cast<cudaStream_t>(stream);
   return project_impl(h, x, w, out);
 }
 
@@ -132,10 +78,7 @@ int lvx_kv_recompute(const lvx_matrix* y, const lvx_matrix* w_k, const lvx_matri
     return LVX_EDTYPE;
   if (k_out->heads != v_out->heads || k_out->d != v_out->d || k_out->rows != v_out->rows)
     return LVX_EINVAL;
-  std::lock_guard<std::mutex> lk(g_mu);
-  cublasHandle_t h = handle_for_current_device();
-  if (!h || cublasSetStream(h, static_cast<cudaStream_t>(stream)) != CUBLAS_STATUS_SUCCESS)
-    return LVX_ECUDA;
+  cudaStream_t h = static_cast<cudaStream_t>(stream);
   const int64_t hd = k_out->heads * k_out->d;
   const int32_t dt = y->dtype;
   // [W_K | W_V] adjacent in one weight and K | V adjacent in one [S, 2 hkv d]
@@ -164,10 +107,7 @@ int lvx_project_bwd(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* do
   if (dout->rows != S || w->rows != e || w->cols != heads * d || dx->rows != S ||
       dx->cols != e || dw->rows != e || dw->cols != heads * d)
     return LVX_EINVAL;
-  std::lock_guard<std::mutex> lk(g_mu);
-  cublasHandle_t h = handle_for_current_device();
-  if (!h || cublasSetStream(h, static_cast<cudaStream_t>(stream)) != CUBLAS_STATUS_SUCCESS)
-    return LVX_ECUDA;
+  cudaStream_t h = static_cast<cudaStream_t>(stream);
   const bool flat = dout->head_stride == d || heads == 1;
   int s;
   // dX = dOut_flat W^T (kernels.py:250)
@@ -192,3 +132,15 @@ int lvx_project_bwd(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* do
 }
 
 }  // extern "C"
+
+extern "C" int lvx_gemm(const lvx_matrix* a, int ta, const lvx_matrix* b, int tb,
+                        const lvx_matrix* c, int accumulate, void* stream) {
+  if (!mat_ok(a) || !mat_ok(b) || !mat_ok(c)) return LVX_EINVAL;
+  if (a->dtype != b->dtype || a->dtype != c->dtype) return LVX_EDTYPE;
+  const int64_t M = ta ? a->cols : a->rows, K = ta ? a->rows : a->cols;
+  const int64_t Kb = tb ? b->cols : b->rows, N = tb ? b->rows : b->cols;
+  if (K != Kb || c->rows != M || c->cols != N) return LVX_EINVAL;
+  GemmCall g{a->dtype, M, N, K, a->data, a->row_stride, ta != 0, b->data, b->row_stride,
+             tb != 0, c->data, c->row_stride, accumulate != 0};
+  return gemm(g, static_cast<cudaStream_t>(stream));
+}

@@ -142,6 +142,8 @@ class HostLayerPipeline:
         pending = {0: self._issue_h2d(steps[0], self._slots[0], bounds)}
         for s, st in enumerate(steps):
             slot = self._slots[s % nslots]
+            if s not in pending:   # one slot: this step's copies wait for the last step's release
+                pending[s] = self._issue_h2d(st, slot, bounds)
             evs = pending.pop(s)
             if nslots == 2 and s + 1 < len(steps):   # prefetch behind this step's copies
                 pending[s + 1] = self._issue_h2d(steps[s + 1], self._slots[(s + 1) % 2], bounds)
@@ -159,8 +161,9 @@ class HostLayerPipeline:
             dq, _, _ = lvx_backward(self.ctx, self.shards, slot.q, slot.k, slot.v, state,
                                     slot.do, self.scale, kv_stream=stream)
             self._d2h(st.dq, dq)
-            if nslots == 2:   # step s+2's copies into this slot wait for this
-                slot.free = torch.cuda.Event()
-                slot.free.record(cur)
+            # the next copies into this slot (step s+1 with one slot, s+2 with
+            # two) wait until this step's kernels have read it
+            slot.free = torch.cuda.Event()
+            slot.free.record(cur)
         self.d2h.synchronize()
         cur.synchronize()

@@ -357,7 +357,7 @@ def dense_attention_backward(Q, K, V, O, L, dO, scale: float | None = None) -> G
 
 
 # ---------------------------------------------------------------------------
-# projections — kernels.py:227-254 (cuBLAS GEMMs through torch.matmul)
+# projections — kernels.py:227-254 (the library's tcgen05 GEMM, lvx_gemm_sm100.cu)
 # ---------------------------------------------------------------------------
 
 def project(x, W, heads: int):
@@ -405,6 +405,14 @@ def project_backward_into(x: torch.Tensor, W: torch.Tensor, d_out: torch.Tensor,
     _lib.check("lvx_project_bwd", _lib.load().lvx_project_bwd(
         _lib.matrix(x), _lib.matrix(W), _lib.view(d_out), _lib.matrix(dx), _lib.matrix(dw),
         _lib.stream_ptr(x.device)))
+
+
+def gemm_into(a: torch.Tensor, ta: bool, b: torch.Tensor, tb: bool, c: torch.Tensor,
+              accumulate: bool = False) -> None:
+    """c (+)= op(a) op(b) for row-major device matrices (lvx_gemm)."""
+    L = _lib.load()
+    _lib.check("lvx_gemm", L.lvx_gemm(_lib.matrix(a), int(ta), _lib.matrix(b), int(tb),
+                                      _lib.matrix(c), int(accumulate), _lib.stream_ptr(c.device)))
 
 
 def project_backward(x, W, dOut):

@@ -32,8 +32,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from .comm import (ClusterAborted, ClusterSpec, CollectiveTimeout, DeviceContext, ThreadGroup,
-                   TransportStats, WorkerFailed, resolve_timeout)
+from .comm import (ClusterAborted, ClusterSpec, CollectiveTimeout, DeviceContext, PeerTransport,
+                   ThreadGroup, TransportStats, WorkerFailed, resolve_timeout)
 
 
 def free_port() -> int:
@@ -89,7 +89,11 @@ def spawn_ranks(spec: ClusterSpec, body, timeout: float | None = None, device=No
         ctxs[rank] = ctx
         results[rank] = body(ctx)
         ctx.synchronize()
-        ctx.barrier()      # no rank frees its arena while a peer still writes into it
+        if isinstance(ctx.transport, PeerTransport):
+            # no rank frees its arena while a peer may still write into it; the
+            # deadline is longer than a hop's so a peer's own timeout (the
+            # root cause) is the failure reported
+            ctx.coll.barrier(timeout=2 * tmo + 5)
         ctx.close()
 
     if n == 1:

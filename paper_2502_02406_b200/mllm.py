@@ -216,23 +216,20 @@ def max_frames_under_budget(config: ToyMllmConfig, policy: ActivationPolicy, bud
     if budget_bytes <= 0:
         raise ValueError(f"budget must be positive, got {budget_bytes}")
 
-    def peak(frames: int) -> int:
-        return analytic_ledger(replace(config, frames=frames), policy, n).peak_total
+    def fits(frames: int) -> bool:
+        return analytic_ledger(replace(config, frames=frames), policy, n).peak_total <= \
+            budget_bytes
 
-    if peak(0) > budget_bytes:
+    if not fits(0):
         return 0
-    lo, hi = 0, 1
-    while peak(hi) <= budget_bytes:
-        lo, hi = hi, hi * 2
-        if hi > 2 ** 60:
-            raise ValueError("budget admits an absurd frame count; check inputs")
-    while hi - lo > 1:
-        mid = (lo + hi) // 2
-        if peak(mid) <= budget_bytes:
-            lo = mid
-        else:
-            hi = mid
-    return lo
+    if fits(1 << 60):
+        raise ValueError("budget admits an absurd frame count; check inputs")
+    # the peak grows with the frame count: set the answer's bits high to low
+    frames = 0
+    for bit in range(59, -1, -1):
+        if fits(frames | (1 << bit)):
+            frames |= 1 << bit
+    return frames
 
 
 @dataclass

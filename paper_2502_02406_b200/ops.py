@@ -74,6 +74,11 @@ class CudaOps:
             K._lib.check("lvx_accumulate", K._lib.load().lvx_accumulate(
                 K._lib.view(src), K._lib.view(dst), K._lib.stream_ptr(dst.device)))
 
+    def gemm(self, a, ta, b, tb, out, accumulate=False) -> None:
+        """out (+)= op(a) op(b) (lvx_gemm)."""
+        if out.numel():
+            K.gemm_into(a, ta, b, tb, out, accumulate)
+
     def kv_recompute(self, y, w_k, w_v, k_out, v_out) -> None:
         """k_out / v_out ([hkv, S, d] views) = project(y, W_K / W_V) (lvx_kv_recompute)."""
         if y.shape[0]:

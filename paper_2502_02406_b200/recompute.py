@@ -17,9 +17,9 @@ the weights are replicated.  Every projection is row-local, so:
             partial sums over the rank's rows and are all-reduced (the
             reference is single-worker, so this collective is new).
 
-The projection GEMMs run on cuBLAS behind the C ABI (``lvx_kv_recompute``,
-``lvx_project_bwd``; plain library GEMMs, heads folded into the GEMM strides);
-the output projection W_O stays a torch matmul.  Fusing the K/V recompute into
+Every projection GEMM runs on the library's own tcgen05 GEMM behind the C ABI
+(``lvx_kv_recompute``, ``lvx_project_bwd``, and ``lvx_gemm`` for W_Q / W_O;
+heads folded into the GEMM strides, no copies).  Fusing the K/V recompute into
 the attention kernels' producer is the next step.  ``OpCounter`` counts forward-direction projection FLOP
 done inside the backward, like ``src/mllm.py:242-253``.
 """
@@ -104,6 +104,25 @@ def _flat(t: torch.Tensor) -> torch.Tensor:
     return t.transpose(0, 1).reshape(s, h * d)
 
 
+def _mm(ctx: DeviceContext, a: torch.Tensor, b: torch.Tensor, ta: bool = False,
+        tb: bool = False, out: torch.Tensor | None = None, accumulate: bool = False):
+    """op(a) op(b) (+ out) through the kernel set's GEMM (lvx_gemm)."""
+    m = a.shape[1] if ta else a.shape[0]
+    n = b.shape[0] if tb else b.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=a.dtype, device=a.device)
+    ctx.ops.gemm(a, ta, b, tb, out, accumulate)
+    return out
+
+
+def _out_proj(ctx: DeviceContext, x_i: torch.Tensor, st: AttentionState,
+              w: CrossAttentionWeights) -> torch.Tensor:
+    """x_i + flat(O_i) W_O (``src/mllm.py:297-301``): the residual is the GEMM's
+    accumulator."""
+    out = x_i.clone()
+    return _mm(ctx, _flat(st.O.to(x_i.dtype)), w.w_o, out=out, accumulate=True)
+
+
 def project_kv(ctx: DeviceContext, y: torch.Tensor, w: CrossAttentionWeights):
     """K/V from the visual tokens with ONE GEMM y [S, e] @ [W_K | W_V]
     (``lvx_kv_recompute``); K and V are zero-copy head views of its output."""
@@ -155,21 +174,19 @@ def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: to
     """Returns (out_i = x_i + flat(O_i) W_O, saved)."""
     policy = ActivationPolicy(policy)
     scale = default_scale(w.d) if scale is None else scale
-    q = _heads(x_i @ w.w_q, w.hq)
+    q = _heads(_mm(ctx, x_i, w.w_q), w.hq)
     if _chunked(ctx, policy, strategy, y_i.shape[0], kv_chunk_rows):
         st = _attend_chunked(ctx, q, y_i, w, scale, kv_chunk_rows)
         saved = SavedCA(policy=policy, x=x_i, state=st, kv=None)
         saved.extras["kv_chunk_rows"] = kv_chunk_rows
-        out = x_i + _flat(st.O.to(x_i.dtype)) @ w.w_o
-        return out, saved
+        return _out_proj(ctx, x_i, st, w), saved
     k, v = project_kv(ctx, y_i, w)
     fwd = lvx_forward if strategy == "lvx" else ring_forward
     st = fwd(ctx, shards, q, k, v, scale)
     saved = SavedCA(policy=policy, x=x_i, state=st,
                     kv=(k, v) if policy is ActivationPolicy.STORE_KV else None)
     del q, k, v   # under RECOMPUTE nothing but y_i remains for the visual side
-    out = x_i + _flat(st.O.to(x_i.dtype)) @ w.w_o
-    return out, saved
+    return _out_proj(ctx, x_i, st, w), saved
 
 
 def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved: SavedCA,
@@ -180,9 +197,9 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     are all-reduced over the process group when n > 1."""
     scale = default_scale(w.d) if scale is None else scale
     dt = g_i.dtype
-    d_o = _heads(g_i @ w.w_o.T, w.hq)
-    g_wo = _flat(saved.state.O.to(dt)).T @ g_i
-    q = _heads(saved.x @ w.w_q, w.hq)
+    d_o = _heads(_mm(ctx, g_i, w.w_o, tb=True), w.hq)                  # g W_O^T
+    g_wo = _mm(ctx, _flat(saved.state.O.to(dt)), g_i, ta=True)         # flat(O)^T g
+    q = _heads(_mm(ctx, saved.x, w.w_q), w.hq)
     if counter is not None:
         counter.add(saved.x.shape[0], w.w_q.shape[0], w.w_q.shape[1])
     hkd = w.hkv * w.d
@@ -218,7 +235,10 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
     if ctx.n > 1:
         for t in (g_wq, g_wk, g_wv, g_wo):
-            dist.all_reduce(t, group=group if group is not None else ctx.group)
+            if group is not None:
+                dist.all_reduce(t, group=group)
+            else:
+                ctx.all_reduce_sum_(t)
     return CrossAttentionGrads(d_x=d_x, d_y=d_y, w_q=g_wq, w_k=g_wk, w_v=g_wv, w_o=g_wo)
 
 

@@ -7,7 +7,8 @@ size, because on B200 Q/K/V/dO travel in bf16 while the softmax state
 (O, L, D) and gradient accumulators (dQ, dK, dV) travel in fp32, and K/V have
 ``hkv`` heads while the query-side classes have ``hq``.  With hq = hkv and one
 element size the functions reduce exactly to the reference's closed forms
-(checked in tests/test_volumes.py against the reference's own counters).
+(tests/test_oracle.py and the protocol tests check them against the byte
+counters the reference itself produced, tests/golden/golden_strategies.npz).
 """
 from __future__ import annotations
 
@@ -25,6 +26,30 @@ EPILOGUE_PAYLOAD = {
     ("ring", "forward"): (),
     ("ring", "backward"): ("dK", "dV"),
 }
+# The B200 lvx backward moves the same bytes per rank on a different message
+# schedule (strategies.lvx_backward): the immutable (Q, dO, L, D) block is sent
+# at the START of each round and dQ lags one hop, so round 0 carries no dQ
+# and a dQ epilogue hop takes the last one home — n + 1 messages per rank
+# instead of the reference's n.  The B200 Ring backward sends K/V and the dK/dV
+# partials as separate hops (the partial lags its block by one round), so
+# 2 (n - 1) + 1 messages.  Per-rank byte totals are unchanged everywhere.
+B200_ROUND_PAYLOAD = {**ROUND_PAYLOAD,
+                      ("lvx", "backward", 0): ("Q", "dO", "L", "D")}
+B200_EPILOGUE_PAYLOAD = {**EPILOGUE_PAYLOAD, ("lvx", "backward"): ("dQ",)}
+
+
+def messages_per_rank(strategy: str, phase: str, n: int, schedule: str = "b200") -> int:
+    """Hops one rank sends in one call (0 at n = 1): rounds with a send plus
+    the epilogue, if the schedule has one."""
+    if n == 1:
+        return 0
+    rounds = n if strategy == "lvx" else n - 1
+    if schedule == "b200" and (strategy, phase) == ("ring", "backward"):
+        rounds *= 2   # K/V lead, the dK/dV partial of the same block follows one round later
+    epi = (B200_EPILOGUE_PAYLOAD if schedule == "b200" else EPILOGUE_PAYLOAD)[(strategy, phase)]
+    return rounds + (1 if epi else 0)
+
+
 _QSIDE = {"Q", "O", "dO", "dQ", "L", "D"}
 _ROWSTAT = {"L", "D"}
 

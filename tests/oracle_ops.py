@@ -111,6 +111,12 @@ class OracleOps:
     def accumulate(self, src, dst):
         dst += src
 
+    def gemm(self, a, ta, b, tb, out, accumulate=False):
+        r = (a.T if ta else a).double() @ (b.T if tb else b).double()
+        if accumulate:
+            r = r + out.double()
+        out.copy_(r.to(out.dtype))
+
     def kv_recompute(self, y, w_k, w_v, k_out, v_out):
         h = k_out.shape[0]
         for w, out in ((w_k, k_out), (w_v, v_out)):

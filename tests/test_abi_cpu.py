@@ -53,3 +53,13 @@ def test_shape_errors_use_reference_messages():
         blockwise_attention(Q, K[:, :, :2], V)
     with pytest.raises(ValueError, match="tile_rows"):
         blockwise_attention(Q, K, V, tile_rows=0)
+
+
+def test_library_links_no_cublas():
+    """Every GEMM of the path is the library's own kernel (lvx_gemm_sm100.cu):
+    the shared object depends on no BLAS library."""
+    import subprocess
+    from paper_2502_02406_b200 import build
+    lib = build.build()
+    deps = subprocess.run(["ldd", str(lib)], capture_output=True, text=True).stdout
+    assert "cublas" not in deps.lower(), deps

@@ -67,7 +67,11 @@ def test_pipeline_prefetch_bit_identical():
     HostLayerPipeline(ctx, shards, default_scale(d), chunks=4).run(steps)
     alone = HostStep.allocate(*ins)
     HostLayerPipeline(ctx, shards, default_scale(d), chunks=4, prefetch=False).run([alone])
-    for st in steps:
+    # one slot over several steps: each step's copies wait for the previous
+    # step's kernels to release the slot
+    single = [HostStep.allocate(*ins) for _ in range(3)]
+    HostLayerPipeline(ctx, shards, default_scale(d), chunks=4, prefetch=False).run(single)
+    for st in steps + single:
         for name in ("o", "l", "dq", "dk", "dv"):
             assert torch.equal(getattr(st, name), getattr(alone, name)), name
 

@@ -1,5 +1,6 @@
-"""Projection entry points (lvx_project / lvx_project_bwd / lvx_kv_recompute,
-cuBLAS behind the C ABI) vs the reference's golden vectors and vs torch.
+"""Projection entry points (lvx_project / lvx_project_bwd / lvx_kv_recompute /
+lvx_gemm: the library's tcgen05 GEMM behind the C ABI) vs the reference's
+golden vectors and vs torch.
 
 Tolerances: f64 1e-12 and f32 1e-5 max-normalised against the reference's own
 outputs (tests/golden/golden_kernels.npz: kernels.py:227-254 run in this
@@ -87,3 +88,55 @@ def test_kv_recompute_bf16(fused):
     K.kv_recompute(y, wk, wv, k, v)
     ref = (y.float() @ wkv.float()).view(S, 2 * hkv, d).transpose(0, 1)
     assert _err(k, ref[:hkv]) <= 1e-2 and _err(v, ref[hkv:]) <= 1e-2
+
+
+GEMM_SHAPES = [  # M, N, K
+    (128, 256, 64), (300, 264, 200), (1000, 1024, 512), (7, 8, 9),
+    (256, 256, 65536),          # few tiles, tall K: split-K with fp32 reduce
+    (4096, 1024, 4096),         # many tiles, persistent loop over both TMEM buffers
+]
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_tcgen05_gemm_vs_torch_fp32(shape, ta, tb):
+    """lvx_gemm (tcgen05 kernel, all four operand majors) against a torch fp32
+    matmul of the same bf16 operands.  Gate 3e-3 max-normalised: one bf16
+    rounding of the output (2^-9 relative) plus fp32 summation order."""
+    from paper_2502_02406_b200 import kernels as K
+    M, N, Kd = shape
+    a = _bf(*((Kd, M) if ta else (M, Kd)), seed=M + 3 * N)
+    b = _bf(*((N, Kd) if tb else (Kd, N)), seed=Kd + 7)
+    ref = (a.float().T if ta else a.float()) @ (b.float().T if tb else b.float())
+    c = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    K.gemm_into(a, ta, b, tb, c)
+    e1 = _err(c, ref)
+    c0 = _bf(M, N, seed=11)
+    c2 = c0.clone()
+    K.gemm_into(a, ta, b, tb, c2, accumulate=True)
+    e2 = _err(c2, ref + c0.float())
+    print(f"\ngemm {shape} ta={ta} tb={tb}: {e1:.2e} / accumulate {e2:.2e}")
+    assert e1 <= 3e-3 and e2 <= 3e-3
+
+
+def test_gemm_strided_operands():
+    """Leading dimensions larger than the logical widths (column blocks of a
+    wider matrix), as the recompute layer's [W_K | W_V] halves are."""
+    from paper_2502_02406_b200 import kernels as K
+    big_a, big_b = _bf(640, 1024, seed=21), _bf(1024, 768, seed=22)
+    a, b = big_a[:, 256:768], big_b[256:768, 128:640]
+    out = torch.empty(640, 1024, dtype=torch.bfloat16, device="cuda")[:, 256:768]
+    K.gemm_into(a, False, b, False, out)
+    assert _err(out, a.float() @ b.float()) <= 3e-3
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_simt_gemm_exact_dtypes(dt):
+    from paper_2502_02406_b200 import kernels as K
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.rand(77, 130, device="cuda", generator=g, dtype=dt)
+    b = torch.rand(90, 130, device="cuda", generator=g, dtype=dt)
+    c = torch.empty(77, 90, device="cuda", dtype=dt)
+    K.gemm_into(a, False, b, True, c)
+    ref = a.double() @ b.double().T
+    assert _err(c, ref) <= (1e-6 if dt == torch.float32 else 1e-13)

@@ -138,3 +138,20 @@ def test_stats_merge_over_ranks():
     assert res.results == [2.0, 0.0, 1.0]        # from the predecessor
     assert res.stats.total_bytes() == 3 * 2 * 3 * 4 * 4
     assert res.stats.link(0, 1).message_count == 1
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_message_counts_match_b200_schedule(n):
+    """Per-link message counts of the B200 schedules (volumes.messages_per_rank:
+    same bytes as the reference, dQ / dK-dV hops on their own messages)."""
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200 import volumes
+    from tests.oracle_ops import OracleOps
+    Q, K, V, dO = orc.make_inputs(11, 23, 2, 4, seed=3)
+    for strategy in ("lvx", "ring"):
+        res = lvx.run_distributed(strategy, Q, K, V, dO=dO, spec=lvx.ClusterSpec(n),
+                                  ops=OracleOps(), ranks="threads")
+        want = volumes.messages_per_rank(strategy, "forward", n) + \
+            volumes.messages_per_rank(strategy, "backward", n)
+        for i in range(n):
+            assert res.stats.link(i, (i + 1) % n).message_count == want, (strategy, i)

@@ -1,0 +1,50 @@
+# One GPU session of measurements, each leg under its own timeout, logs into
+# gpurun_out/<tag>_*.  Usage (from the repo root, on the GPU box):
+#   bash tools/gpu_session.sh <tag> <leg> [<leg> ...]
+# legs: probe (DSMEM dQ reduce probe), bench (C2 N=1), c3, c4, c5 (Lkv sweeps /
+#       layer stack at N=1), launches (ncu launch list of the C2 bench),
+#       ncu_full (ncu --set full of the dominant kernel), pytest (pytest -m gpu)
+set -u
+tag=$1; shift
+out=gpurun_out
+mkdir -p $out
+python -m paper_2502_02406_b200.build > $out/${tag}_build.log 2>&1 || { echo "build failed"; exit 1; }
+nvidia-smi -q -d CLOCK,PERFORMANCE > $out/${tag}_clocks_before.txt 2>&1
+for leg in "$@"; do
+  t0=$(date +%s)
+  case $leg in
+    probe)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/dqprobe \
+        tools/dq_cluster_reduce_probe.cu > $out/${tag}_probe_build.log 2>&1 &&
+      timeout 120 /tmp/dqprobe > $out/${tag}_probe.jsonl 2>&1 ;;
+    bench)
+      timeout 600 python bench.py --steps 10 --warmup 3 > $out/${tag}_bench_c2.json 2> $out/${tag}_bench_c2.err ;;
+    c3)
+      timeout 900 python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu --no-e2e \
+        > $out/${tag}_bench_c3.json 2> $out/${tag}_bench_c3.err ;;
+    c4)
+      timeout 900 python bench.py --workload c4 --steps 3 --warmup 3 --no-cpu \
+        > $out/${tag}_bench_c4.json 2> $out/${tag}_bench_c4.err ;;
+    c5)
+      timeout 1200 python bench.py --workload c5 --steps 3 --warmup 3 --no-cpu --no-e2e \
+        > $out/${tag}_bench_c5.json 2> $out/${tag}_bench_c5.err ;;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        --log-file $out/${tag}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
+        > $out/${tag}_launches.log 2>&1 ;;
+    gemm)
+      timeout 300 python tools/gemm_probe.py --preset llama > $out/${tag}_gemm_llama.jsonl 2>&1
+      timeout 300 python tools/gemm_probe.py --preset flamingo > $out/${tag}_gemm_flamingo.jsonl 2>&1 ;;
+    pytest_gemm)
+      timeout 900 python -m pytest tests/test_gpu_project.py tests/test_gpu_recompute.py tests/test_gpu_mllm.py -q -s --timeout 600 -p no:cacheprovider \
+        > $out/${tag}_pytest_gemm.log 2>&1 ;;
+    pytest)
+      timeout 1800 python -m pytest tests -m gpu -q -s --timeout 600 -p no:cacheprovider \
+        > $out/${tag}_pytest.log 2>&1 ;;
+    pytest_multi)
+      timeout 900 python -m pytest tests/test_gpu_multi.py -q -s --timeout 600 -p no:cacheprovider \
+        > $out/${tag}_pytest_multi.log 2>&1 ;;
+    *) echo "unknown leg $leg" ;;
+  esac
+  echo "$leg exit=$? secs=$(( $(date +%s) - t0 ))" | tee -a $out/${tag}_legs.txt
+done
