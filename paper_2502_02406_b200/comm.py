@@ -177,6 +177,9 @@ class ThreadGroup:
         # rank, FIFO queues keyed by (src, message index)
         self.cond = threading.Condition()
         self.boxes: list = [dict() for _ in range(n)]
+        # copy-engine transport between thread ranks: the largest value whose
+        # stream-side write into rank r's flag word w has been ENQUEUED
+        self.marks: list = [dict() for _ in range(n)]
 
     def fail(self, rank: int, exc: BaseException) -> None:
         with self._lock:
@@ -192,6 +195,30 @@ class ThreadGroup:
     @property
     def aborted(self) -> bool:
         return self.first_failure is not None
+
+    def mark(self, rank: int, word: int, value: int) -> None:
+        with self.cond:
+            m = self.marks[rank]
+            if value > m.get(word, -1):
+                m[word] = value
+                self.cond.notify_all()
+
+    def await_mark(self, rank: int, word: int, value: int) -> None:
+        """Block the host until a write of >= value into rank's flag word has
+        been enqueued (on any stream).  Thread ranks share one CUDA context:
+        a device-side wait enqueued before its write could deadlock against
+        any device-synchronising call (allocator, free) another rank's thread
+        makes meanwhile, so a wait is only ever enqueued behind its signal."""
+        deadline = time.monotonic() + self.timeout
+        with self.cond:
+            while self.marks[rank].get(word, -1) < value:
+                if self.aborted:
+                    raise ClusterAborted(f"worker {rank}: cluster aborted while waiting for a hop")
+                now = time.monotonic()
+                if now >= deadline:
+                    raise CollectiveTimeout(f"worker {rank}: hop (flag {word} >= {value}) did "
+                                            f"not arrive within {self.timeout}s")
+                self.cond.wait(timeout=deadline - now)
 
     def put(self, dst: int, key, payload) -> None:
         with self.cond:
@@ -296,13 +323,14 @@ class _Coll:
 # transports
 # ---------------------------------------------------------------------------
 
-def _as_rows(t: torch.Tensor) -> tuple[int, int, int, int]:
+def _as_rows(t: torch.Tensor, split: bool = False) -> tuple[int, int, int, int]:
     """(ptr, pitch, width, height) bytes of a [h, rows, d] or [h, rows] view
-    whose rows are contiguous within each head."""
+    whose rows are contiguous within each head: one span when the view is
+    contiguous (unless ``split``), else one row of ``width`` bytes per head."""
     es = t.element_size()
     if t.numel() == 0:
         return t.data_ptr(), 0, 0, 0
-    if t.is_contiguous():
+    if t.is_contiguous() and (not split or t.shape[0] == 1):
         return t.data_ptr(), t.numel() * es, t.numel() * es, 1
     inner = t[0]
     if not inner.is_contiguous():
@@ -494,6 +522,7 @@ class PeerTransport:
         self.epoch = 0
         self._touched: set = set()
         self._aborted = False
+        self.tg = coll.group.group if coll.threaded else None
         if coll.threaded:
             coll.group.group.transports[self.rank] = self
 
@@ -529,6 +558,9 @@ class PeerTransport:
         flags = self.arena[cap:].view(torch.int32)
         flags[self.EPOCH:self.EPOCH + self.MAXN].fill_(self.epoch)
         torch.cuda.synchronize(self.device)
+        if self.tg is not None:
+            for p in range(self.n):
+                self.tg.mark(self.rank, self.EPOCH + p, self.epoch)
         if self.coll.threaded:
             maps = self.coll.all_gather_object(m.value)
             for p in range(self.n):
@@ -555,6 +587,20 @@ class PeerTransport:
     def _flag(self, word: int) -> int:
         return self.capacity + 4 * word
 
+    def _signal(self, peer: int, word: int, value: int, stream) -> None:
+        """peer's flag word <- value, stream-ordered after prior work."""
+        self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
+            self.map, peer, self._flag(word), value & 0xFFFFFFFF, stream))
+        if self.tg is not None:
+            self.tg.mark(peer, word, value)
+
+    def _wait(self, word: int, value: int, stream) -> None:
+        """stream waits until this rank's flag word >= value."""
+        if self.tg is not None:
+            self.tg.await_mark(self.rank, word, value)
+        self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
+            self.map, self._flag(word), value & 0xFFFFFFFF, stream))
+
     def _check(self, fn: str, st: int) -> None:
         if st != 0:
             from . import _lib
@@ -578,17 +624,19 @@ class PeerTransport:
         cs = self.copy.cuda_stream
         for p in range(self.n):
             if p != self.rank:
-                self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
-                    self.map, p, self._flag(self.EPOCH + self.rank), self.epoch, cs))
+                self._signal(p, self.EPOCH + self.rank, self.epoch, cs)
         done = torch.cuda.Event()
         done.record(self.copy)
         cur.wait_event(done)
 
     def _put_many(self, peer: int, send, recv) -> None:
         """Copy each ``send`` tensor into ``peer``'s arena at the offset of the
-        matching ``recv`` view of this rank's arena (identical layouts).
-        Contiguous pieces laid out identically on both sides (a packed record
-        sent from a record) coalesce into one copy."""
+        matching ``recv`` view of this rank's arena (identical layouts).  A
+        contiguous block and a strided one (per-head rows) go as a 2-D copy
+        with their own pitches.  Pieces that are exactly adjacent on both
+        sides and both inside this rank's arena (a record forwarded whole)
+        coalesce into one copy; nothing else does, since a gap between two
+        pieces may hold rows the receiver already has."""
         cs = self.copy.cuda_stream
         runs = []   # [dst_off, dst_pitch, src_ptr, src_pitch, width, height]
         for s, r in zip(send, recv):
@@ -598,19 +646,24 @@ class PeerTransport:
                 raise ClusterError(f"shift mismatch {tuple(s.shape)} vs {tuple(r.shape)}")
             sp, spitch, w, h = _as_rows(s)
             rp, rpitch, w2, h2 = _as_rows(r)
-            if (w, h) != (w2, h2):
-                raise ClusterError(f"shift layout mismatch {tuple(s.shape)}/{s.stride()} vs "
-                                   f"{tuple(r.shape)}/{r.stride()}")
+            if (w, h) != (w2, h2):       # one side strided: copy per head on both
+                sp, spitch, w, h = _as_rows(s, split=True)
+                rp, rpitch, w2, h2 = _as_rows(r, split=True)
+                if (w, h) != (w2, h2):
+                    raise ClusterError(f"shift layout mismatch {tuple(s.shape)}/{s.stride()} "
+                                       f"vs {tuple(r.shape)}/{r.stride()}")
             off = rp - self.base
             if off < 0 or off + (h - 1) * rpitch + w > self.capacity:
                 raise ClusterError("receive buffer is not in the transport arena")
-            if runs and h == 1 and runs[-1][5] == 1:
-                o0, _, s0, _, w0, _ = runs[-1]
-                if off >= o0 + w0 and off - o0 == sp - s0:
-                    runs[-1][4] = off + w - o0
+            src_in_arena = self.base <= sp and sp + (h - 1) * spitch + w <= self.base + \
+                self.capacity
+            if runs and h == 1 and runs[-1][5] == 1 and src_in_arena and runs[-1][6]:
+                o0, _, s0, _, w0, _, _ = runs[-1]
+                if off == o0 + w0 and sp == s0 + w0:
+                    runs[-1][4] = w0 + w
                     continue
-            runs.append([off, rpitch, sp, spitch, w, h])
-        for off, rpitch, sp, spitch, w, h in runs:
+            runs.append([off, rpitch, sp, spitch, w, h, src_in_arena])
+        for off, rpitch, sp, spitch, w, h, _ in runs:
             self._check("lvx_peer_put", self.lib.lvx_peer_put(
                 self.map, peer, off, rpitch, ctypes.c_void_p(sp), spitch, w, h, cs))
 
@@ -625,20 +678,16 @@ class PeerTransport:
         cs = self.copy.cuda_stream
         if to not in self._touched:     # the successor finished its previous call
             self._touched.add(to)
-            self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-                self.map, self._flag(self.EPOCH + to), self.epoch - 1, cs))
+            self._wait(self.EPOCH + to, self.epoch - 1, cs)
         if after is not None:           # the successor released the slot
             word, value = after
-            self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-                self.map, self._flag(self.FREE + word), value, cs))
+            self._wait(self.FREE + word, value, cs)
         self._put_many(to, send, dst)
-        self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
-            self.map, to, self._flag(self.READY + k * self.MAXN + self.rank), self.epoch, cs))
+        self._signal(to, self.READY + k * self.MAXN + self.rank, self.epoch, cs)
 
         def wait():
-            self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-                self.map, self._flag(self.READY + k * self.MAXN + frm), self.epoch,
-                torch.cuda.current_stream(self.device).cuda_stream))
+            self._wait(self.READY + k * self.MAXN + frm, self.epoch,
+                       torch.cuda.current_stream(self.device).cuda_stream)
         return _Hop(wait)
 
     def release(self, word: int, value: int, peer: int) -> None:
@@ -648,8 +697,7 @@ class PeerTransport:
         ev = torch.cuda.Event()
         ev.record(cur)
         self.copy.wait_event(ev)
-        self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
-            self.map, peer, self._flag(self.FREE + word), value, self.copy.cuda_stream))
+        self._signal(peer, self.FREE + word, value, self.copy.cuda_stream)
 
     def all_to_all(self, chunks, recv, dst, rank: int, k: int):
         cur = torch.cuda.current_stream(self.device)
@@ -662,18 +710,15 @@ class PeerTransport:
                 continue
             if w not in self._touched:
                 self._touched.add(w)
-                self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-                    self.map, self._flag(self.EPOCH + w), self.epoch - 1, cs))
+                self._wait(self.EPOCH + w, self.epoch - 1, cs)
             self._put_many(w, chunks[w], dst[w])
-            self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
-                self.map, w, self._flag(self.READY + k * self.MAXN + rank), self.epoch, cs))
+            self._signal(w, self.READY + k * self.MAXN + rank, self.epoch, cs)
 
         def wait():
             st = torch.cuda.current_stream(self.device).cuda_stream
             for w in range(self.n):
                 if w != rank:
-                    self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-                        self.map, self._flag(self.READY + k * self.MAXN + w), self.epoch, st))
+                    self._wait(self.READY + k * self.MAXN + w, self.epoch, st)
         return _Hop(wait)
 
     def abort(self) -> None:
@@ -708,21 +753,23 @@ _ALIGN = 256
 
 
 class _Layout:
-    """Bump allocator for one scheduler call (identical on every rank)."""
+    """Bump allocator for one scheduler call (identical on every rank).
+    Buffers start on 256-byte boundaries; the fields of one record on 16-byte
+    boundaries, so a record whose fields are all full is one adjacent span."""
 
     def __init__(self):
         self.items = []
         self.size = 0
 
-    def add(self, shape, dtype) -> int:
+    def add(self, shape, dtype, align: int = _ALIGN) -> int:
         if isinstance(shape, int):
             shape = (shape,)
         nbytes = 1
         for s in shape:
             nbytes *= int(s)
         nbytes *= torch.empty((), dtype=dtype).element_size()
-        off = self.size
-        self.size = (off + nbytes + _ALIGN - 1) // _ALIGN * _ALIGN
+        off = (self.size + align - 1) // align * align
+        self.size = off + nbytes
         self.items.append((off, tuple(int(s) for s in shape), dtype))
         return len(self.items) - 1
 
@@ -742,7 +789,8 @@ class _Call:
         plan = {}
         for name, (a, b) in spec.items():
             if isinstance(b, list):
-                plan[name] = [{f: lay.add(shape, dt) for f, shape, dt in b} for _ in range(a)]
+                plan[name] = [{f: lay.add(shape, dt, align=_ALIGN if j == 0 else 16)
+                               for j, (f, shape, dt) in enumerate(b)} for _ in range(a)]
             else:
                 plan[name] = lay.add(a, b)
         base = self.ctx._raw(lay.size)

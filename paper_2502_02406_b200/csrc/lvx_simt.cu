@@ -13,6 +13,8 @@
 //   simt_bwd_dkv_kernel  kernels.py:192-224, the dK/dV half (GQA summed)
 //   merge_kernel         kernels.py:144-161 merge_states
 //   row_stats_kernel     kernels.py:164-169 attention_row_stats
+#include <type_traits>
+
 #include "lvx_common.cuh"
 
 namespace lvx {
@@ -294,6 +296,124 @@ __global__ void row_stats_kernel(View3<const Ts> O, View3<const Tg> dO, View3<Ts
   if (lane == 0) *D.at(h, i) = from_acc<Ts, Acc>(acc);
 }
 
+// f32 states (the bf16 tensor-core path's O / L / D): HBM-bound, so one
+// 16-byte vector per thread, LPR = d/4 lanes per row (a power of two <= 32),
+// several rows per warp, fp32 math (logaddexp / exp to ~1e-7 relative, far
+// inside every gate).  The row weights are recomputed by each lane of the row
+// from the two L values (one broadcast load per lane group).
+template <int LPR>
+__global__ void __launch_bounds__(256)
+merge_f32v_kernel(View3<const float> OA, View3<const float> LA, View3<const float> OB,
+                  View3<const float> LB, View3<float> O, View3<float> L, int64_t nrows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gr = t / LPR;
+  const int c = (int)(t % LPR) * 4;
+  if (gr >= nrows) return;
+  const int64_t h = gr / O.rows, i = gr % O.rows;
+  const float la = *LA.at(h, i), lb = *LB.at(h, i);
+  float lm;
+  if (la == lb) {
+    lm = la + 0.693147180559945309f;      // numpy.logaddexp(x, x); -inf stays -inf
+  } else {
+    const float hi = fmaxf(la, lb), lo = fminf(la, lb);
+    lm = isinf(hi) ? hi : hi + log1pf(expf(lo - hi));
+  }
+  const float safe = (isinf(lm) && lm < 0.f) ? 0.f : lm;
+  const float wa = expf(la - safe), wb = expf(lb - safe);
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(OA.at(h, i) + c));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(OB.at(h, i) + c));
+  __stcs(reinterpret_cast<float4*>(O.at(h, i) + c),
+         make_float4(wa * a.x + wb * b.x, wa * a.y + wb * b.y, wa * a.z + wb * b.z,
+                     wa * a.w + wb * b.w));
+  if (c == 0) *L.at(h, i) = lm;
+}
+
+template <int LPR, typename Tg>
+__global__ void __launch_bounds__(256)
+row_stats_f32v_kernel(View3<const float> O, View3<const Tg> dO, View3<float> D, int64_t nrows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gr = t / LPR;
+  const int c = (int)(t % LPR) * 4;
+  const bool live = gr < nrows;
+  float acc = 0.f;
+  int64_t h = 0, i = 0;
+  if (live) {
+    h = gr / O.rows;
+    i = gr % O.rows;
+    const float4 o = __ldcs(reinterpret_cast<const float4*>(O.at(h, i) + c));
+    float g[4];
+    if constexpr (std::is_same<Tg, float>::value) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(dO.at(h, i) + c));
+      g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
+    } else {
+      const uint2 v = __ldcs(reinterpret_cast<const uint2*>(dO.at(h, i) + c));
+      const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+      const __nv_bfloat162 p1 = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+      g[0] = __bfloat162float(p0.x); g[1] = __bfloat162float(p0.y);
+      g[2] = __bfloat162float(p1.x); g[3] = __bfloat162float(p1.y);
+    }
+    acc = o.x * g[0] + o.y * g[1] + o.z * g[2] + o.w * g[3];
+  }
+#pragma unroll
+  for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (live && c == 0) *D.at(h, i) = acc;
+}
+
+bool f32_vec_ok(const lvx_view* v) {
+  return v->d % 4 == 0 && (reinterpret_cast<uintptr_t>(v->data) & 15) == 0 &&
+         v->row_stride % 4 == 0 && (v->heads <= 1 || v->head_stride % 4 == 0);
+}
+bool bf16_vec_ok(const lvx_view* v) {
+  return v->d % 4 == 0 && (reinterpret_cast<uintptr_t>(v->data) & 7) == 0 &&
+         v->row_stride % 4 == 0 && (v->heads <= 1 || v->head_stride % 4 == 0);
+}
+// lanes per row of the vector kernels: d/4 when that is a power of two <= 32
+int vec_lanes(int64_t d) {
+  const int64_t l = d / 4;
+  return (l >= 1 && l <= 32 && (l & (l - 1)) == 0) ? (int)l : 0;
+}
+
+template <int LPR>
+int merge_vec(const lvx_view* oa, const lvx_view* la, const lvx_view* ob, const lvx_view* lb,
+              const lvx_view* o, const lvx_view* l, int64_t nrows, cudaStream_t st) {
+  const int64_t threads = nrows * LPR;
+  merge_f32v_kernel<LPR><<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(
+      View3<const float>{static_cast<const float*>(oa->data), oa->heads, oa->rows, oa->d,
+                         oa->head_stride, oa->row_stride},
+      View3<const float>{static_cast<const float*>(la->data), la->heads, la->rows, la->d,
+                         la->head_stride, la->row_stride},
+      View3<const float>{static_cast<const float*>(ob->data), ob->heads, ob->rows, ob->d,
+                         ob->head_stride, ob->row_stride},
+      View3<const float>{static_cast<const float*>(lb->data), lb->heads, lb->rows, lb->d,
+                         lb->head_stride, lb->row_stride},
+      make_view<float>(o), make_view<float>(l), nrows);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+template <int LPR, typename Tg>
+int row_stats_vec(const lvx_view* o, const lvx_view* dO, const lvx_view* D, int64_t nrows,
+                  cudaStream_t st) {
+  row_stats_f32v_kernel<LPR, Tg><<<(unsigned)ceil_div(nrows * LPR, 256), 256, 0, st>>>(
+      View3<const float>{static_cast<const float*>(o->data), o->heads, o->rows, o->d,
+                         o->head_stride, o->row_stride},
+      View3<const Tg>{static_cast<const Tg*>(dO->data), dO->heads, dO->rows, dO->d,
+                      dO->head_stride, dO->row_stride},
+      make_view<float>(D), nrows);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
+#define LVX_LPR_DISPATCH(lpr, CALL)            \
+  switch (lpr) {                               \
+    case 1: { constexpr int LPR = 1; CALL; }   \
+    case 2: { constexpr int LPR = 2; CALL; }   \
+    case 4: { constexpr int LPR = 4; CALL; }   \
+    case 8: { constexpr int LPR = 8; CALL; }   \
+    case 16: { constexpr int LPR = 16; CALL; } \
+    default: { constexpr int LPR = 32; CALL; } \
+  }
+
 template <typename Ts>
 __global__ void fill_empty_kernel(View3<Ts> O, View3<Ts> L) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -416,6 +536,9 @@ int merge(const lvx_view* oa, const lvx_view* la, const lvx_view* ob, const lvx_
   if (!warps) return LVX_OK;
   const int threads = 256;
   const int64_t blocks = ceil_div(warps * 32, threads);
+  const int lpr = vec_lanes(o->d);
+  if (o->dtype == LVX_F32 && lpr && f32_vec_ok(oa) && f32_vec_ok(ob) && f32_vec_ok(o))
+    LVX_LPR_DISPATCH(lpr, return merge_vec<LPR>(oa, la, ob, lb, o, l, warps, st))
   if (o->dtype == LVX_F32)
     merge_kernel<float><<<blocks, threads, 0, st>>>(cview<float>(oa), cview<float>(la),
                                                     cview<float>(ob), cview<float>(lb),
@@ -434,6 +557,13 @@ int row_stats(const lvx_view* o, const lvx_view* dO, const lvx_view* D, cudaStre
   if (!warps) return LVX_OK;
   const int threads = 256;
   const int64_t blocks = ceil_div(warps * 32, threads);
+  const int lpr = vec_lanes(o->d);
+  if (o->dtype == LVX_F32 && lpr && f32_vec_ok(o) && D->dtype == LVX_F32) {
+    if (dO->dtype == LVX_F32 && f32_vec_ok(dO))
+      LVX_LPR_DISPATCH(lpr, return (row_stats_vec<LPR, float>(o, dO, D, warps, st)))
+    if (dO->dtype == LVX_BF16 && bf16_vec_ok(dO))
+      LVX_LPR_DISPATCH(lpr, return (row_stats_vec<LPR, __nv_bfloat16>(o, dO, D, warps, st)))
+  }
   if (o->dtype == LVX_F32 && dO->dtype == LVX_F32)
     row_stats_kernel<float, float><<<blocks, threads, 0, st>>>(cview<float>(o), cview<float>(dO),
                                                                make_view<float>(D));

@@ -101,8 +101,9 @@ GEMM_SHAPES = [  # M, N, K
 @pytest.mark.parametrize("shape", GEMM_SHAPES)
 def test_tcgen05_gemm_vs_torch_fp32(shape, ta, tb):
     """lvx_gemm (tcgen05 kernel, all four operand majors) against a torch fp32
-    matmul of the same bf16 operands.  Gate 3e-3 max-normalised: one bf16
-    rounding of the output (2^-9 relative) plus fp32 summation order."""
+    matmul of the same bf16 operands.  Gate 4e-3 max-normalised: one bf16
+    rounding of the output is up to half an ulp, 2^-8 of the largest element
+    (3.9e-3), plus fp32 summation order."""
     from paper_2502_02406_b200 import kernels as K
     M, N, Kd = shape
     a = _bf(*((Kd, M) if ta else (M, Kd)), seed=M + 3 * N)
@@ -116,7 +117,7 @@ def test_tcgen05_gemm_vs_torch_fp32(shape, ta, tb):
     K.gemm_into(a, ta, b, tb, c2, accumulate=True)
     e2 = _err(c2, ref + c0.float())
     print(f"\ngemm {shape} ta={ta} tb={tb}: {e1:.2e} / accumulate {e2:.2e}")
-    assert e1 <= 3e-3 and e2 <= 3e-3
+    assert e1 <= 4e-3 and e2 <= 4e-3
 
 
 def test_gemm_strided_operands():
@@ -127,7 +128,7 @@ def test_gemm_strided_operands():
     a, b = big_a[:, 256:768], big_b[256:768, 128:640]
     out = torch.empty(640, 1024, dtype=torch.bfloat16, device="cuda")[:, 256:768]
     K.gemm_into(a, False, b, False, out)
-    assert _err(out, a.float() @ b.float()) <= 3e-3
+    assert _err(out, a.float() @ b.float()) <= 4e-3
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
