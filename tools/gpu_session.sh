@@ -32,6 +32,18 @@ for leg in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file $out/${tag}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
         > $out/${tag}_launches.log 2>&1 ;;
+    bench_n)   # all visible GPUs, torchrun, C2 (BENCH_SKV overrides Lkv)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29517 bench.py --gpus $n --steps 10 --warmup 3 ${BENCH_SKV:+--skv $BENCH_SKV} \
+        > $out/${tag}_bench_n${n}${BENCH_SKV:+_skv$BENCH_SKV}.json 2> $out/${tag}_bench_n${n}.err ;;
+    c5_n)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29518 bench.py --gpus $n --workload c5 --steps 3 --warmup 3 --no-e2e \
+        > $out/${tag}_bench_c5_n${n}.json 2> $out/${tag}_bench_c5_n${n}.err ;;
+    hbm)
+      timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
       timeout 300 python tools/gemm_probe.py --preset llama > $out/${tag}_gemm_llama.jsonl 2>&1
       timeout 300 python tools/gemm_probe.py --preset flamingo > $out/${tag}_gemm_flamingo.jsonl 2>&1 ;;
