@@ -341,6 +341,18 @@ def _as_rows(t: torch.Tensor, split: bool = False) -> tuple[int, int, int, int]:
     return t.data_ptr(), t.stride(0) * es, inner.numel() * es, t.shape[0]
 
 
+def _copy_overlap(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """dst <- src over the rows both have (blocks of uneven shards differ by
+    one row); same-shape blocks are a plain copy."""
+    if src.numel() == 0 or dst.numel() == 0 or src.data_ptr() == dst.data_ptr():
+        return
+    if src.shape == dst.shape:
+        dst.copy_(src)
+        return
+    m = min(src.shape[1], dst.shape[1])
+    dst[:, :m].copy_(src[:, :m])
+
+
 class _Hop:
     """An in-flight shift; ``wait()`` orders the caller's stream after it."""
 
@@ -822,10 +834,11 @@ class DeviceContext:
     (one process per GPU; gloo in the CPU protocol tests), a ``ThreadRank``
     (thread ranks sharing one GPU), or ``None`` with n = 1.  ``transport``:
     "ce" (copy-engine arenas, the default on CUDA) or "pg" (torch.distributed
-    send/recv: NCCL or gloo).  ``comm_enabled=False`` runs the identical
-    schedule with every hop skipped — the no-communication arm of
-    PAPER.md:233 (receive slots then hold zeros, so every kernel still reads
-    finite data)."""
+    send/recv: NCCL or gloo), or another context's transport object.
+    ``comm_enabled=False`` runs the identical schedule with every hop skipped
+    — the no-communication arm of PAPER.md:233.  Its receive slots hold
+    zeros (a fresh arena) or, sharing the comm arm's transport, the data of
+    the last real hop, so every kernel reads the same kind of values."""
 
     def __init__(self, rank: int = 0, n: int = 1, group=None, device=None, ops=None,
                  comm_enabled: bool = True, transport: str | None = None,
@@ -856,6 +869,10 @@ class DeviceContext:
                 ("mailbox" if isinstance(group, ThreadRank) else "pg")
         if n == 1:
             self.transport = None
+        elif isinstance(transport, (PeerTransport, ProcessGroupTransport, MailboxTransport)):
+            # another context's transport: the no-comm arm shares the comm
+            # arm's arena, so its receive slots hold the last real hop's data
+            self.transport = transport
         elif transport == "mailbox":
             self.transport = MailboxTransport(self.coll)
         elif transport == "ce":
@@ -936,11 +953,37 @@ class DeviceContext:
         k = self._msg()
         sent = {c: t.numel() * t.element_size() for c, t in zip(classes, send)}
         if not self.comm_enabled:
-            return _Hop(), sent
+            return self._local_hop(list(zip(send, recv))), sent
         hop = self.transport.shift(send, recv if dst is None else dst, recv, self.successor,
                                    self.predecessor, k, after)
         self.stats.record(self.rank, self.successor, payload_nbytes(send))
         return hop, sent
+
+    def _local_hop(self, pairs):
+        """No-communication arm: instead of the hop, each receive slot gets a
+        local copy of the matching send block (the overlapping rows when
+        uneven shards make them differ), on the transport's side stream like
+        a real hop.  The kernels then read the same kind of values as with
+        communication (a stale or recycled slot can hold anything, and the
+        attention kernels' speed depends on the score range)."""
+        if not pairs:
+            return _Hop()
+        side = getattr(self.transport, "copy", None) if self.device.type == "cuda" else None
+        if side is None:
+            def copy_now():
+                for s_, r_ in pairs:
+                    _copy_overlap(s_, r_)
+            return _Hop(copy_now)
+        cur = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            for s_, r_ in pairs:
+                _copy_overlap(s_, r_)
+        done = torch.cuda.Event()
+        done.record(side)
+        return _Hop(lambda: torch.cuda.current_stream(self.device).wait_event(done))
 
     def release(self, word: int, value: int) -> None:
         """The slot the predecessor filled may be reused (see ``shift(after=)``)."""
@@ -976,7 +1019,13 @@ class DeviceContext:
             return _Hop(copy_local), sent
         k = self._msg()
         if not self.comm_enabled:
-            return _Hop(copy_local), sent
+            hop = self._local_hop([(c, r) for w in range(self.n) if w != self.rank
+                                   for c, r in zip(chunks[w], recv[w])])
+
+            def wait_nc():
+                copy_local()
+                hop.wait()
+            return _Hop(wait_nc), sent
         for w in range(self.n):
             if w != self.rank:
                 self.stats.record(self.rank, w, payload_nbytes(chunks[w]))
