@@ -270,8 +270,10 @@ def native_arm(args):
     else:
         import paper_2502_02406_b200 as lvx
         ctx = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev)
+        # the no-comm arm shares the comm arm's arena and side stream (its hops
+        # are local copies into the same receive slots)
         ctx_nc = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev,
-                                   comm_enabled=False)
+                                   comm_enabled=False, transport=ctx.transport)
         head_skv = CFG["s_kv"] if CFG["s_kv"] in args.points else args.points[-1]
         lines = []
         for skv in args.points:
@@ -299,9 +301,12 @@ def _summary(line: dict) -> dict:
     out["roofline_frac"] = line["roofline"]["frac"]
     out["fwd_tflops"] = line["roofline"]["fwd_tflops"]
     out["bwd_tflops"] = line["roofline"]["bwd_tflops"]
-    if "ring_baseline" in line:
-        out["ring_ms_per_step"] = line["ring_baseline"]["ms_per_step"]
-        out["speedup_lvx_over_ring"] = line["ring_baseline"]["speedup_lvx_over_ring"]
+    rb = line.get("ring_baseline") or {}
+    if "ms_per_step" in rb:
+        out["ring_ms_per_step"] = rb["ms_per_step"]
+        out["speedup_lvx_over_ring"] = rb["speedup_lvx_over_ring"]
+    elif rb:
+        out["ring"] = rb.get("skipped")
     return out
 
 
@@ -497,7 +502,11 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
             "fwd_kernel": sec([a for a, _ in tr_nc], "fwd_kernel") * 1e3,
             "dq_kernel": sec([b for _, b in tr_nc], "dq_kernel") * 1e3,
             "dkv_kernel": sec([b for _, b in tr_nc], "dkv_kernel") * 1e3}
-        if not args.no_ring_compare and args.strategy == "lvx":
+        ring_fits = _ring_fits(env, shards, hq, hkv, d, dev)
+        if not args.no_ring_compare and args.strategy == "lvx" and not ring_fits:
+            out["ring_baseline"] = {"skipped": "the Ring baseline's rotating K/V slots and fp32 "
+                                               "dK/dV partials do not fit in HBM at this Lkv"}
+        elif not args.no_ring_compare and args.strategy == "lvx":
             ms_ring, rtr, *_ = timed(ctx, max(2, args.steps // 2), 1,
                                      strategy=(ring_forward, ring_backward))
             out["ring_baseline"] = {"ms_per_step": ms_ring,
@@ -516,6 +525,26 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         out["e2e"] = e2e_arm(args, ctx, shards, (q_i, k_i, v_i, do_i), scale, fwd, bwd, flops,
                              world, dev)
     return out
+
+
+def _ring_fits(env, shards, hq, hkv, d, dev) -> bool:
+    """Whether ring_backward's buffers fit beside what is resident: per rank
+    RING_SLOTS bf16 K/V slots, as many fp32 dK/dV partial slots, the fp32
+    homecoming, its own and a scratch fp32 dK/dV, and the bf16 gradients
+    (strategies.ring_backward).  Decided collectively (min over ranks)."""
+    import torch
+    from paper_2502_02406_b200.strategies import RING_SLOTS
+    n = env.world
+    mk = max(shards.kv_sizes)
+    slots = max(1, min(RING_SLOTS, n - 1))
+    kv = hkv * mk * d
+    need = slots * kv * 2 * 2 + slots * kv * 4 * 2 + kv * 4 * 2 + 2 * kv * 4 * 2 + kv * 2 * 2
+    free, _ = torch.cuda.mem_get_info(dev)
+    ok = torch.tensor([1.0 if need < 0.9 * free else 0.0], device=dev)
+    if n > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item() > 0)
 
 
 def cpu_c1_timing(reps: int = 3) -> dict:

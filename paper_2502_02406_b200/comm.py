@@ -550,8 +550,10 @@ class PeerTransport:
         if data_bytes <= self.capacity:
             return
         from . import _lib
-        cap = max(int(data_bytes * 1.25), 1 << 20)
-        cap = (cap + 4095) // 4096 * 4096
+        # exact need rounded to 2 MiB (HBM is the Ring baseline's limit at
+        # multi-million-row shards); calls of one schedule repeat their sizes
+        cap = max(data_bytes, 1 << 20)
+        cap = (cap + (2 << 20) - 1) // (2 << 20) * (2 << 20)
         # every rank asks for the same layout; agree on the largest request
         cap = max(self.coll.all_gather_object(cap))
         torch.cuda.synchronize(self.device)
