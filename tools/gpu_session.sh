@@ -42,6 +42,12 @@ for leg in "$@"; do
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
         --master-port 29518 bench.py --gpus $n --workload c5 --steps 3 --warmup 3 --no-e2e \
         > $out/${tag}_bench_c5_n${n}.json 2> $out/${tag}_bench_c5_n${n}.err ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck; do
+        timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_small.py \
+          > $out/${tag}_sanitize_$tool.log 2>&1
+        echo "sanitize $tool exit=$?" >> $out/${tag}_legs.txt
+      done ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
