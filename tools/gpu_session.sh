@@ -48,6 +48,16 @@ for leg in "$@"; do
           > $out/${tag}_sanitize_$tool.log 2>&1
         echo "sanitize $tool exit=$?" >> $out/${tag}_legs.txt
       done ;;
+    ncu_full)   # one --set full capture per hot kernel
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd_dkv_kernel -c 1 \
+        -o $out/${tag}_ncu_dkv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu \
+        > $out/${tag}_ncu_dkv.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_kernel -c 2 \
+        -o $out/${tag}_ncu_gemm python tools/gemm_probe.py --preset llama \
+        > $out/${tag}_ncu_gemm.log 2>&1 ;;
+    guards)
+      timeout 600 python -m pytest tests/test_gpu_guards.py -q -s --timeout 300 -p no:cacheprovider \
+        > $out/${tag}_guards.log 2>&1 ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
