@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "lvx_common.cuh"
 #include "lvx_sm100.cuh"
@@ -224,6 +225,198 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------- CTA pairs
+// The same GEMM on cta_group::2: a pair of CTAs (one cluster) owns a
+// 256 x 256 output tile; the leader issues M = 256, N = 256 MMAs for both.
+// Operands split as the pair MMA reads them: A by M (each CTA its 128 rows),
+// B by N (each CTA 128 of the 256 columns), so each CTA stages 32 KB per
+// 64-deep K block instead of 48 KB and its tensor core reads 2/3 of the
+// operand bytes per FLOP of the 1-CTA kernel.  Each CTA's TMEM holds its 128
+// rows x 256 fp32 columns, double-buffered.  Barriers: `full` (the leader's,
+// expecting both CTAs' TMA bytes), `empty` / `acc_full` (multicast commits
+// into both CTAs), `acc_empty` (the leader's, 256 epilogue arrivals).
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2;       // this CTA's M half of A: 16 KB
+constexpr int P_B_BYTES = 128 * BK * 2;       // this CTA's N half of B: 16 KB
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int PAIR_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* acc_full = empty + P_STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto decode = [&](int u, int& m0, int& n0, int& kb0, int& kb1) {
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int split = u / tiles, t = u % tiles;
+    m0 = (t / p.n_tiles) * 256;
+    n0 = (t % p.n_tiles) * 256;
+    kb0 = split * p.kb_per_split;
+    kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (elect_one()) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      int it = 0;
+      for (int u = pair; u < p.units; u += npairs) {
+        int m0, n0, kb0, kb1;
+        decode(u, m0, n0, kb0, kb1);
+        const int ma = m0 + 128 * (int)rank, nb = n0 + 128 * (int)rank;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          if (it >= P_STAGES) mbar_wait(&empty[s], ((it / P_STAGES) - 1) & 1);
+          uint8_t* sa = sm + s * P_STAGE_BYTES;
+          uint8_t* sb = sa + P_A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+          const uint32_t lf = leader_addr(&full[s]);
+          const int k0 = kb * BK;
+          const uint64_t pol = l2_evict_last();
+          if (!A_MN) {
+            tma2_load_3d(sa, &tmA, lf, k0, ma, 0, pol);
+          } else {
+            tma2_load_3d(sa, &tmA, lf, ma, k0, 0, pol);
+            tma2_load_3d(sa + 8192, &tmA, lf, ma + 64, k0, 0, pol);
+          }
+          if (!B_MN) {
+            tma2_load_3d(sb, &tmB, lf, k0, nb, 0, pol);
+          } else {
+            tma2_load_3d(sb, &tmB, lf, nb, k0, 0, pol);
+            tma2_load_3d(sb + 8192, &tmB, lf, nb + 64, k0, 0, pol);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
+      const uint32_t base = smem_u32(sm);
+      int it = 0, lt = 0;
+      for (int u = pair; u < p.units; u += npairs, ++lt) {
+        int m0, n0, kb0, kb1;
+        decode(u, m0, n0, kb0, kb1);
+        const int buf = lt & 1;
+        if (lt >= 2) mbar_wait_cluster(&acc_empty[buf], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * 256;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          mbar_wait_cluster(&full[s], (it / P_STAGES) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = base + s * P_STAGE_BYTES, sb = sa + P_A_BYTES;
+            const uint64_t da = A_MN ? umma_desc_sw128(sa, 8192, 1024) : umma_desc_sw128(sa, 0, 1024);
+            const uint64_t db = B_MN ? umma_desc_sw128(sb, 8192, 1024) : umma_desc_sw128(sb, 0, 1024);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t oa = A_MN ? (uint64_t)((kk * 16 * 128) >> 4) : (uint64_t)((kk * 32) >> 4);
+              const uint64_t ob = B_MN ? (uint64_t)((kk * 16 * 128) >> 4) : (uint64_t)((kk * 32) >> 4);
+              mma2_bf16_ss(acc, da + oa, db + ob, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            }
+            mma2_commit_mc(&empty[s]);
+            if (kb + 1 == kb1) mma2_commit_mc(&acc_full[buf]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    int lt = 0;
+    for (int u = pair; u < p.units; u += npairs, ++lt) {
+      int m0, n0, kb0, kb1;
+      decode(u, m0, n0, kb0, kb1);
+      const int buf = lt & 1;
+      mbar_wait(&acc_full[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 128 * (int)rank + q * 32 + lane;
+      const uint32_t tbase = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < 256 / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_wait_ld();
+        const int col0 = n0 + c * 32;
+        if (row >= p.M || col0 >= p.N) continue;
+        if (p.Cf) {
+          float* dst = p.Cf + (int64_t)row * p.N + col0;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (col0 + 4 * g < p.N)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
+                           "f"(__uint_as_float(r[4 * g])), "f"(__uint_as_float(r[4 * g + 1])),
+                           "f"(__uint_as_float(r[4 * g + 2])), "f"(__uint_as_float(r[4 * g + 3]))
+                           : "memory");
+        } else {
+          __nv_bfloat16* dst = p.C + (int64_t)row * p.ldc + col0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (col0 + 8 * g >= p.N) break;
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * g + e]);
+            uint4* d4 = reinterpret_cast<uint4*>(dst + 8 * g);
+            if (p.accumulate) {
+              const uint4 old = *d4;
+              const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+                v[2 * e] += __bfloat162float(o2.x);
+                v[2 * e + 1] += __bfloat162float(o2.y);
+              }
+            }
+            *d4 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                             pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+          }
+        }
+      }
+      tc_fence_before();
+      if (rank == 0) mbar_arrive(&acc_empty[buf]);
+      else mbar_arrive_cluster(leader_addr(&acc_empty[buf]));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+
 // split-K finish: C (+)= bf16(Cf)
 __global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
                                      __nv_bfloat16* __restrict__ C, int64_t ldc, int accumulate) {
@@ -296,26 +489,66 @@ bool tc_ok(const GemmCall& g) {
          g.N % 8 == 0 && g.M < (1ll << 31) && g.N < (1ll << 31) && g.K < (1ll << 31);
 }
 
+// The split-K scratch comes from the device's default stream-ordered pool.
+// By default the pool returns freed memory to the driver at every
+// synchronisation, so the next cudaMallocAsync maps it again (~0.1-0.2 ms,
+// measured: a 0.18 ms weight-gradient GEMM took 0.35 ms per call); keep it.
+bool keep_pool_memory() {
+  static std::atomic<unsigned> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const unsigned bit = dev < 32 ? 1u << dev : 0u;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return false;
+  uint64_t keep = ~0ull;
+  if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess)
+    return false;
+  done.fetch_or(bit, std::memory_order_release);
+  return true;
+}
+
+// Split K so the work units fill whole waves of `slots` (SMs, or CTA pairs):
+// maximise units / (waves x slots) over splits with >= 8 K blocks each; more
+// splits only when they raise that efficiency by > 2 % (each split adds an
+// M x N fp32 reduce-add pass).
+int plan_splits(int tiles, int kb_total, int slots) {
+  int best = 1;
+  double best_eff = (double)tiles / (double)(((tiles + slots - 1) / slots) * slots);
+  for (int s = 2; s <= 16 && kb_total / s >= 8; ++s) {
+    const int units = tiles * s;
+    const double eff = (double)units / (double)(((units + slots - 1) / slots) * slots);
+    if (eff > best_eff + 0.02) {
+      best = s;
+      best_eff = eff;
+    }
+  }
+  return best;
+}
+
 template <bool A_MN, bool B_MN>
 int launch_tc(const GemmCall& g, cudaStream_t st) {
+  const int sms = device_sms();
+  // CTA pairs for every product with at least two 256-row bands; the 1-CTA
+  // kernel for thin ones (fewer rows than a pair tile wastes half of it)
+  const bool pairs = g.M >= 256;
+  const int tm = pairs ? 256 : BM, tn = pairs ? 256 : BN;
+  const int box_m = pairs ? 128 : BM, box_n = pairs ? 128 : BN;
   CUtensorMap ta, tb;
-  // A: [M, K] K-major box 128 rows; [K, M] MN-major boxes of 64 K rows
-  const bool okA = A_MN ? map2d(&ta, g.a, g.K, g.M, g.lda, 64) : map2d(&ta, g.a, g.M, g.K, g.lda, 128);
-  const bool okB = B_MN ? map2d(&tb, g.b, g.K, g.N, g.ldb, 64) : map2d(&tb, g.b, g.N, g.K, g.ldb, 256);
+  // A: [M, K] K-major box of box_m rows; [K, M] MN-major boxes of 64 K rows
+  const bool okA = A_MN ? map2d(&ta, g.a, g.K, g.M, g.lda, 64) : map2d(&ta, g.a, g.M, g.K, g.lda, box_m);
+  const bool okB = B_MN ? map2d(&tb, g.b, g.K, g.N, g.ldb, 64) : map2d(&tb, g.b, g.N, g.K, g.ldb, box_n);
   if (!okA || !okB) return LVX_ECUDA;
   GemmParams p{};
   p.M = (int)g.M;
   p.N = (int)g.N;
   p.K = (int)g.K;
-  p.m_tiles = (int)((g.M + BM - 1) / BM);
-  p.n_tiles = (int)((g.N + BN - 1) / BN);
+  p.m_tiles = (int)((g.M + tm - 1) / tm);
+  p.n_tiles = (int)((g.N + tn - 1) / tn);
   p.kb_total = (int)((g.K + BK - 1) / BK);
-  const int sms = device_sms();
+  const int slots = pairs ? sms / 2 : sms;
   const int tiles = p.m_tiles * p.n_tiles;
-  int splits = 1;
-  if (tiles < sms && p.kb_total >= 32)   // tall-K, few tiles: split K over the idle SMs
-    splits = std::min((2 * sms + tiles - 1) / tiles, p.kb_total / 16);
-  splits = std::max(1, splits);
+  const int splits = plan_splits(tiles, p.kb_total, slots);
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   p.units = tiles * p.splits;
@@ -325,15 +558,23 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   float* scratch = nullptr;
   if (p.splits > 1) {
     const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
+    if (!keep_pool_memory()) return LVX_ECUDA;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
       return LVX_ECUDA;
     if (cudaMemsetAsync(scratch, 0, bytes, st) != cudaSuccess) return LVX_ECUDA;
     p.Cf = scratch;
   }
-  auto kern = gemm_bf16_kernel<A_MN, B_MN>;
-  static std::atomic<unsigned> attr_done{0};
-  if (!ensure_smem_attr(kern, GEMM_SMEM, attr_done)) return LVX_ECUDA;
-  kern<<<std::min(p.units, sms), GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+  if (pairs) {
+    auto kern = gemm_bf16_pair_kernel<A_MN, B_MN>;
+    static std::atomic<unsigned> attr_done{0};
+    if (!ensure_smem_attr(kern, PAIR_SMEM, attr_done)) return LVX_ECUDA;
+    kern<<<2 * std::min(p.units, slots), GEMM_THREADS, PAIR_SMEM, st>>>(ta, tb, p);
+  } else {
+    auto kern = gemm_bf16_kernel<A_MN, B_MN>;
+    static std::atomic<unsigned> attr_done{0};
+    if (!ensure_smem_attr(kern, GEMM_SMEM, attr_done)) return LVX_ECUDA;
+    kern<<<std::min(p.units, slots), GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+  }
   note_launch();
   if (scratch) {
     const int64_t n = g.M * g.N;
