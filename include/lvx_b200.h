@@ -236,6 +236,10 @@ int lvx_peer_put(const lvx_peer_map* m, int peer, uint64_t dst_off, uint64_t dst
 int lvx_peer_signal(const lvx_peer_map* m, int peer, uint64_t flag_off, uint32_t value,
                     void* stream);
 int lvx_peer_wait(const lvx_peer_map* m, uint64_t flag_off, uint32_t value, void* stream);
+/* A dedicated non-blocking CUDA stream (a rank's compute / copy stream; thread
+ * ranks sharing one GPU must not share streams). */
+int lvx_stream_create(void** out);
+int lvx_stream_destroy(void* stream);
 
 #ifdef __cplusplus
 }

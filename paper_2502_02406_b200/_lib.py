@@ -26,7 +26,8 @@ EXPORTS = ("lvx_abi_version", "lvx_kernel_launches", "lvx_strerror", "lvx_tc_eli
            "lvx_bwd_dq_finish", "lvx_bwd_dkv", "lvx_project", "lvx_project_bwd",
            "lvx_kv_recompute", "lvx_gemm", "lvx_accumulate", "lvx_peer_create", "lvx_peer_destroy",
            "lvx_peer_base", "lvx_peer_handle_bytes", "lvx_peer_export", "lvx_peer_open",
-           "lvx_peer_attach", "lvx_peer_put", "lvx_peer_signal", "lvx_peer_wait")
+           "lvx_peer_attach", "lvx_peer_put", "lvx_peer_signal", "lvx_peer_wait",
+           "lvx_stream_create", "lvx_stream_destroy")
 
 
 class LvxView(ctypes.Structure):
@@ -100,6 +101,8 @@ def load() -> ctypes.CDLL:
         "lvx_peer_put": (i32, [vp, i32, u64, u64, vp, u64, u64, u64, vp]),
         "lvx_peer_signal": (i32, [vp, i32, u64, ctypes.c_uint32, vp]),
         "lvx_peer_wait": (i32, [vp, u64, ctypes.c_uint32, vp]),
+        "lvx_stream_create": (i32, [ctypes.POINTER(vp)]),
+        "lvx_stream_destroy": (i32, [vp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)
@@ -153,3 +156,23 @@ def check(fn: str, status: int) -> None:
 
 def stream_ptr(device: torch.device | None = None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class OwnStream:
+    """A CUDA stream of its own (lvx_stream_create) usable as a torch stream;
+    destroyed with ``close()``."""
+
+    def __init__(self, device):
+        import torch
+        self.device = torch.device(device)
+        p = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check("lvx_stream_create", load().lvx_stream_create(ctypes.byref(p)))
+        self.ptr = p.value
+        self.stream = torch.cuda.ExternalStream(self.ptr, device=self.device)
+
+    def close(self) -> None:
+        if self.ptr:
+            self.stream.synchronize()
+            load().lvx_stream_destroy(ctypes.c_void_p(self.ptr))
+            self.ptr = None

@@ -526,7 +526,8 @@ class PeerTransport:
         if self.n > self.MAXN:
             raise ClusterError(f"copy-engine transport supports at most {self.MAXN} ranks")
         self.device = torch.device(device)
-        self.copy = torch.cuda.Stream(self.device)
+        self._copy_own = _lib.OwnStream(self.device)    # never a pooled stream another rank holds
+        self.copy = self._copy_own.stream
         self.map = None
         self.capacity = 0
         self.base = 0
@@ -754,9 +755,11 @@ class PeerTransport:
 
     def close(self) -> None:
         try:
-            torch.cuda.synchronize(self.device)
+            self.copy.synchronize()
+            torch.cuda.current_stream(self.device).synchronize()
         finally:
             self._free_map()
+            self._copy_own.close()
 
 
 # ---------------------------------------------------------------------------

@@ -166,4 +166,20 @@ int lvx_peer_wait(const lvx_peer_map* m, uint64_t flag_off, uint32_t value, void
              : LVX_ECUDA;
 }
 
+// A dedicated non-blocking stream (torch's streams come from a fixed pool of
+// 32 per device handed out round-robin, so two live torch.cuda.Stream objects
+// can be the same CUDA stream; ranks sharing a GPU need streams of their own).
+int lvx_stream_create(void** out) {
+  if (!out) return LVX_EINVAL;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return LVX_ECUDA;
+  *out = st;
+  return LVX_OK;
+}
+
+int lvx_stream_destroy(void* stream) {
+  if (!stream) return LVX_OK;
+  return cudaStreamDestroy(static_cast<cudaStream_t>(stream)) == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+
 }  // extern "C"

@@ -32,6 +32,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from . import _lib
 from .comm import (ClusterAborted, ClusterSpec, CollectiveTimeout, DeviceContext, PeerTransport,
                    ThreadGroup, TransportStats, WorkerFailed, resolve_timeout)
 
@@ -71,17 +72,26 @@ def spawn_ranks(spec: ClusterSpec, body, timeout: float | None = None, device=No
     ctxs: list = [None] * n
 
     def run(rank: int) -> None:
+        own = None
         try:
             ops = ops_factory() if ops_factory is not None else None
             if device.type == "cuda":
                 torch.cuda.set_device(device)
-                stream = torch.cuda.Stream(device)
-                with torch.cuda.stream(stream):
-                    _run_one(rank, ops, stream)
+                # a stream of its own: torch's pooled streams repeat after 32,
+                # and two ranks on one stream would share its workspaces
+                own = _lib.OwnStream(device)
+                with torch.cuda.stream(own.stream):
+                    _run_one(rank, ops, own.stream)
             else:
                 _run_one(rank, ops, None)
         except BaseException as exc:   # surfaced as WorkerFailed below
-            group.fail(rank, exc)
+            group.fail(rank, exc)      # releases every rank's stream-side waits
+        finally:
+            if own is not None:
+                try:
+                    own.close()
+                except Exception:      # noqa: BLE001 - a failed rank's stream
+                    pass
 
     def _run_one(rank, ops, stream):
         ctx = DeviceContext(rank, n, group=group.rank(rank) if n > 1 else None, device=device,

@@ -58,6 +58,9 @@ for leg in "$@"; do
     guards)
       timeout 600 python -m pytest tests/test_gpu_guards.py -q -s --timeout 300 -p no:cacheprovider \
         > $out/${tag}_guards.log 2>&1 ;;
+    recompute)
+      timeout 600 python tools/bench_recompute.py --preset flamingo > $out/${tag}_recompute_flamingo.json 2>&1
+      timeout 600 python tools/bench_recompute.py --preset llama > $out/${tag}_recompute_llama.json 2>&1 ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
