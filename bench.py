@@ -317,7 +317,8 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
     import torch
     from paper_2502_02406_b200 import _lib, volumes
     from paper_2502_02406_b200.strategies import (RoundTrace, ShardSpec, lvx_backward,
-                                                  lvx_forward, ring_backward, ring_forward)
+                                                  lvx_forward, ring_backward,
+                                                  ring_backward_reference_schedule, ring_forward)
     world, rank, local, dev = env.world, env.rank, env.local, env.dev
     s_q, hq, hkv, d = CFG["s_q"], CFG["hq"], CFG["hkv"], CFG["d"]
     scale = 1.0 / d ** 0.5
@@ -516,6 +517,14 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
                                                 "partials one hop behind (overlapped)",
                                     "bytes_per_step_rank0": rtr[0][0].total_sent_bytes()
                                     + rtr[0][1].total_sent_bytes()}
+            # the Ring in the reference's own order (compute, then shift and wait)
+            ms_rref, _, *_ = timed(ctx, max(2, args.steps // 2), 1,
+                                   strategy=(ring_forward, ring_backward_reference_schedule))
+            out["ring_baseline_reference_schedule"] = {
+                "ms_per_step": ms_rref, "value": flops / (ms_rref * 1e-3) / 1e12,
+                "speedup_lvx_over_ring": ms_rref / ms,
+                "schedule": "strategies.py:314-361 order: compute, then (K, V, dK, dV) shift, "
+                            "then wait"}
     else:
         out["no_comm_ms_per_step"] = ms
         out["overhead_vs_no_comm"] = 0.0

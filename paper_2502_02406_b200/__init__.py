@@ -20,7 +20,8 @@ from .kernels import (AttentionState, GradientBundle, attention_row_stats, block
                       project_backward, validate_qkv)
 from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, StrategyKind,
                          head_parallel_backward, head_parallel_forward,
-                         lvx_backward, lvx_forward, partition_rows, ring_backward, ring_forward,
+                         lvx_backward, lvx_forward, partition_rows, ring_backward,
+                         ring_backward_reference_schedule, ring_forward,
                          run_distributed, run_rank)
 from . import analytics, tensorio, volumes
 
@@ -32,6 +33,7 @@ __all__ = [
     "StrategyKind", "TransportStats", "WorkerFailed", "attention_row_stats",
     "blockwise_attention", "blockwise_attention_backward", "default_scale", "dense_attention",
     "dense_attention_backward", "empty_state", "lvx_backward", "lvx_forward", "merge_states",
-    "partition_rows", "project", "project_backward", "ring_backward", "ring_forward",
+    "partition_rows", "project", "project_backward", "ring_backward",
+    "ring_backward_reference_schedule", "ring_forward",
     "run_distributed", "run_rank", "validate_qkv", "volumes", "analytics", "tensorio",
 ]

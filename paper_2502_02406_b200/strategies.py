@@ -661,6 +661,89 @@ def ring_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_blo
     return _cast(dq, gd), dk, dv
 
 
+def ring_backward_reference_schedule(ctx: DeviceContext, shards: ShardSpec, q_block, k_block,
+                                     v_block, state: AttentionState, do_block, scale: float,
+                                     trace: RoundTrace | None = None):
+    """The Ring backward in the reference's own order (strategies.py:314-361):
+    each round computes on the block in hand, THEN ships (K, V, dK, dV)
+    together and waits for the predecessor's — no overlap of the hop with
+    compute.  Same results and bytes as ``ring_backward``; kept as the
+    reference-faithful Ring baseline beside the overlapped one."""
+    n, i, ops = ctx.n, ctx.rank, ctx.ops
+    h, rows, d = q_block.shape
+    hk = k_block.shape[0]
+    dev = q_block.device
+    sd = ops.state_dtype(q_block.dtype)
+    gd = _grad_dtype(ops, q_block.dtype)
+    ks = shards.kv_sizes
+    mk = max(ks) if ks else 0
+    if n == 1:
+        return ring_backward(ctx, shards, q_block, k_block, v_block, state, do_block, scale,
+                             trace)
+    D = torch.empty((h, rows), dtype=sd, device=dev)
+    ops.row_stats(state.O, do_block, D)
+    L = state.L
+    dq = torch.zeros((h, rows, d), dtype=sd, device=dev)
+    with ctx.call() as call:
+        buf = call.alloc({"rec": (2, [("K", hk * mk * d, k_block.dtype),
+                                      ("V", hk * mk * d, v_block.dtype),
+                                      ("dK", hk * mk * d, sd), ("dV", hk * mk * d, sd)]),
+                          "home": (1, [("dK", hk * mk * d, sd), ("dV", hk * mk * d, sd)])})
+        R, home = buf["rec"], buf["home"][0]
+        acc_k = torch.empty((hk, ks[i], d), dtype=sd, device=dev)   # round 0's partial
+        acc_v = torch.empty((hk, ks[i], d), dtype=sd, device=dev)
+        tmp_k = torch.empty((hk * mk * d,), dtype=sd, device=dev)
+        tmp_v = torch.empty((hk * mk * d,), dtype=sd, device=dev)
+        k_cur, v_cur, blk = k_block, v_block, i
+        for r in range(n):
+            _expect(blk, (i - r) % n, f"worker {i} ring backward round {r}")
+            t0 = ops.event() if trace is not None else None
+            ws = ops.bwd_workspace(q_block, k_cur)
+            ops.bwd_dq_partial(q_block, k_cur, v_cur, L, D, do_block, scale, ws)
+            ops.bwd_dq_finish(q_block, k_cur, ws, dq, accumulate=True)
+            if r == 0:
+                ops.bwd_dkv(q_block, k_cur, v_cur, L, D, do_block, scale, acc_k, acc_v,
+                            accumulate=False)
+            else:
+                tk, tv = _shaped(tmp_k, hk, ks[blk], d), _shaped(tmp_v, hk, ks[blk], d)
+                ops.bwd_dkv(q_block, k_cur, v_cur, L, D, do_block, scale, tk, tv,
+                            accumulate=False)
+                ops.accumulate(tk, acc_k)
+                ops.accumulate(tv, acc_v)
+            t1 = ops.event() if trace is not None else None
+            sent = {}
+            nxt = (i - r - 1) % n
+            if r < n - 1:   # compute, then shift (K, V, dK, dV) and wait
+                s = R[r % 2]
+                recv = [_shaped(s["K"], hk, ks[nxt], d), _shaped(s["V"], hk, ks[nxt], d),
+                        _shaped(s["dK"], hk, ks[nxt], d), _shaped(s["dV"], hk, ks[nxt], d)]
+                dst = [_shaped(s["K"], hk, ks[blk], d), _shaped(s["V"], hk, ks[blk], d),
+                       _shaped(s["dK"], hk, ks[blk], d), _shaped(s["dV"], hk, ks[blk], d)]
+                # a slot is rewritten two rounds later, after its reader has
+                # finished with it (this wait chain orders the whole ring)
+                hop, sent = ctx.shift([k_cur, v_cur, acc_k, acc_v], recv,
+                                      ["K", "V", "dK", "dV"], dst=dst,
+                                      after=_after(ctx, 0, r, 2))
+                hop.wait()
+                if r >= 1:
+                    _release(ctx, 0, r - 1, 2)
+                k_cur, v_cur, acc_k, acc_v = recv
+                blk = nxt
+            t2 = ops.event() if trace is not None else None
+            if trace is not None:
+                trace._add_timed(ops, t0, t1, t2, sent)
+        _expect(blk, (i + 1) % n, f"worker {i} backward epilogue")
+        recv_h = [_shaped(home["dK"], hk, ks[i], d), _shaped(home["dV"], hk, ks[i], d)]
+        dst = [_shaped(home["dK"], hk, ks[blk], d), _shaped(home["dV"], hk, ks[blk], d)]
+        hop_h, epi = ctx.shift([acc_k, acc_v], recv_h, ["dK", "dV"], dst=dst)
+        hop_h.wait()
+        _release(ctx, 0, n - 2, 2)
+        dk, dv = recv_h[0].to(gd, copy=True), recv_h[1].to(gd, copy=True)
+    if trace is not None:
+        trace.epilogue_bytes_by_class = epi
+    return _cast(dq, gd), dk, dv
+
+
 def _cast(t: torch.Tensor, dt) -> torch.Tensor:
     return t if t.dtype == dt else t.to(dt)
 

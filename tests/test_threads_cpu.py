@@ -155,3 +155,33 @@ def test_message_counts_match_b200_schedule(n):
             volumes.messages_per_rank(strategy, "backward", n)
         for i in range(n):
             assert res.stats.link(i, (i + 1) % n).message_count == want, (strategy, i)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_ring_backward_reference_schedule_matches_oracle(n):
+    """The Ring backward in the reference's compute-then-shift order gives the
+    same gradients and bytes as the reference (oracle simulation)."""
+    from paper_2502_02406_b200 import volumes
+    from paper_2502_02406_b200.strategies import (RoundTrace, ShardSpec, ring_backward_reference_schedule,
+                                                  ring_forward)
+    Q, K, V, dO = orc.make_inputs(13, 29, 4, 8, seed=17, hkv=2)
+    sim = orc.simulate("ring", Q, K, V, dO, n=n)
+    sh = ShardSpec.balanced(13, 29, n)
+    T = torch.from_numpy
+
+    def body(ctx):
+        (qa, qb), (ka, kb) = sh.q_ranges[ctx.rank], sh.kv_ranges[ctx.rank]
+        q, k, v, g = T(Q[:, qa:qb]), T(K[:, ka:kb]), T(V[:, ka:kb]), T(dO[:, qa:qb])
+        st = ring_forward(ctx, sh, q, k, v, 8 ** -0.5)
+        tb = RoundTrace("ring", "backward")
+        dq, dk, dv = ring_backward_reference_schedule(ctx, sh, q, k, v, st, g, 8 ** -0.5, tb)
+        return dq.numpy(), dk.numpy(), dv.numpy(), tb.total_sent_bytes()
+
+    res = _spawn(n, body)
+    dq = np.concatenate([r[0] for r in res.results], axis=1)
+    dk = np.concatenate([r[1] for r in res.results], axis=1)
+    dv = np.concatenate([r[2] for r in res.results], axis=1)
+    assert orc.max_norm_error(dq, sim.dQ) <= 1e-12
+    assert orc.max_norm_error(dk, sim.dK) <= 1e-12
+    assert orc.max_norm_error(dv, sim.dV) <= 1e-12
+    assert [r[3] for r in res.results] == list(sim.bwd_bytes)

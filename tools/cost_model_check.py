@@ -42,7 +42,7 @@ def row(path: Path) -> dict:
     if rb:
         out["ring_over_lvx_measured"] = rb["ms_per_step"] / d["ms_per_step"]
         out["ring_over_lvx_model_calibrated"] = ring_pred / lvx_pred
-        if P2P and n > 1:   # the same with the measured NCCL shift bandwidth per hop size
+        if P2P and n > 1:   # the same with the measured shift bandwidth per hop size (p2p_bw.py)
             def at(nbytes):
                 return A.HardwareSpec(1.0, p2p_bandwidth(nbytes))
             ring_t = 0.0
@@ -79,7 +79,7 @@ def main():
     rows = [row(p) for p in paths]
     print("| n | measured ms/step | model @1419.9 TF | model calibrated | fwd round meas / model (ms) "
           "| LVX / Ring fwd hop (ms @900 GB/s) | regime (lvx / ring) | Ring/LVX meas | Ring/LVX model "
-          "| Ring/LVX model, measured NCCL GB/s |")
+          "| Ring/LVX model, measured shift GB/s |")
     print("|---|---|---|---|---|---|---|---|---|---|")
     for r in rows:
         print(f"| {r['n']} | {r['measured_step_ms']:.1f} | {r['model_step_ms_at_peak']:.1f} | "

@@ -61,6 +61,10 @@ for leg in "$@"; do
     recompute)
       timeout 600 python tools/bench_recompute.py --preset flamingo > $out/${tag}_recompute_flamingo.json 2>&1
       timeout 600 python tools/bench_recompute.py --preset llama > $out/${tag}_recompute_llama.json 2>&1 ;;
+    p2p)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29519 tools/p2p_bw.py > $out/${tag}_p2p_n${n}.json 2> $out/${tag}_p2p.err ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)

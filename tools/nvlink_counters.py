@@ -75,7 +75,7 @@ def main():
         st = lvx_forward(ctx, shards, q, k, v, scale)
         lvx_backward(ctx, shards, q, k, v, st, do, scale)
 
-    step()   # warm-up (NCCL connections)
+    step()   # warm-up (arena mapping)
     torch.cuda.synchronize()
     dist.barrier()
     h0, c0 = nvlink_bytes(handle), ctx.stats.bytes_sent_by(rank)

@@ -1,5 +1,6 @@
-"""Achieved ring-shift bandwidth over NVLink (the transport the schedulers use:
-``DeviceContext.shift`` = grouped NCCL send to (r+1)%n / recv from (r-1)%n).
+"""Achieved ring-shift bandwidth over NVLink through the transport the
+schedulers use: ``DeviceContext.shift`` = a copy-engine put into the
+successor's arena + a stream-ordered flag (comm.PeerTransport).
 
     torchrun --nproc-per-node N tools/p2p_bw.py
 
@@ -19,7 +20,6 @@ sys.path.insert(0, str(ROOT))
 
 
 def main():
-    os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl")
@@ -28,17 +28,22 @@ def main():
     out = {}
     for mib in (1, 4, 16, 64, 256, 1024):
         n = mib * (1 << 20) // 2
-        a = torch.empty(n, dtype=torch.bfloat16, device="cuda").fill_(1)
-        b = torch.empty_like(a)
-        for _ in range(3):
-            ctx.shift([a], [b], ["K"])[0].wait()
+        a = torch.empty((1, n, 1), dtype=torch.bfloat16, device="cuda").fill_(1)
+        iters = 10
+
+        def shifts(k):
+            # one scheduler call = k shifts into k receive slots of the arena
+            with ctx.call() as call:
+                slots = call.alloc({"r": (k, [("K", n, torch.bfloat16)])})["r"]
+                for j in range(k):
+                    hop, _ = ctx.shift([a], [slots[j]["K"].view(1, n, 1)], ["K"])
+                    hop.wait()
+        shifts(3)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        iters = 10
-        for _ in range(iters):
-            ctx.shift([a], [b], ["K"])[0].wait()
+        shifts(iters)
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / 1e3 / iters], device="cuda")
