@@ -65,6 +65,9 @@ for leg in "$@"; do
       n=$(nvidia-smi -L | wc -l)
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
         --master-port 29519 tools/p2p_bw.py > $out/${tag}_p2p_n${n}.json 2> $out/${tag}_p2p.err ;;
+    ce)
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29520 tools/ce_probe.py > $out/${tag}_ce_probe.json 2> $out/${tag}_ce_probe.err ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)

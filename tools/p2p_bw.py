@@ -38,7 +38,7 @@ def main():
                 for j in range(k):
                     hop, _ = ctx.shift([a], [slots[j]["K"].view(1, n, 1)], ["K"])
                     hop.wait()
-        shifts(3)
+        shifts(iters)   # warm-up with the timed call's layout (the arena is sized once)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
