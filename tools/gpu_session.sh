@@ -37,6 +37,11 @@ for leg in "$@"; do
       timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
         --master-port 29517 bench.py --gpus $n --steps 10 --warmup 3 ${BENCH_SKV:+--skv $BENCH_SKV} \
         > $out/${tag}_bench_n${n}${BENCH_SKV:+_skv$BENCH_SKV}.json 2> $out/${tag}_bench_n${n}.err ;;
+    c3_n)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29521 bench.py --gpus $n --workload c3 --steps 3 --warmup 3 --no-e2e \
+        > $out/${tag}_bench_c3_n${n}.json 2> $out/${tag}_bench_c3_n${n}.err ;;
     c5_n)
       n=$(nvidia-smi -L | wc -l)
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
