@@ -1160,10 +1160,28 @@ __global__ void dq_combine_kernel(const float* __restrict__ ws, int splits, int 
   float acc[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float* src = ws + s * stride + (size_t)gw * D + lane * PER;
+  // batches of B splits with every load in flight; summation order unchanged
+  constexpr int B = 8;
+  for (int s0 = 0; s0 < splits; s0 += B) {
+    float v[B][PER];
 #pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] += src[e];
+    for (int b = 0; b < B; ++b) {
+      const float* src = ws + (size_t)(s0 + b) * stride + (size_t)gw * D + lane * PER;
+      const bool live = s0 + b < splits;
+      if constexpr (PER == 4) {
+        const float4 t = live ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0, 0, 0, 0);
+        v[b][0] = t.x; v[b][1] = t.y; v[b][2] = t.z; v[b][3] = t.w;
+      } else {
+        const float2 t = live ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0, 0);
+        v[b][0] = t.x; v[b][1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (s0 + b >= splits) break;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[e] += v[b][e];
+    }
   }
   float* o = dQ.at(h, i) + lane * PER;
 #pragma unroll

@@ -465,22 +465,46 @@ __global__ void fwd_combine_kernel(const float* __restrict__ ws_o, const float* 
   if (gw >= (int64_t)hq * rows) return;
   const int h = (int)(gw / rows), i = (int)(gw % rows);
   const size_t stride = (size_t)hq * rows;
+  // splits in batches of B: all loads of a batch are in flight together (with
+  // one query tile per head there are few rows and up to ~64 splits, and a
+  // load-use chain per split left this kernel latency-bound); the summation
+  // order stays s = 0, 1, ... (bit-identical results)
+  constexpr int B = 8;
   float mx = -INFINITY;
-  for (int s = 0; s < splits; ++s) mx = fmaxf(mx, ws_l[s * stride + gw]);
+  for (int s0 = 0; s0 < splits; s0 += B) {
+    float lv[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      lv[b] = s0 + b < splits ? __ldg(ws_l + (size_t)(s0 + b) * stride + gw) : -INFINITY;
+#pragma unroll
+    for (int b = 0; b < B; ++b) mx = fmaxf(mx, lv[b]);
+  }
   float acc[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) acc[e] = 0.f;
   float tot = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float w = __expf(ws_l[s * stride + gw] - mx);
-    tot += w;
-    const float* src = ws_o + (s * stride + gw) * D + lane * PER;
-    if constexpr (PER == 4) {
-      const float4 v = *reinterpret_cast<const float4*>(src);
-      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
-    } else {
-      const float2 v = *reinterpret_cast<const float2*>(src);
-      acc[0] += w * v.x; acc[1] += w * v.y;
+  for (int s0 = 0; s0 < splits; s0 += B) {
+    float lv[B], v[B][PER];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const bool live = s0 + b < splits;
+      lv[b] = live ? __ldg(ws_l + (size_t)(s0 + b) * stride + gw) : -INFINITY;
+      const float* src = ws_o + ((size_t)(s0 + b) * stride + gw) * D + lane * PER;
+      if constexpr (PER == 4) {
+        const float4 t = live ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0, 0, 0, 0);
+        v[b][0] = t.x; v[b][1] = t.y; v[b][2] = t.z; v[b][3] = t.w;
+      } else {
+        const float2 t = live ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0, 0);
+        v[b][0] = t.x; v[b][1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (s0 + b >= splits) break;
+      const float w = __expf(lv[b] - mx);
+      tot += w;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[e] += w * v[b][e];
     }
   }
   float lse = mx + __logf(tot);

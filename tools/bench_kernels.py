@@ -86,6 +86,18 @@ def main():
         # tensor work actually issued: dkv 4 GEMMs, dq 3 GEMMs of 2*sq*skv*hq*d each
         res["dkv_tensor_tflops"] = 8.0 * sq * skv * hq * d / res["bwd_dkv_ms"] / 1e9
         res["dq_tensor_tflops"] = 6.0 * sq * skv * hq * d / res["bwd_dq_ms"] / 1e9
+    # HBM roofline of the K/V stream (the bound when few query rows meet many
+    # KV rows, e.g. c4round: 128 FLOP / byte in the forward): K and V read once
+    kv_bytes = 2 * skv * hkv * d * 2
+    hbm = peaks.get("hbm_gbs", 6500.0)
+    res["kv_bytes"] = kv_bytes
+    res["fwd_kv_GBps"] = kv_bytes / res["fwd_partial_ms"] / 1e6
+    res["fwd_hbm_frac"] = res["fwd_kv_GBps"] / hbm
+    res["fwd_hbm_roofline_tflops"] = ff / (kv_bytes / (hbm * 1e9)) / 1e12
+    if a.bwd:
+        res["dq_kv_GBps"] = kv_bytes / res["bwd_dq_ms"] / 1e6
+        res["dkv_bytes"] = 2 * kv_bytes if a.bf16_grads else 3 * kv_bytes   # + dK, dV written
+        res["dkv_GBps"] = res["dkv_bytes"] / res["bwd_dkv_ms"] / 1e6
     print(json.dumps(res))
 
 

@@ -73,6 +73,10 @@ for leg in "$@"; do
     ce)
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
         --master-port 29520 tools/ce_probe.py > $out/${tag}_ce_probe.json 2> $out/${tag}_ce_probe.err ;;
+    kernels)   # kernel-level rates at round shapes
+      for sh in c2round c4round c4gath c3round c2gath; do
+        timeout 300 python tools/bench_kernels.py --shape $sh --bwd --bf16-grads >> $out/${tag}_kernels.jsonl 2>&1
+      done ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
