@@ -296,7 +296,8 @@ def native_arm(args):
 
 
 def _summary(line: dict) -> dict:
-    keep = ("value", "ms_per_step", "overhead_vs_no_comm", "no_comm_ms_per_step")
+    keep = ("value", "ms_per_step", "overhead_vs_no_comm", "no_comm_ms_per_step",
+            "host_submit_ms_per_step")
     out = {"s_kv": line["config"]["s_kv"], **{k: line.get(k) for k in keep}}
     out["roofline_frac"] = line["roofline"]["frac"]
     out["fwd_tflops"] = line["roofline"]["fwd_tflops"]
@@ -359,8 +360,10 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         w0 = time.time()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        h0 = time.perf_counter()
         for _ in range(steps):
             step(c, traces, strategy)
+        host_ms = (time.perf_counter() - h0) * 1e3 / steps   # host submission time per step
         e1.record()
         torch.cuda.synchronize()
         if cs:
@@ -373,6 +376,7 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         for tf, tb in traces:
             tf.resolve()
             tb.resolve()
+        timed.host_ms = env.max_over_ranks(host_ms)
         return env.max_over_ranks(ms), traces, launches, (cs.summary() if cs else None)
 
     ms, traces, launches, clocks = timed(ctx, args.steps, args.warmup, sampler=True)
@@ -465,7 +469,10 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
                       "l2": "inputs larger than L2 (K/V shard >= 16 MiB per rank and the "
                             "step touches > 126 MB)"},
            "roofline": roofline, "comm": comm, "clocks": clocks,
-           "gpu_launches": int(launches)}
+           "gpu_launches": int(launches),
+           # host time to submit one step (Python schedulers + C ABI calls); a
+           # step whose device time is not well above it is launch-bound
+           "host_submit_ms_per_step": timed.host_ms}
 
     # --- no-communication arm and the Ring baseline
     if world > 1:

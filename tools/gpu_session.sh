@@ -42,6 +42,16 @@ for leg in "$@"; do
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
         --master-port 29521 bench.py --gpus $n --workload c3 --steps 3 --warmup 3 --no-e2e \
         > $out/${tag}_bench_c3_n${n}.json 2> $out/${tag}_bench_c3_n${n}.err ;;
+    c4_n)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29522 bench.py --gpus $n --workload c4 --steps 3 --warmup 3 --no-e2e \
+        > $out/${tag}_bench_c4_n${n}.json 2> $out/${tag}_bench_c4_n${n}.err ;;
+    c5small_n)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29523 bench.py --gpus $n --workload c5 --sweep 65536,262144 --steps 5 --warmup 3 --no-e2e \
+        > $out/${tag}_bench_c5small_n${n}.json 2> $out/${tag}_bench_c5small_n${n}.err ;;
     c5_n)
       n=$(nvidia-smi -L | wc -l)
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
