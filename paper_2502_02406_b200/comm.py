@@ -353,6 +353,11 @@ def _copy_overlap(src: torch.Tensor, dst: torch.Tensor) -> None:
     dst[:, :m].copy_(src[:, :m])
 
 
+def _rows_packed(t: torch.Tensor) -> bool:
+    """Rows contiguous within each head (any head stride)."""
+    return t.numel() == 0 or t[0].is_contiguous()
+
+
 class _Hop:
     """An in-flight shift; ``wait()`` orders the caller's stream after it."""
 
@@ -659,6 +664,18 @@ class PeerTransport:
                 continue
             if s.numel() != r.numel() or s.dtype != r.dtype:
                 raise ClusterError(f"shift mismatch {tuple(s.shape)} vs {tuple(r.shape)}")
+            if not (_rows_packed(s) and _rows_packed(r)):
+                # rows strided inside a head (heads interleaved in the rows of a
+                # projection output): one 2-D copy of the head's rows per head
+                es = s.element_size()
+                for hh in range(s.shape[0]):
+                    sh, rh = s[hh], r[hh]
+                    off = rh.data_ptr() - self.base
+                    rows = sh.shape[0]
+                    w = (sh.shape[1] if sh.dim() > 1 else 1) * es
+                    runs.append([off, rh.stride(0) * es, sh.data_ptr(), sh.stride(0) * es, w, rows,
+                                 False])
+                continue
             sp, spitch, w, h = _as_rows(s)
             rp, rpitch, w2, h2 = _as_rows(r)
             if (w, h) != (w2, h2):       # one side strided: copy per head on both
