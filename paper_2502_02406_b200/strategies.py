@@ -182,8 +182,20 @@ def _shaped(flat: torch.Tensor, h: int, rows: int, d: int | None = None) -> torc
     """[h, rows, d] (or [h, rows] for d=None) view of the prefix of a flat
     buffer: a block of any row count has the same layout on every rank, so a
     record sent as a whole lands exactly where the receiver reads it."""
-    t = flat[:h * rows * (d or 1)]
-    return t.view(h, rows) if d is None else t.view(h, rows, d)
+    cache = getattr(flat, "_lvx_shaped", None)
+    if cache is None:
+        cache = {}
+        try:
+            flat._lvx_shaped = cache    # arena views live across calls (comm._Call.alloc)
+        except (AttributeError, RuntimeError):
+            pass
+    key = (h, rows, d)
+    v = cache.get(key)
+    if v is None:
+        t = flat[:h * rows * (d or 1)]
+        v = t.view(h, rows) if d is None else t.view(h, rows, d)
+        cache[key] = v
+    return v
 
 
 def _slot_value(ctx: DeviceContext, m: int) -> int:
