@@ -9,7 +9,8 @@
 // (so each K/V tile fetched into shared memory feeds 256 query rows), and one
 // split of the resident KV block.  With a single query tile per kv head (MHA,
 // <= 128 rows; KVP instantiation) the two tiles are the same Q against the
-// even / odd KV tiles of the split, each writing its own split partial.  Warp roles (320 threads):
+// even / odd KV tiles of the split, each writing its own split partial.  Warp roles (384
+// threads, kThreads; warps 10-11 only donate registers via setmaxnreg):
 //   warps 0-3  softmax for query tile 0 (TMEM lanes 0-127, one row per thread)
 //   warps 4-7  softmax for query tile 1
 //   warp  8    TMA producer: Q tiles once, then K_j / V_j into a 5-slot
