@@ -46,8 +46,19 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef LVX_DKV_POLY
 #define LVX_DKV_POLY 2
 #endif
-constexpr int kPolyPairs = LVX_DQ_POLY;     // of every 8 column pairs, exp2 by polynomial (FMA pipe)
-constexpr int kPolyPairsDkv = LVX_DKV_POLY; // the same for the dK/dV kernel's phase A
+// At d = 64 the MMAs take half as long per step while the exponentials do
+// not, so the softmax side is rebalanced toward the FMA pipe (same-box A/B,
+// tools/ab_poly.sh: c4gath dQ +3-5 %, dK/dV +1 %; d = 128 unchanged).
+#ifndef LVX_DQ_POLY64
+#define LVX_DQ_POLY64 2
+#endif
+#ifndef LVX_DKV_POLY64
+#define LVX_DKV_POLY64 3
+#endif
+template <int D>
+constexpr int kPolyPairsD = D == 64 ? LVX_DQ_POLY64 : LVX_DQ_POLY;   // of every 8 column pairs, exp2 by polynomial (FMA pipe)
+template <int D>
+constexpr int kPolyPairsDkvD = D == 64 ? LVX_DKV_POLY64 : LVX_DKV_POLY;   // the dK/dV kernel's phase A
 #ifndef LVX_DKV_CHUNKS
 #define LVX_DKV_CHUNKS 2
 #endif
@@ -184,9 +195,10 @@ __device__ __forceinline__ int dkv_chunk_kk(int c, int j) {
 
 // phase A: P^T = exp2(S^T c + nL[q]) over this thread's 64 columns at tS; the
 // fp32 P^T stays in pf for phase B; arrive(c) after each packed chunk is stored
-template <class Arrive>
+template <int D, class Arrive>
 __device__ __forceinline__ void dkv_phase_a(uint32_t tS, uint32_t lds, float2 sc2, int debug,
                                             float2 (&pf)[32], Arrive&& arrive) {
+  constexpr int kPolyPairsDkv = kPolyPairsDkvD<D>;
   constexpr int CW = 64 / kDkvChunks;   // query columns per chunk
   uint32_t sv[2][32];
   tmem_ld32(tS, sv[0]);
@@ -475,7 +487,7 @@ bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
           mbar_arrive(bar);
         }
       };
-      dkv_phase_a(tl + C::R1 + wg * 64, ldl, sc2, p.debug, pf, [&](int c) {
+      dkv_phase_a<D>(tl + C::R1 + wg * 64, ldl, sc2, p.debug, pf, [&](int c) {
         arrive(&p_ready[c]);
         if (q4 == 0) DKV_STAMP(wg, i, 1 + c);
       });
@@ -779,7 +791,7 @@ bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_wait(s_full, ph);
       tc_fence_after();
       float2 pf[32];     // P^T in fp32 for phase B
-      dkv_phase_a(tl + C::R1 + wg * 64, lds, sc2, p.debug, pf,
+      dkv_phase_a<D>(tl + C::R1 + wg * 64, lds, sc2, p.debug, pf,
                   [&](int hh) { arrive_pair(&p_ready[hh]); });
       mbar_wait(dp_full, ph);
       tc_fence_after();
@@ -1079,7 +1091,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
               x.x = c < nvalid ? x.x : -INFINITY;
               x.y = c + 1 < nvalid ? x.y : -INFINITY;
             }
-            const float2 pq = (((c / 2) * 3) % 8) < kPolyPairs && !decltype(masked)::value
+            const float2 pq = (((c / 2) * 3) % 8) < kPolyPairsD<D> && !decltype(masked)::value
                                   ? ex2_poly2(x)
                                   : make_float2(ex2(x.x), ex2(x.y));
             pf[c / 2] = pq;
