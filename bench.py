@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--no-ring-compare", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay leg")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
                     help="BASELINE config (c2 = the headline; c3 / c5 sweep Lkv, c4 = layers "
                          "with K/V recompute)")
@@ -299,6 +300,10 @@ def _summary(line: dict) -> dict:
     keep = ("value", "ms_per_step", "overhead_vs_no_comm", "no_comm_ms_per_step",
             "host_submit_ms_per_step")
     out = {"s_kv": line["config"]["s_kv"], **{k: line.get(k) for k in keep}}
+    gr = line.get("graph_replay") or {}
+    if "ms_per_step" in gr:
+        out["graph_ms_per_step"] = gr["ms_per_step"]
+        out["graph_value"] = gr["value"]
     out["roofline_frac"] = line["roofline"]["frac"]
     out["fwd_tflops"] = line["roofline"]["fwd_tflops"]
     out["bwd_tflops"] = line["roofline"]["bwd_tflops"]
@@ -474,6 +479,11 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
            # step whose device time is not well above it is launch-bound
            "host_submit_ms_per_step": timed.host_ms}
 
+    # --- the same step recorded once as a CUDA graph and replayed (no host
+    # work per step: the kernels, copy-engine hops and one-shot flags replay)
+    if not args.no_graph:
+        out["graph_replay"] = graph_replay(env, ctx, lambda: step(ctx), args.steps, flops)
+
     # --- no-communication arm and the Ring baseline
     if world > 1:
         # the identical schedule with every hop skipped, measured as interleaved
@@ -561,6 +571,34 @@ def _ring_fits(env, shards, hq, hkv, d, dev) -> bool:
         import torch.distributed as dist
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     return bool(ok.item() > 0)
+
+
+def graph_replay(env, ctx, fn, steps, flops) -> dict:
+    """Time ``steps`` replays of ``fn`` recorded as a StepGraph (CUDA events,
+    max over ranks).  The graph and its memory pool are released after."""
+    import torch
+    from paper_2502_02406_b200.strategies import StepGraph
+    try:
+        g = StepGraph(ctx, fn)
+    except Exception as exc:  # noqa: BLE001 - reported, the eager number stands
+        return {"error": f"capture failed: {exc!r}"[:300]}
+    g.replay()
+    torch.cuda.synchronize()
+    env.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h0 = time.perf_counter()
+    for _ in range(steps):
+        g.replay()
+    host_ms = (time.perf_counter() - h0) * 1e3 / steps
+    e1.record()
+    torch.cuda.synchronize()
+    env.barrier()
+    ms = env.max_over_ranks(e0.elapsed_time(e1) / steps)
+    del g
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "value": flops / (ms * 1e-3) / 1e12,
+            "host_submit_ms_per_step": env.max_over_ranks(host_ms), "steps": steps}
 
 
 def cpu_c1_timing(reps: int = 3) -> dict:

@@ -18,7 +18,7 @@ from .kernels import (AttentionState, GradientBundle, attention_row_stats, block
                       blockwise_attention_backward, default_scale, dense_attention,
                       dense_attention_backward, empty_state, merge_states, project,
                       project_backward, validate_qkv)
-from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, StrategyKind,
+from .strategies import (RoundRecord, RoundTrace, RunResult, ShardSpec, StepGraph, StrategyKind,
                          head_parallel_backward, head_parallel_forward,
                          lvx_backward, lvx_forward, partition_rows, ring_backward,
                          ring_backward_reference_schedule, ring_forward,
@@ -30,7 +30,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttentionState", "ClusterError", "ClusterSpec", "CollectiveTimeout", "DeviceContext",
     "GradientBundle", "Instant", "RoundRecord", "RoundTrace", "RunResult", "ShardSpec",
-    "StrategyKind", "TransportStats", "WorkerFailed", "attention_row_stats",
+    "StepGraph", "StrategyKind", "TransportStats", "WorkerFailed", "attention_row_stats",
     "blockwise_attention", "blockwise_attention_backward", "default_scale", "dense_attention",
     "dense_attention_backward", "empty_state", "lvx_backward", "lvx_forward", "merge_states",
     "partition_rows", "project", "project_backward", "ring_backward",

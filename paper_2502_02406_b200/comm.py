@@ -177,9 +177,11 @@ class ThreadGroup:
         # rank, FIFO queues keyed by (src, message index)
         self.cond = threading.Condition()
         self.boxes: list = [dict() for _ in range(n)]
-        # copy-engine transport between thread ranks: the largest value whose
-        # stream-side write into rank r's flag word w has been ENQUEUED
+        # copy-engine transport between thread ranks: per rank r and flag word
+        # w, how many stream-side writes into it have been ENQUEUED, and how
+        # many of them r's waits have consumed
         self.marks: list = [dict() for _ in range(n)]
+        self.consumed: list = [dict() for _ in range(n)]
 
     def fail(self, rank: int, exc: BaseException) -> None:
         with self._lock:
@@ -196,29 +198,38 @@ class ThreadGroup:
     def aborted(self) -> bool:
         return self.first_failure is not None
 
-    def mark(self, rank: int, word: int, value: int) -> None:
+    def mark(self, rank: int, word: int) -> None:
+        """One more write into rank's flag word has been enqueued."""
         with self.cond:
             m = self.marks[rank]
-            if value > m.get(word, -1):
-                m[word] = value
-                self.cond.notify_all()
+            m[word] = m.get(word, 0) + 1
+            self.cond.notify_all()
 
-    def await_mark(self, rank: int, word: int, value: int) -> None:
-        """Block the host until a write of >= value into rank's flag word has
-        been enqueued (on any stream).  Thread ranks share one CUDA context:
-        a device-side wait enqueued before its write could deadlock against
-        any device-synchronising call (allocator, free) another rank's thread
-        makes meanwhile, so a wait is only ever enqueued behind its signal."""
+    def await_mark(self, rank: int, word: int) -> None:
+        """Block the host until a write into rank's flag word that this wait
+        has not consumed yet has been enqueued (on any stream), and consume
+        it.  Thread ranks share one CUDA context: a device-side wait enqueued
+        before its write could deadlock against any device-synchronising call
+        (allocator growth, free) another rank's thread makes meanwhile, so a
+        wait is only ever enqueued behind its signal."""
         deadline = time.monotonic() + self.timeout
         with self.cond:
-            while self.marks[rank].get(word, -1) < value:
+            c = self.consumed[rank]
+            while self.marks[rank].get(word, 0) <= c.get(word, 0):
                 if self.aborted:
                     raise ClusterAborted(f"worker {rank}: cluster aborted while waiting for a hop")
                 now = time.monotonic()
                 if now >= deadline:
-                    raise CollectiveTimeout(f"worker {rank}: hop (flag {word} >= {value}) did "
-                                            f"not arrive within {self.timeout}s")
+                    raise CollectiveTimeout(f"worker {rank}: hop (flag {word}) did not arrive "
+                                            f"within {self.timeout}s")
                 self.cond.wait(timeout=deadline - now)
+            c[word] = c.get(word, 0) + 1
+
+    def reset_marks(self, rank: int) -> None:
+        """rank's flag words were re-created at zero (a new arena)."""
+        with self.cond:
+            self.marks[rank] = {}
+            self.consumed[rank] = {}
 
     def put(self, dst: int, key, payload) -> None:
         with self.cond:
@@ -506,20 +517,24 @@ class PeerTransport:
     """Copy-engine hops into symmetric arenas (see the module docstring).
 
     Arena = data region (laid out per scheduler call by ``DeviceContext.call``)
-    + a flag region of u32 words at the end:
-      READY[k * 16 + src]  message k of the current call from rank src landed
-                           (value = call epoch)
-      FREE[c * 16 + s]     the receiver released slot s of channel c
-                           (value = epoch * 4096 + channel message + 1)
-      EPOCH[src]           rank src finished call `value` (its arena is reusable)
-    Every rank issues the same sequence of calls and messages, so flag values
-    are known on both sides without any host exchange."""
+    + a flag region of u32 words at the end.  Flags are one-shot: the writer
+    sets a word to 1 (fenced behind its copies), its single consumer waits for
+    >= 1 and resets it to 0 on the same stream, and every word is written and
+    consumed at most once per call:
+      READY[k * 16 + src]  message k of this call from rank src has landed
+      FREE[c * 256 + m]    the receiver is done with message m of channel c
+                           (the sender may rewrite that slot)
+      EPOCH[src]           rank src finished its previous call (its arena and
+                           its reads of ours are done); consumed by begin()
+    The values never change, so a recorded step replays as a CUDA graph
+    (``strategies.StepGraph``), and no host exchange is needed per call."""
 
     kind = "copy-engine"
     MAXN = 16
     READY, NREADY = 0, 768 * 16
     FREE = READY + NREADY
-    EPOCH = FREE + 64 * 16
+    FREE_PER_CHANNEL = 256
+    EPOCH = FREE + 2 * FREE_PER_CHANNEL
     FLAG_WORDS = 16384
     FLAG_BYTES = FLAG_WORDS * 4
 
@@ -538,7 +553,6 @@ class PeerTransport:
         self.base = 0
         self.arena: torch.Tensor | None = None
         self.epoch = 0
-        self._touched: set = set()
         self._aborted = False
         self.tg = coll.group.group if coll.threaded else None
         if coll.threaded:
@@ -574,13 +588,11 @@ class PeerTransport:
         self.base = int(self.lib.lvx_peer_base(m))
         self.capacity = cap
         self.arena = self._wrap(self.base, cap + self.FLAG_BYTES)
-        # the previous call's end-of-call flags live in the freed arena
-        flags = self.arena[cap:].view(torch.int32)
-        flags[self.EPOCH:self.EPOCH + self.MAXN].fill_(self.epoch)
+        # the new arena's flags are zero (lvx_peer_create): this call's EPOCH
+        # handshake was consumed in the old one by begin()
         torch.cuda.synchronize(self.device)
         if self.tg is not None:
-            for p in range(self.n):
-                self.tg.mark(self.rank, self.EPOCH + p, self.epoch)
+            self.tg.reset_marks(self.rank)
         if self.coll.threaded:
             maps = self.coll.all_gather_object(m.value)
             for p in range(self.n):
@@ -598,7 +610,6 @@ class PeerTransport:
                     with torch.cuda.device(self.device):
                         _lib.check("lvx_peer_open", self.lib.lvx_peer_open(m, p, hbuf))
         self.coll.barrier()
-        self._touched = set()
 
     def alloc(self, nbytes: int, device) -> torch.Tensor:
         self.reserve(nbytes)
@@ -628,10 +639,17 @@ class PeerTransport:
 
     # -- calls and hops -----------------------------------------------------
     def begin(self):
+        """A call starts: the copy stream waits until every peer finished its
+        previous call (so it is no longer reading our arena or writing into
+        the slots this call will reuse)."""
         if self._aborted:
             raise ClusterAborted(f"worker {self.rank}: transport aborted")
         self.epoch += 1
-        self._touched = set()
+        if self.map is not None:
+            cs = self.copy.cuda_stream
+            for p in range(self.n):
+                if p != self.rank:
+                    self._wait(self.EPOCH + p, cs)
 
     def end(self):
         """The caller's arena is free once its compute stream gets here; tell
@@ -644,7 +662,7 @@ class PeerTransport:
         cs = self.copy.cuda_stream
         for p in range(self.n):
             if p != self.rank:
-                self._signal(p, self.EPOCH + self.rank, self.epoch, cs)
+                self._signal(p, self.EPOCH + self.rank, cs)
         done = torch.cuda.Event()
         done.record(self.copy)
         cur.wait_event(done)
@@ -708,28 +726,25 @@ class PeerTransport:
         ev.record(cur)
         self.copy.wait_event(ev)
         cs = self.copy.cuda_stream
-        if to not in self._touched:     # the successor finished its previous call
-            self._touched.add(to)
-            self._wait(self.EPOCH + to, self.epoch - 1, cs)
         if after is not None:           # the successor released the slot
-            word, value = after
-            self._wait(self.FREE + word, value, cs)
+            self._wait(self.FREE + after[0], cs)
         self._put_many(to, send, dst)
-        self._signal(to, self.READY + k * self.MAXN + self.rank, self.epoch, cs)
+        self._signal(to, self.READY + k * self.MAXN + self.rank, cs)
 
         def wait():
-            self._wait(self.READY + k * self.MAXN + frm, self.epoch,
+            self._wait(self.READY + k * self.MAXN + frm,
                        torch.cuda.current_stream(self.device).cuda_stream)
         return _Hop(wait)
 
     def release(self, word: int, value: int, peer: int) -> None:
-        """Tell ``peer`` (the sender) that slot ``word`` may be overwritten once
-        the compute stream gets here (and our own sends from it are done)."""
+        """Tell ``peer`` (the sender) that the message behind FREE word
+        ``word`` is consumed, once the compute stream gets here (and our own
+        sends from that slot, earlier on the copy stream, are done)."""
         cur = torch.cuda.current_stream(self.device)
         ev = torch.cuda.Event()
         ev.record(cur)
         self.copy.wait_event(ev)
-        self._signal(peer, self.FREE + word, value, self.copy.cuda_stream)
+        self._signal(peer, self.FREE + word, self.copy.cuda_stream)
 
     def all_to_all(self, chunks, recv, dst, rank: int, k: int):
         cur = torch.cuda.current_stream(self.device)
@@ -740,17 +755,14 @@ class PeerTransport:
         for w in range(self.n):
             if w == rank:
                 continue
-            if w not in self._touched:
-                self._touched.add(w)
-                self._wait(self.EPOCH + w, self.epoch - 1, cs)
             self._put_many(w, chunks[w], dst[w])
-            self._signal(w, self.READY + k * self.MAXN + rank, self.epoch, cs)
+            self._signal(w, self.READY + k * self.MAXN + rank, cs)
 
         def wait():
             st = torch.cuda.current_stream(self.device).cuda_stream
             for w in range(self.n):
                 if w != rank:
-                    self._wait(self.READY + k * self.MAXN + w, self.epoch, st)
+                    self._wait(self.READY + k * self.MAXN + w, st)
         return _Hop(wait)
 
     def abort(self) -> None:
@@ -760,8 +772,8 @@ class PeerTransport:
         if self.arena is None:
             return
         s = torch.cuda.Stream(self.device)
-        with torch.cuda.stream(s):
-            self.arena[self.capacity:].view(torch.int32).fill_(1 << 30)
+        with torch.cuda.stream(s):   # every pending one-shot wait passes
+            self.arena[self.capacity:].view(torch.int32).fill_(1)
 
     def _free_map(self) -> None:
         if self.map is not None:

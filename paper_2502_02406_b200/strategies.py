@@ -198,21 +198,17 @@ def _shaped(flat: torch.Tensor, h: int, rows: int, d: int | None = None) -> torc
     return v
 
 
-def _slot_value(ctx: DeviceContext, m: int) -> int:
-    """Flag value released for message m of a slot channel in this call."""
-    return (ctx.epoch * 4096 + m + 1) & 0xFFFFFFFF
-
-
 def _after(ctx: DeviceContext, chan: int, m: int, slots: int):
-    """Message m of channel ``chan`` reuses slot m % slots: wait until the
-    receiver released message m - slots (earlier calls: the epoch fence)."""
+    """Message m of channel ``chan`` reuses slot m % slots: it waits until the
+    receiver released message m - slots (one FREE word per message, so every
+    word is written and consumed once per call)."""
     if m < slots:
         return None
-    return (chan * 16 + m % slots, _slot_value(ctx, m - slots))
+    return (chan * 256 + (m - slots), 0)
 
 
 def _release(ctx: DeviceContext, chan: int, m: int, slots: int) -> None:
-    ctx.release(chan * 16 + m % slots, _slot_value(ctx, m))
+    ctx.release(chan * 256 + m, 0)
 
 
 @dataclass
@@ -894,6 +890,48 @@ def head_parallel_backward(ctx: DeviceContext, shards: ShardSpec, saved, do_bloc
         trace.section("bwd_kernel", ops, t1, t2)
         trace.section("all_to_all", ops, t0, t1)
     return res
+
+
+# ---------------------------------------------------------------------------
+# one rank's step as a CUDA graph
+# ---------------------------------------------------------------------------
+
+class StepGraph:
+    """One rank's step — e.g. ``lvx_forward`` + ``lvx_backward`` of a layer on
+    fixed device buffers — recorded once as a CUDA graph and replayed.
+
+    The schedulers issue ~10 kernel launches, ~10 copies and ~20 stream-side
+    flag operations per ring round from Python; at small shards (C4 at n = 8,
+    Lkv 64K at n >= 4) that host time is as long as the device work.  A replay
+    is one host call.  Everything the schedulers do is capturable: kernels,
+    copy-engine puts into peer arenas, one-shot flag writes / waits with
+    constant values (comm.PeerTransport), and the side stream's fork / join
+    through events.  Collective: every rank records (the flags pair up at
+    capture like at run time) and every rank replays the same number of times.
+    ``fn`` must not need tracing, host sync or new arena space after
+    ``warmup`` eager runs (which size the arena and the workspaces)."""
+
+    def __init__(self, ctx: DeviceContext, fn, warmup: int = 2):
+        self.ctx = ctx
+        for _ in range(warmup):
+            fn()
+        ctx.synchronize()
+        ctx.barrier()
+        from . import _lib
+        self.graph = torch.cuda.CUDAGraph()
+        # a capture stream of its own (torch's default one comes from the
+        # shared pool, and thread ranks record concurrently)
+        self._stream = _lib.OwnStream(ctx.device)
+        with torch.cuda.graph(self.graph, stream=self._stream.stream,
+                              capture_error_mode="thread_local"):
+            self.outputs = fn()
+        ctx.barrier()
+
+    def replay(self):
+        """Runs the recorded step on the current stream; returns the outputs
+        of the recorded call (overwritten by every replay)."""
+        self.graph.replay()
+        return self.outputs
 
 
 # ---------------------------------------------------------------------------
