@@ -618,19 +618,21 @@ class PeerTransport:
     def _flag(self, word: int) -> int:
         return self.capacity + 4 * word
 
-    def _signal(self, peer: int, word: int, value: int, stream) -> None:
-        """peer's flag word <- value, stream-ordered after prior work."""
+    def _signal(self, peer: int, word: int, stream) -> None:
+        """peer's flag word <- 1, stream-ordered after prior work."""
         self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
-            self.map, peer, self._flag(word), value & 0xFFFFFFFF, stream))
+            self.map, peer, self._flag(word), 1, stream))
         if self.tg is not None:
-            self.tg.mark(peer, word, value)
+            self.tg.mark(peer, word)
 
-    def _wait(self, word: int, value: int, stream) -> None:
-        """stream waits until this rank's flag word >= value."""
+    def _wait(self, word: int, stream) -> None:
+        """stream waits until this rank's flag word is set, then clears it."""
         if self.tg is not None:
-            self.tg.await_mark(self.rank, word, value)
+            self.tg.await_mark(self.rank, word)
         self._check("lvx_peer_wait", self.lib.lvx_peer_wait(
-            self.map, self._flag(word), value & 0xFFFFFFFF, stream))
+            self.map, self._flag(word), 1, stream))
+        self._check("lvx_peer_signal", self.lib.lvx_peer_signal(
+            self.map, self.rank, self._flag(word), 0, stream))
 
     def _check(self, fn: str, st: int) -> None:
         if st != 0:
