@@ -657,9 +657,10 @@ def layer_arm(args, env):
             saved.append(sv)
         gx, dy = go, torch.zeros_like(y, dtype=torch.float32)
         for w, sv in zip(reversed(layers), reversed(saved)):
-            gr = ca_backward(ctx, sh, gx, sv, y, w, counter=counter, group=env.group)
+            # every layer's dY is reduce-added into the fp32 dy in its GEMM
+            gr = ca_backward(ctx, sh, gx, sv, y, w, counter=counter, group=env.group,
+                             d_y_acc=dy)
             gx = gr.d_x
-            dy += gr.d_y
         return gx, dy
 
     def timed(policy, steps, warm, sampler=False):

@@ -141,6 +141,7 @@ struct GemmCall {
   void* c;
   int64_t ldc;
   bool accumulate;
+  int32_t c_dtype;   // = dtype, or LVX_F32 for bf16 operands into an fp32 C
 };
 int gemm(const GemmCall& g, cudaStream_t st);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (null if absent)

@@ -51,7 +51,9 @@ struct GemmParams {
   int m_tiles, n_tiles, kb_total, kb_per_split, splits, units;
   __nv_bfloat16* C;
   int64_t ldc;
-  float* Cf;          // split-K fp32 partial sums ([M, N], ld N), else null
+  float* Cf;          // fp32 output: split-K scratch or the caller's fp32 C, else null
+  int64_t ldcf;       // its leading dimension
+  int f32_store;      // 1: plain stores into Cf (one split, overwrite); 0: reduce-add
   int accumulate;     // bf16 C += A B
 };
 
@@ -181,14 +183,20 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.N + col0;
+          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            if (col0 + 4 * g < p.N)
+          for (int g = 0; g < 8; ++g) {
+            if (col0 + 4 * g >= p.N) break;
+            const float4 v4 = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                          __uint_as_float(r[4 * g + 2]),
+                                          __uint_as_float(r[4 * g + 3]));
+            if (p.f32_store)
+              *reinterpret_cast<float4*>(dst + 4 * g) = v4;
+            else
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
-                           "f"(__uint_as_float(r[4 * g])), "f"(__uint_as_float(r[4 * g + 1])),
-                           "f"(__uint_as_float(r[4 * g + 2])), "f"(__uint_as_float(r[4 * g + 3]))
+                           "f"(v4.x), "f"(v4.y), "f"(v4.z), "f"(v4.w)
                            : "memory");
+          }
         } else {
           __nv_bfloat16* dst = p.C + (int64_t)row * p.ldc + col0;
 #pragma unroll
@@ -372,14 +380,20 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.N + col0;
+          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            if (col0 + 4 * g < p.N)
+          for (int g = 0; g < 8; ++g) {
+            if (col0 + 4 * g >= p.N) break;
+            const float4 v4 = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                          __uint_as_float(r[4 * g + 2]),
+                                          __uint_as_float(r[4 * g + 3]));
+            if (p.f32_store)
+              *reinterpret_cast<float4*>(dst + 4 * g) = v4;
+            else
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
-                           "f"(__uint_as_float(r[4 * g])), "f"(__uint_as_float(r[4 * g + 1])),
-                           "f"(__uint_as_float(r[4 * g + 2])), "f"(__uint_as_float(r[4 * g + 3]))
+                           "f"(v4.x), "f"(v4.y), "f"(v4.z), "f"(v4.w)
                            : "memory");
+          }
         } else {
           __nv_bfloat16* dst = p.C + (int64_t)row * p.ldc + col0;
 #pragma unroll
@@ -430,9 +444,9 @@ __global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
 
 // ---------------------------------------------------------------- SIMT
 // One output element per thread; op(A)[m, k] = A[m * lda + k] or A[k * lda + m].
-template <typename T, typename Acc>
+template <typename T, typename Acc, typename TO = T>
 __global__ void gemm_simt_kernel(const T* __restrict__ A, int64_t lda, bool ta,
-                                 const T* __restrict__ B, int64_t ldb, bool tb, T* __restrict__ C,
+                                 const T* __restrict__ B, int64_t ldb, bool tb, TO* __restrict__ C,
                                  int64_t ldc, int64_t M, int64_t N, int64_t K, bool accumulate) {
   constexpr int TS = 16;
   __shared__ Acc sa[TS][TS + 1], sb[TS][TS + 1];
@@ -452,18 +466,18 @@ __global__ void gemm_simt_kernel(const T* __restrict__ A, int64_t lda, bool ta,
     __syncthreads();
   }
   if (m < M && n < N) {
-    T* c = C + m * ldc + n;
-    *c = from_acc<T>(accumulate ? acc + to_acc<Acc>(*c) : acc);
+    TO* c = C + m * ldc + n;
+    *c = from_acc<TO>(accumulate ? acc + to_acc<Acc>(*c) : acc);
   }
 }
 
-template <typename T, typename Acc>
+template <typename T, typename Acc, typename TO = T>
 int launch_simt(const GemmCall& g, cudaStream_t st) {
   dim3 block(16, 16), grid((unsigned)((g.N + 15) / 16), (unsigned)((g.M + 15) / 16));
   if (grid.y > 65535) return LVX_EUNSUPPORTED;
-  gemm_simt_kernel<T, Acc><<<grid, block, 0, st>>>(
+  gemm_simt_kernel<T, Acc, TO><<<grid, block, 0, st>>>(
       static_cast<const T*>(g.a), g.lda, g.ta, static_cast<const T*>(g.b), g.ldb, g.tb,
-      static_cast<T*>(g.c), g.ldc, g.M, g.N, g.K, g.accumulate);
+      static_cast<TO*>(g.c), g.ldc, g.M, g.N, g.K, g.accumulate);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
@@ -484,8 +498,9 @@ bool map2d(CUtensorMap* m, const void* p, int64_t rows, int64_t cols, int64_t ld
 
 bool tc_ok(const GemmCall& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int64_t ldc_align = g.c_dtype == LVX_F32 ? 4 : 8;   // 16-byte rows
   return g.dtype == LVX_BF16 && is_sm100() && g.M > 0 && g.N > 0 && g.K > 0 && al16(g.a) &&
-         al16(g.b) && al16(g.c) && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0 &&
+         al16(g.b) && al16(g.c) && g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % ldc_align == 0 &&
          g.N % 8 == 0 && g.M < (1ll << 31) && g.N < (1ll << 31) && g.K < (1ll << 31);
 }
 
@@ -556,13 +571,24 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   p.ldc = g.ldc;
   p.accumulate = g.accumulate ? 1 : 0;
   float* scratch = nullptr;
-  if (p.splits > 1) {
+  if (g.c_dtype == LVX_F32) {
+    // fp32 C: stored directly (one split, overwrite) or reduce-added into
+    // (accumulate, or several splits over a zeroed C); no scratch, no finish
+    p.C = nullptr;
+    p.Cf = static_cast<float*>(g.c);
+    p.ldcf = g.ldc;
+    p.f32_store = (p.splits == 1 && !g.accumulate) ? 1 : 0;
+    if (p.splits > 1 && !g.accumulate &&
+        cudaMemset2DAsync(g.c, g.ldc * 4, 0, g.N * 4, g.M, st) != cudaSuccess)
+      return LVX_ECUDA;
+  } else if (p.splits > 1) {
     const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
     if (!keep_pool_memory()) return LVX_ECUDA;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
       return LVX_ECUDA;
     if (cudaMemsetAsync(scratch, 0, bytes, st) != cudaSuccess) return LVX_ECUDA;
     p.Cf = scratch;
+    p.ldcf = g.N;
   }
   if (pairs) {
     auto kern = gemm_bf16_pair_kernel<A_MN, B_MN>;
@@ -592,10 +618,12 @@ int gemm(const GemmCall& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return LVX_OK;
   if (g.K <= 0) {   // empty contraction: C = 0, or unchanged when accumulating
     if (g.accumulate) return LVX_OK;
-    const size_t es = g.dtype == LVX_F64 ? 8 : (g.dtype == LVX_F32 ? 4 : 2);
+    const size_t es = g.c_dtype == LVX_F64 ? 8 : (g.c_dtype == LVX_F32 ? 4 : 2);
     return cudaMemset2DAsync(g.c, g.ldc * es, 0, g.N * es, g.M, st) == cudaSuccess ? LVX_OK
                                                                                     : LVX_ECUDA;
   }
+  if (g.c_dtype == LVX_F32 && g.dtype == LVX_BF16 && !tc_ok(g))
+    return launch_simt<__nv_bfloat16, float, float>(g, st);
   if (tc_ok(g)) {
     if (!g.ta && !g.tb) return launch_tc<false, true>(g, st);
     if (!g.ta && g.tb) return launch_tc<false, false>(g, st);

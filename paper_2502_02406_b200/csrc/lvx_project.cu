@@ -29,7 +29,7 @@ int gemm_rm(cudaStream_t st, int32_t dt, bool ta, bool tb, int64_t M, int64_t N,
     GemmCall g{dt, M, N, K,
                static_cast<const char*>(A) + b * sA * es, lda, ta,
                static_cast<const char*>(B) + b * sB * es, ldb, tb,
-               static_cast<char*>(C) + b * sC * es, ldc, accumulate};
+               static_cast<char*>(C) + b * sC * es, ldc, accumulate, dt};
     const int s = gemm(g, st);
     if (s) return s;
   }
@@ -136,11 +136,13 @@ int lvx_project_bwd(const lvx_matrix* x, const lvx_matrix* w, const lvx_view* do
 extern "C" int lvx_gemm(const lvx_matrix* a, int ta, const lvx_matrix* b, int tb,
                         const lvx_matrix* c, int accumulate, void* stream) {
   if (!mat_ok(a) || !mat_ok(b) || !mat_ok(c)) return LVX_EINVAL;
-  if (a->dtype != b->dtype || a->dtype != c->dtype) return LVX_EDTYPE;
+  if (a->dtype != b->dtype) return LVX_EDTYPE;
+  // c in the operands' dtype, or fp32 for bf16 operands (an fp32 accumulator)
+  if (c->dtype != a->dtype && !(a->dtype == LVX_BF16 && c->dtype == LVX_F32)) return LVX_EDTYPE;
   const int64_t M = ta ? a->cols : a->rows, K = ta ? a->rows : a->cols;
   const int64_t Kb = tb ? b->cols : b->rows, N = tb ? b->rows : b->cols;
   if (K != Kb || c->rows != M || c->cols != N) return LVX_EINVAL;
   GemmCall g{a->dtype, M, N, K, a->data, a->row_stride, ta != 0, b->data, b->row_stride,
-             tb != 0, c->data, c->row_stride, accumulate != 0};
+             tb != 0, c->data, c->row_stride, accumulate != 0, c->dtype};
   return gemm(g, static_cast<cudaStream_t>(stream));
 }

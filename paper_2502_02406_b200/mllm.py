@@ -313,7 +313,10 @@ def mllm_backward(d_out: torch.Tensor, saved: SavedActivations, y: torch.Tensor,
     scale = default_scale(config.d)
     ca_set = set(config.ca_positions)
     g = d_out
-    d_y = torch.zeros_like(y)
+    # the visual tokens' gradient sums over the CA layers (mllm.py:368); each
+    # layer's dY is reduce-added into this accumulator inside its GEMM
+    d_y_acc = torch.zeros(y.shape, dtype=torch.float64 if y.dtype == torch.float64
+                          else torch.float32, device=y.device)
     ca_grads: dict = {}
     lm_grads: list = [None] * config.num_lm_blocks
     for blk in reversed(range(config.num_lm_blocks)):
@@ -331,10 +334,11 @@ def mllm_backward(d_out: torch.Tensor, saved: SavedActivations, y: torch.Tensor,
             if blk not in saved.ca:
                 raise ValueError(f"layer {blk}: missing saved activations")
             gr: CrossAttentionGrads = ca_backward(ctx, shards, g, saved.ca[blk], y,
-                                                  params.ca[blk], scale, counter=counter)
-            d_y += gr.d_y
+                                                  params.ca[blk], scale, counter=counter,
+                                                  d_y_acc=d_y_acc)
             ca_grads[blk] = gr
             g = gr.d_x
+    d_y = d_y_acc.to(y.dtype)
     return MllmGradients(d_x0=g, d_y=d_y, ca=ca_grads, lm=lm_grads)
 
 

@@ -58,7 +58,15 @@ class CrossAttentionWeights:
         return self.w_q.shape[1] // self.hq
 
     def kv_weight(self) -> torch.Tensor:
-        return torch.cat([self.w_k, self.w_v], dim=1)
+        """[W_K | W_V] as one [e, 2*hkv*d] matrix (one GEMM for K and V),
+        built once and rebuilt only when either weight changes (in place or
+        by reassignment)."""
+        key = (self.w_k.data_ptr(), self.w_k._version, self.w_v.data_ptr(), self.w_v._version)
+        cached = getattr(self, "_wkv", None)
+        if cached is None or cached[0] != key:
+            cached = (key, torch.cat([self.w_k, self.w_v], dim=1))
+            object.__setattr__(self, "_wkv", cached)
+        return cached[1]
 
 
 @dataclass
@@ -192,9 +200,15 @@ def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: to
 def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved: SavedCA,
                 y_i: torch.Tensor, w: CrossAttentionWeights, scale: float | None = None,
                 strategy: str = "lvx", counter: OpCounter | None = None,
-                group=None) -> CrossAttentionGrads:
+                group=None, d_y_acc: torch.Tensor | None = None) -> CrossAttentionGrads:
     """Backward of ``ca_forward`` (``src/mllm.py:343-370``).  Weight gradients
-    are all-reduced over the process group when n > 1."""
+    are all-reduced over the process group when n > 1.
+
+    ``d_y_acc``: an fp32 [S_kv, e] accumulator of the visual tokens' gradient
+    over the CA layers that share y (``src/mllm.py:368`` ``d_y +=``).  Given,
+    this layer's dY = [dK|dV] [W_K|W_V]^T is reduce-added into it inside the
+    GEMM's epilogue (no bf16 dY, no separate add pass) and returned as
+    ``d_y``; else a fresh dY in y's dtype is returned."""
     scale = default_scale(w.d) if scale is None else scale
     dt = g_i.dtype
     d_o = _heads(_mm(ctx, g_i, w.w_o, tb=True), w.hq)                  # g W_O^T
@@ -210,7 +224,7 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
             counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
             counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
         dq, d_y, g_wkv = _backward_chunked(ctx, q, y_i, w, wkv, saved.state,
-                                           d_o.to(q.dtype), scale, chunk)
+                                           d_o.to(q.dtype), scale, chunk, d_y_acc)
         dq = _flat(dq.to(dt))
     else:
         if saved.policy is ActivationPolicy.STORE_KV:
@@ -225,9 +239,14 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
         del k, v
         dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
         dkv = torch.cat([dk, dv], dim=1)
-        d_y = torch.empty_like(y_i)
         g_wkv = torch.empty_like(wkv)
-        ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
+        if d_y_acc is not None:
+            ctx.ops.gemm(dkv, False, wkv, True, d_y_acc, accumulate=True)   # += dKV W^T
+            ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
+            d_y = d_y_acc
+        else:
+            d_y = torch.empty_like(y_i)
+            ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
     d_x = torch.empty_like(g_i)
     g_wq = torch.empty_like(w.w_q)
     ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
@@ -243,18 +262,19 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
 
 
 def _backward_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, wkv, state,
-                      d_o, scale: float, chunk: int):
+                      d_o, scale: float, chunk: int, d_y_acc=None):
     """n = 1 backward over K/V chunks: per chunk re-project K/V, add its dQ
     contribution (fp32, in place), compute its dK/dV and fold them into the
-    chunk's d_y rows and the K/V weight gradient.  Returns (dQ, d_y, g_wkv)."""
+    chunk's d_y rows (or reduce-add them into ``d_y_acc``) and into the fp32
+    K/V weight gradient (the GEMM accumulates across chunks in its epilogue).
+    Returns (dQ, d_y, g_wkv)."""
     ops = ctx.ops
     sd = ops.state_dtype(q.dtype)
     D = torch.empty(state.L.shape, dtype=sd, device=q.device)
     ops.row_stats(state.O, d_o, D)
     dq = torch.empty(q.shape, dtype=sd, device=q.device)
-    d_y = torch.empty_like(y)
-    g_wkv = torch.zeros(wkv.shape, dtype=sd, device=y.device)
-    part = torch.empty_like(wkv)
+    d_y = d_y_acc if d_y_acc is not None else torch.empty_like(y)
+    g_wkv = torch.empty(wkv.shape, dtype=ops.state_dtype(wkv.dtype), device=y.device)
     hkd = w.hkv * w.d
     for c, (a, b) in enumerate(_row_chunks(y.shape[0], chunk)):
         k, v = project_kv(ctx, y[a:b], w)
@@ -265,8 +285,8 @@ def _backward_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, wkv, s
         ops.bwd_dkv(q, k, v, state.L, D, d_o, scale, _heads(dkv[:, :hkd], w.hkv),
                     _heads(dkv[:, hkd:], w.hkv), accumulate=False)
         del k, v
-        ops.project_backward(y[a:b], wkv, _heads(dkv, 2 * w.hkv), d_y[a:b], part)
-        g_wkv += part
+        ops.gemm(dkv, False, wkv, True, d_y[a:b], accumulate=d_y_acc is not None)   # dKV W^T
+        ops.gemm(y[a:b], True, dkv, False, g_wkv, accumulate=c > 0)                # y^T dKV
     return dq, d_y, g_wkv.to(wkv.dtype)
 
 

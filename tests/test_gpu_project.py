@@ -141,3 +141,23 @@ def test_simt_gemm_exact_dtypes(dt):
     K.gemm_into(a, False, b, True, c)
     ref = a.double() @ b.double().T
     assert _err(c, ref) <= (1e-6 if dt == torch.float32 else 1e-13)
+
+
+@pytest.mark.parametrize("shape", [(300, 264, 200), (256, 256, 65536), (1000, 1024, 512)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_gemm_bf16_into_fp32(shape, accumulate):
+    """bf16 operands into an fp32 C (the visual tokens' gradient accumulator
+    shared by the CA layers): stored or reduce-added in the epilogue, one or
+    several K splits.  Only fp32 summation order differs from torch (1e-5)."""
+    from paper_2502_02406_b200 import kernels as K
+    M, N, Kd = shape
+    a, b = _bf(M, Kd, seed=31), _bf(N, Kd, seed=32)
+    ref = a.float() @ b.float().T
+    c0 = torch.randn(M, N, device="cuda") if accumulate else torch.full((M, N), float("nan"),
+                                                                         device="cuda")
+    c = c0.clone()
+    K.gemm_into(a, False, b, True, c, accumulate=accumulate)
+    want = ref + c0 if accumulate else ref
+    e = _err(c, want)
+    print(f"\ngemm bf16->fp32 {shape} acc={accumulate}: {e:.2e}")
+    assert e <= 1e-5

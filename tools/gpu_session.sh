@@ -63,6 +63,10 @@ for leg in "$@"; do
           > $out/${tag}_sanitize_$tool.log 2>&1
         echo "sanitize $tool exit=$?" >> $out/${tag}_legs.txt
       done ;;
+    launches_c4)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+        --log-file $out/${tag}_launches_c4.csv python bench.py --workload c4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph \
+        > $out/${tag}_launches_c4.log 2>&1 ;;
     ncu_full)   # one --set full capture per hot kernel
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd_dkv_kernel -c 1 \
         -o $out/${tag}_ncu_dkv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu \
