@@ -234,11 +234,17 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
             if counter is not None:
                 counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
                 counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
-        bwd = lvx_backward if strategy == "lvx" else ring_backward
-        dq, dk, dv = bwd(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
+        if strategy == "lvx":   # dK / dV written straight into the [S, 2 hkv d] GEMM operand
+            dkv = torch.empty((y_i.shape[0], 2 * hkd), dtype=dt, device=y_i.device)
+            dq, _, _ = lvx_backward(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale,
+                                    dk_out=_heads(dkv[:, :hkd], w.hkv),
+                                    dv_out=_heads(dkv[:, hkd:], w.hkv))
+            dq = _flat(dq.to(dt))
+        else:
+            dq, dk, dv = ring_backward(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
+            dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
+            dkv = torch.cat([dk, dv], dim=1)
         del k, v
-        dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
-        dkv = torch.cat([dk, dv], dim=1)
         g_wkv = torch.empty_like(wkv)
         if d_y_acc is not None:
             ctx.ops.gemm(dkv, False, wkv, True, d_y_acc, accumulate=True)   # += dKV W^T

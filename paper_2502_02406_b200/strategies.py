@@ -347,7 +347,8 @@ def lvx_forward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block
 
 def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_block,
                  state: AttentionState, do_block, scale: float,
-                 trace: RoundTrace | None = None, kv_stream: KVStream | None = None):
+                 trace: RoundTrace | None = None, kv_stream: KVStream | None = None,
+                 dk_out=None, dv_out=None):
     """Query-rotation backward (strategies.py:234-276): the tuple
     (Q, dO, L, D, dQ) of every block travels once around the ring and every
     rank adds its K/V block's contribution; the last dQ hop is the
@@ -376,8 +377,10 @@ def lvx_backward(ctx: DeviceContext, shards: ShardSpec, q_block, k_block, v_bloc
     gd = _grad_dtype(ops, q_block.dtype)
     qs, qr = shards.q_sizes, shards.q_ranges
     mq = max(qs) if qs else 0
-    dk = torch.empty(k_block.shape, dtype=gd, device=dev)   # written once, in gd
-    dv = torch.empty(v_block.shape, dtype=gd, device=dev)
+    # written once, in gd; ``dk_out`` / ``dv_out`` let the caller choose the
+    # layout (e.g. head views of one [rows, 2 hkv d] matrix the next GEMM reads)
+    dk = dk_out if dk_out is not None else torch.empty(k_block.shape, dtype=gd, device=dev)
+    dv = dv_out if dv_out is not None else torch.empty(v_block.shape, dtype=gd, device=dev)
     with ctx.call() as call:
         if n == 1:
             return _lvx_backward_local(ops, q_block, k_block, v_block, state, do_block, scale,
