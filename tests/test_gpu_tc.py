@@ -305,3 +305,43 @@ def test_tc_two_devices_one_process():
             torch.cuda.synchronize(dev)
             assert orc.max_norm_error(st.O.cpu().numpy(), O) <= TOL_BF16
             assert all(torch.isfinite(t).all() for t in grads)
+
+
+def _rand_shapes(n, seed):
+    """Seeded random bf16 tensor-core shapes: GQA groups 1-4, ragged query and
+    KV tails, d in {64, 128}."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        hkv = int(rng.integers(1, 4))
+        hq = hkv * int(rng.choice([1, 2, 4]))
+        sq = int(rng.integers(1, 400))
+        skv = int(rng.integers(1, 3000))
+        d = int(rng.choice([64, 128]))
+        out.append((hq, hkv, sq, skv, d))
+    return out
+
+
+@pytest.mark.parametrize("shape", _rand_shapes(12, 2026))
+def test_tc_random_shapes_fwd_bwd_vs_oracle(shape):
+    """Forward + backward (dQ, dK, dV) on seeded random shapes against the f64
+    oracle, gated at 2x torch SDPA's bf16 error on the same inputs
+    (tests/sdpa_ref.py)."""
+    from tests import sdpa_ref
+    from paper_2502_02406_b200 import kernels as K
+    hq, hkv, sq, skv, d = shape
+    (q, k, v, g), (Q, Kr, Vr, G) = bf16_inputs(hq, hkv, sq, skv, d, seed=sum(shape))
+    scale = d ** -0.5
+    st = K.blockwise_attention(q, k, v)
+    D = K.attention_row_stats(st, g)
+    dq, dk, dv = K.blockwise_attention_backward(q, k, v, st.L, D, g)
+    torch.cuda.synchronize()
+    O, L = orc.dense_attention(Q, Kr, Vr)
+    rq, rk, rv = orc.dense_attention_backward(Q, Kr, Vr, O, L, G)
+    want = {"O": O, "L": L, "dQ": rq, "dK": rk, "dV": rv}
+    ours = sdpa_ref.errors({"O": st.O.float().cpu(), "L": st.L.cpu(), "dQ": dq.float().cpu(),
+                            "dK": dk.float().cpu(), "dV": dv.float().cpu()}, want)
+    so, sq_, sk, sv = (t.float().cpu() for t in sdpa_ref.sdpa_grads(q, k, v, g, scale))
+    sdpa = sdpa_ref.errors({"O": so, "dQ": sq_, "dK": sk, "dV": sv}, want)
+    print(f"\nrandom {shape}: ours {ours}\n    sdpa {sdpa}")
+    assert not sdpa_ref.gate(ours, sdpa), sdpa_ref.gate(ours, sdpa)
