@@ -271,10 +271,10 @@ def native_arm(args):
     else:
         import paper_2502_02406_b200 as lvx
         ctx = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev)
-        # the no-comm arm shares the comm arm's arena and side stream (its hops
-        # are local copies into the same receive slots)
+        # the no-comm arm: its own arena and side stream; its hops are local
+        # copies of the send blocks into its receive slots
         ctx_nc = lvx.DeviceContext(env.rank, env.world, group=env.group, device=env.dev,
-                                   comm_enabled=False, transport=ctx.transport)
+                                   comm_enabled=False)
         head_skv = CFG["s_kv"] if CFG["s_kv"] in args.points else args.points[-1]
         lines = []
         for skv in args.points:

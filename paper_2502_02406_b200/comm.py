@@ -396,10 +396,10 @@ class ProcessGroupTransport:
     def alloc(self, nbytes: int, device) -> torch.Tensor:
         return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
 
-    def begin(self):
+    def begin(self, handshake: bool = True):
         pass
 
-    def end(self):
+    def end(self, handshake: bool = True):
         pass
 
     def shift(self, send, dst, recv, to: int, frm: int, k: int, after=None):
@@ -475,11 +475,11 @@ class MailboxTransport:
     def alloc(self, nbytes: int, device) -> torch.Tensor:
         return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
 
-    def begin(self):
+    def begin(self, handshake: bool = True):
         if self.group.aborted:
             raise ClusterAborted(f"worker {self.rank}: group aborted")
 
-    def end(self):
+    def end(self, handshake: bool = True):
         pass
 
     def _recv_into(self, frm: int, k: int, recv) -> None:
@@ -527,7 +527,12 @@ class PeerTransport:
       EPOCH[src]           rank src finished its previous call (its arena and
                            its reads of ours are done); consumed by begin()
     The values never change, so a recorded step replays as a CUDA graph
-    (``strategies.StepGraph``), and no host exchange is needed per call."""
+    (``strategies.StepGraph``), and no host exchange is needed per call.
+    One-shot EPOCH words stay unambiguous because a peer's next end-of-call
+    write cannot come before this rank consumed the previous one: in every
+    schedule here (ring shifts, all-to-all) a rank's call finishes only after
+    receiving data that transitively left every peer after that peer's
+    begin(); calls that send nothing skip the handshake (``handshake``)."""
 
     kind = "copy-engine"
     MAXN = 16
@@ -640,20 +645,22 @@ class PeerTransport:
             _lib.check(fn, st)
 
     # -- calls and hops -----------------------------------------------------
-    def begin(self):
+    def begin(self, handshake: bool = True):
         """A call starts: the copy stream waits until every peer finished its
         previous call (so it is no longer reading our arena or writing into
-        the slots this call will reuse)."""
+        the slots this call will reuse).  ``handshake=False``: a call that
+        never writes into peers (the no-communication arm) skips the flags,
+        so a context of its own never races the ring's one-shot EPOCH words."""
         if self._aborted:
             raise ClusterAborted(f"worker {self.rank}: transport aborted")
         self.epoch += 1
-        if self.map is not None:
+        if self.map is not None and handshake:
             cs = self.copy.cuda_stream
             for p in range(self.n):
                 if p != self.rank:
                     self._wait(self.EPOCH + p, cs)
 
-    def end(self):
+    def end(self, handshake: bool = True):
         """The caller's arena is free once its compute stream gets here; tell
         every peer (they may write into it in the next call), then join the
         copy stream back so nothing outlives the call."""
@@ -662,7 +669,7 @@ class PeerTransport:
         ev.record(cur)
         self.copy.wait_event(ev)
         cs = self.copy.cuda_stream
-        for p in range(self.n):
+        for p in range(self.n if handshake else 0):
             if p != self.rank:
                 self._signal(p, self.EPOCH + self.rank, cs)
         done = torch.cuda.Event()
@@ -960,12 +967,12 @@ class DeviceContext:
             raise ClusterError("scheduler calls do not nest")
         self._call = _Call(self)
         if self.transport is not None:
-            self.transport.begin()
+            self.transport.begin(handshake=self.comm_enabled)
         try:
             yield self._call
         finally:
             if self.transport is not None:
-                self.transport.end()
+                self.transport.end(handshake=self.comm_enabled)
             self._call = None
 
     def _raw(self, nbytes: int) -> torch.Tensor:
