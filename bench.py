@@ -196,22 +196,43 @@ def cpu_reference_rate(budget_s: float = 12.0):
 
 
 def reference_arm(args):
+    """The reference's algorithm on the host cores (the oracle port of
+    strategies.py lvx fwd + bwd, numpy f64 + multithreaded BLAS).  A step is
+    ONE bounded sample of the workload — the C2 heads / head_dim on 64 query
+    rows x 16384 KV rows — because the full layer takes about an hour of CPU;
+    ms_per_step is that sample step's wall time and value its TFLOP/s, so the
+    rate is comparable with the GPU's and every step is really run."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, sample, threads = [], "", 1
-    for i in range(args.warmup + args.steps):
-        v, sample, threads = cpu_reference_rate(budget_s=4.0)
-        if i >= args.warmup:
-            vals.append(v)
-    val = statistics.median(vals)
-    flops = 14.0 * CFG["s_q"] * CFG["s_kv"] * CFG["hq"] * CFG["d"]
-    ms = flops / (val * 1e12) * 1e3
+    import numpy as np
+    from threadpoolctl import threadpool_info, threadpool_limits
+    from oracle import lvx_oracle as orc
+    sq, skv = 64, 16384
+    Q, K, V, dO = orc.make_inputs(sq, skv, CFG["hq"], CFG["d"], seed=7, hkv=CFG["hkv"])
+    Q, K, V, dO = (t.astype(np.float32) for t in (Q, K, V, dO))
+    flops = orc.attention_flops(sq, skv, CFG["hq"], CFG["d"])
+    times = []
+    with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()
+                       if i.get("user_api") == "blas"), default=1)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            orc.simulate("lvx", Q, K, V, dO, n=1)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    val = flops / sec / 1e12
+    sample = (f"oracle port of lvx fwd+bwd (numpy f64, {threads} host threads BLAS) on "
+              f"Lq={sq} x Lkv={skv} rows of the workload, hq={CFG['hq']}/hkv={CFG['hkv']}, "
+              f"d={CFG['d']}, fp32 in; one sample per step")
     line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**CFG, "note": "CPU sample of the workload; ms_per_step extrapolated"},
+            "config": {**CFG, "sample_s_q": sq, "sample_s_kv": skv,
+                       "note": "a step = one bounded sample of the workload (same heads, "
+                               "head_dim and dtype path); the rate is the compared quantity"},
             "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
