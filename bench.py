@@ -556,6 +556,11 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
                                     "bytes_per_step_rank0": rtr[0][0].total_sent_bytes()
                                     + rtr[0][1].total_sent_bytes()}
             # the Ring in the reference's own order (compute, then shift and wait)
+            if not _ring_fits(env, shards, hq, hkv, d, dev, reference_order=True):
+                out["ring_baseline_reference_schedule"] = {
+                    "skipped": "two (K, V, dK, dV) records do not fit in HBM at this Lkv"}
+                return _finish(out, args, head, ctx, shards, q_i, k_i, v_i, do_i, scale, fwd,
+                               bwd, flops, world, dev)
             ms_rref, _, *_ = timed(ctx, max(2, args.steps // 2), 1,
                                    strategy=(ring_forward, ring_backward_reference_schedule))
             out["ring_baseline_reference_schedule"] = {
@@ -567,6 +572,12 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         out["no_comm_ms_per_step"] = ms
         out["overhead_vs_no_comm"] = 0.0
 
+    return _finish(out, args, head, ctx, shards, q_i, k_i, v_i, do_i, scale, fwd, bwd, flops,
+                   world, dev)
+
+
+def _finish(out, args, head, ctx, shards, q_i, k_i, v_i, do_i, scale, fwd, bwd, flops, world,
+            dev):
     # --- end to end through the host-buffer API (pinned host -> HBM -> host)
     if head and not args.no_e2e:
         out["e2e"] = e2e_arm(args, ctx, shards, (q_i, k_i, v_i, do_i), scale, fwd, bwd, flops,
@@ -574,7 +585,7 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
     return out
 
 
-def _ring_fits(env, shards, hq, hkv, d, dev) -> bool:
+def _ring_fits(env, shards, hq, hkv, d, dev, reference_order: bool = False) -> bool:
     """Whether ring_backward's buffers fit beside what is resident: per rank
     RING_SLOTS bf16 K/V slots, as many fp32 dK/dV partial slots, the fp32
     homecoming, its own and a scratch fp32 dK/dV, and the bf16 gradients
@@ -585,7 +596,11 @@ def _ring_fits(env, shards, hq, hkv, d, dev) -> bool:
     mk = max(shards.kv_sizes)
     slots = max(1, min(RING_SLOTS, n - 1))
     kv = hkv * mk * d
-    need = slots * kv * 2 * 2 + slots * kv * 4 * 2 + kv * 4 * 2 + 2 * kv * 4 * 2 + kv * 2 * 2
+    if reference_order:   # two (K, V, dK, dV) records + homecoming + acc / tmp + grads
+        need = 2 * (kv * 2 * 2 + kv * 4 * 2) + kv * 4 * 2 + 2 * kv * 4 * 2 + kv * 2 * 2
+    else:
+        need = slots * kv * 2 * 2 + slots * kv * 4 * 2 + kv * 4 * 2 + 2 * kv * 4 * 2 + kv * 2 * 2
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info(dev)
     ok = torch.tensor([1.0 if need < 0.9 * free else 0.0], device=dev)
     if n > 1:
