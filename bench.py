@@ -24,6 +24,7 @@ end-to-end number through the host-buffer API, clocks, and kernel launches.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -300,6 +301,7 @@ def native_arm(args):
         lines = []
         for skv in args.points:
             lines.append(measure_point(args, env, ctx, ctx_nc, skv, head=(skv == head_skv)))
+            gc.collect()               # the point's closures hold its shard tensors
             torch.cuda.empty_cache()
         out = next(ln for ln, skv in zip(lines, args.points) if skv == head_skv)
         if len(lines) > 1:
@@ -373,6 +375,8 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
             traces.append((tf, tb))
         return st, g
 
+    host_stats = {}
+
     def timed(c, steps, warm, strategy=None, sampler=False):
         cs = ClockSampler(local) if sampler else None
         if cs:
@@ -402,7 +406,7 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         for tf, tb in traces:
             tf.resolve()
             tb.resolve()
-        timed.host_ms = env.max_over_ranks(host_ms)
+        host_stats["host_ms"] = env.max_over_ranks(host_ms)
         return env.max_over_ranks(ms), traces, launches, (cs.summary() if cs else None)
 
     ms, traces, launches, clocks = timed(ctx, args.steps, args.warmup, sampler=True)
@@ -498,7 +502,7 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
            "gpu_launches": int(launches),
            # host time to submit one step (Python schedulers + C ABI calls); a
            # step whose device time is not well above it is launch-bound
-           "host_submit_ms_per_step": timed.host_ms}
+           "host_submit_ms_per_step": host_stats["host_ms"]}
 
     # --- the same step recorded once as a CUDA graph and replayed (no host
     # work per step: the kernels, copy-engine hops and one-shot flags replay)
