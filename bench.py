@@ -302,6 +302,8 @@ def native_arm(args):
         for skv in args.points:
             lines.append(measure_point(args, env, ctx, ctx_nc, skv, head=(skv == head_skv)))
             gc.collect()               # the point's closures hold its shard tensors
+            ctx.release_arena()        # the Ring's K/V slots are sized for this point
+            ctx_nc.release_arena()
             torch.cuda.empty_cache()
         out = next(ln for ln, skv in zip(lines, args.points) if skv == head_skv)
         if len(lines) > 1:

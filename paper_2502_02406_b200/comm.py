@@ -620,6 +620,15 @@ class PeerTransport:
         self.reserve(nbytes)
         return self.arena[:max(nbytes, 1)]
 
+    def release_arena(self) -> None:
+        """Collective, between calls: free the arena (the next call maps a new
+        one of the size it needs) — after a schedule with big slots (the Ring
+        baseline's K/V) when later calls need far less."""
+        torch.cuda.synchronize(self.device)
+        self.coll.barrier()
+        self._free_map()
+        self.coll.barrier()
+
     def _flag(self, word: int) -> int:
         return self.capacity + 4 * word
 
@@ -974,6 +983,12 @@ class DeviceContext:
             if self.transport is not None:
                 self.transport.end(handshake=self.comm_enabled)
             self._call = None
+
+    def release_arena(self) -> None:
+        """Collective: drop the transport's arena (see PeerTransport)."""
+        if isinstance(self.transport, PeerTransport):
+            self.transport.release_arena()
+            self._views.clear()
 
     def _raw(self, nbytes: int) -> torch.Tensor:
         if self.transport is not None and isinstance(self.transport, PeerTransport):
