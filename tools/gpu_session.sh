@@ -91,6 +91,12 @@ for leg in "$@"; do
       for sh in c2round c4round c4gath c3round c2gath; do
         timeout 300 python tools/bench_kernels.py --shape $sh --bwd --bf16-grads >> $out/${tag}_kernels.jsonl 2>&1
       done ;;
+    fullscale_n)
+      n=$(nvidia-smi -L | wc -l)
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29524 tools/fullscale_multi_check.py > $out/${tag}_fullscale_n${n}.json 2> $out/${tag}_fullscale.err
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+        --master-port 29525 tools/nvlink_counters.py > $out/${tag}_nvlink_n${n}.json 2> $out/${tag}_nvlink.err ;;
     hbm)
       timeout 300 python tools/bench_hbm_kernels.py > $out/${tag}_hbm.json 2>&1 ;;
     gemm)
