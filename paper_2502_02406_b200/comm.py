@@ -709,6 +709,8 @@ class PeerTransport:
                     off = rh.data_ptr() - self.base
                     rows = sh.shape[0]
                     w = (sh.shape[1] if sh.dim() > 1 else 1) * es
+                    if off < 0 or off + (rows - 1) * rh.stride(0) * es + w > self.capacity:
+                        raise ClusterError("receive buffer is not in the transport arena")
                     runs.append([off, rh.stride(0) * es, sh.data_ptr(), sh.stride(0) * es, w, rows,
                                  False])
                 continue
