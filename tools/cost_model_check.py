@@ -1,6 +1,6 @@
 """Cost model (paper_2502_02406_b200.analytics) vs measured bench runs.
 
-    python tools/cost_model_check.py [profiles/r01_bench_n2.json ...]
+    python tools/cost_model_check.py [profiles/r02_bench_c2_n2.json ...]
 
 For each committed bench line: the model's per-round compute / comm times at
 the B200 GEMM peak, the same with the compute side calibrated to the
@@ -17,7 +17,7 @@ from paper_2502_02406_b200 import analytics as A  # noqa: E402
 
 
 def row(path: Path) -> dict:
-    d = json.loads(path.read_text())
+    d = json.loads([ln for ln in path.read_text().splitlines() if ln.startswith("{")][-1])
     c = d["config"]
     n = d["n_gpus"]
     w = A.WorkloadSpec.b200(c["s_q"], c["s_kv"], c["hq"], c["hkv"], c["d"], n)
@@ -56,10 +56,12 @@ def row(path: Path) -> dict:
 
 
 P2P = None
-_p2p = ROOT / "profiles" / "r01b_p2p_bw_n2.json"
+# the ring's transport: the copy-engine shift of round 2 (tools/p2p_bw.py)
+_p2p = ROOT / "profiles" / "r02_p2p_bw_ce_n4.json"
 if _p2p.exists():
     P2P = sorted((int(k[:-3]) << 20, v["GBps_per_direction"] * 1e9)
-                 for k, v in json.loads(_p2p.read_text())["shift"].items())
+                 for k, v in json.loads([ln for ln in _p2p.read_text().splitlines()
+                                         if ln.startswith("{")][-1])["shift"].items())
 
 
 def p2p_bandwidth(nbytes: float) -> float:
@@ -75,9 +77,11 @@ def p2p_bandwidth(nbytes: float) -> float:
 
 
 def main():
-    paths = [Path(p) for p in sys.argv[1:]] or sorted((ROOT / "profiles").glob("r01_bench_n*.json"))
+    paths = [Path(p) for p in sys.argv[1:]] or [
+        ROOT / "profiles" / f for f in ("r02_bench_c2_n2.json", "r02_bench_c2_n4.json",
+                                        "r02_bench_c2_n4_skv524288.json")]
     rows = [row(p) for p in paths]
-    print("| n | measured ms/step | model @1419.9 TF | model calibrated | fwd round meas / model (ms) "
+    print("| n | measured ms/step | model @sustained peak | model calibrated | fwd round meas / model (ms) "
           "| LVX / Ring fwd hop (ms @900 GB/s) | regime (lvx / ring) | Ring/LVX meas | Ring/LVX model "
           "| Ring/LVX model, measured shift GB/s |")
     print("|---|---|---|---|---|---|---|---|---|---|")
