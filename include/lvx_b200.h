@@ -180,7 +180,10 @@ typedef struct lvx_matrix {
 
 /* General GEMM of the layer's projections: c (+)= op(a) op(b), row-major
  * matrices, op = transpose when ta / tb.  bf16 runs on the tcgen05 kernel
- * (fp32 accumulate), f32 / f64 on an exact SIMT kernel.  Used for the output
+ * (fp32 accumulate), f32 / f64 on an exact SIMT kernel.  With bf16 a / b, c
+ * may be F32: the result is stored or (accumulate) reduce-added in fp32 in
+ * the epilogue — the CA layers' shared visual-token gradient
+ * (mllm.py:368 d_y +=) accumulates this way.  Used for the output
  * projection W_O of the cross-attention block (mllm.py:297-301 forward,
  * :343-351 backward); the three calls below are special cases of it. */
 int lvx_gemm(const lvx_matrix* a, int ta, const lvx_matrix* b, int tb, const lvx_matrix* c,
