@@ -54,7 +54,11 @@ constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a 
 #ifndef LVX_FWD_POLY
 #define LVX_FWD_POLY 3
 #endif
-constexpr int kPolyPairs = LVX_FWD_POLY;   // of every 8 column pairs, exp2 by polynomial
+#ifndef LVX_FWD_POLY64
+#define LVX_FWD_POLY64 LVX_FWD_POLY
+#endif
+template <int D>
+constexpr int kPolyPairsD = D == 64 ? LVX_FWD_POLY64 : LVX_FWD_POLY;   // of every 8 column pairs, exp2 by polynomial
 
 // LVX_FWD_TRACE=<split> (profiling builds only, tools/fwd_trace.py): clock64
 // stamps of CTA (pair 0, split, head 0), [role][kv tile][event]
@@ -337,7 +341,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
             };
             using I = std::integral_constant<int, 0>;
             if (nvalid < kBN) half(std::true_type{}, I{});
-            else half(std::false_type{}, std::integral_constant<int, kPolyPairs>{});
+            else half(std::false_type{}, std::integral_constant<int, kPolyPairsD<D>>{});
             const float rs = acc.x + acc.y;
             if (__any_sync(0xffffffffu, !(rs <= kFastBound))) {   // also inf / NaN
               fail_half = h;
