@@ -459,14 +459,14 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
         peak = sust
         peak_kind = f"{pk_kind} bf16 sustained (kernel timed inside a long step)"
     traffic, traffic_src = None, None
-    tj = ROOT / "profiles" / "r01b_traffic.json"
+    tj = ROOT / "profiles" / "r02_traffic.json"
     if world == 1 and args.strategy == "lvx" and args.workload == "c2" and \
             s_kv == WORKLOADS["c2"]["s_kv"] and tj.exists():
         # ncu DRAM bytes per launch of this kernel at this exact launch shape
         rec = json.loads(tj.read_text())["per_launch"].get(kname)
         if rec:
             traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
-            traffic_src = {"file": "profiles/r01b_traffic.json", "read": rec["dram_bytes_read"],
+            traffic_src = {"file": "profiles/r02_traffic.json", "read": rec["dram_bytes_read"],
                            "write": rec["dram_bytes_write"], "algorithmic": rec["algorithmic_bytes"]}
     roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
