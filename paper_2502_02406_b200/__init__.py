@@ -3,8 +3,9 @@ contexts (arXiv 2502.02406), drop-in for the reference package ``lvxattn``'s
 hot path (kernels + query/KV-rotation strategies).
 
 Kernels: hand-written sm_100a CUDA (tcgen05/TMEM/TMA) in ``liblvx_b200.so``
-behind the C ABI of ``include/lvx_b200.h``.  Schedulers: one process per GPU
-over NCCL (``strategies``).  There is no CPU fallback.
+behind the C ABI of ``include/lvx_b200.h``.  Schedulers (``strategies``): one
+rank per GPU, or thread ranks sharing one GPU; the ring hops are copy-engine
+transfers into the peers' arenas (``comm``).  There is no CPU fallback.
 
 Submodules beyond the kernels and schedulers: ``recompute`` (the CA layer with
 the K/V recompute), ``mllm`` (the toy MLLM stack, memory ledger, frame

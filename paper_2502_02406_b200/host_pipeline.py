@@ -13,8 +13,8 @@ Three streams per rank:
            chunk), each chunk followed by an event.  The forward's round 0
            consumes chunks as they land (``strategies.KVStream``); later
            rounds and the backward find the block resident.
-  compute  the LV-XAttn forward / backward of ``strategies`` (NCCL hops on
-           NCCL's own stream as usual).
+  compute  the LV-XAttn forward / backward of ``strategies`` (the ring hops
+           on the transport's copy stream as usual).
   d2h      dK/dV leave per chunk as soon as the batched dK/dV pass has
            finished that chunk (at n = 1 that pass runs before dQ, so dQ
            hides the tail); O, L, dQ leave at the end.

@@ -1,9 +1,11 @@
 """Distributed cross-attention schedulers on B200 — drop-in for
 ``lvxattn.strategies`` (reference ``pkg/src/lvxattn/strategies.py``).
 
-One process per GPU.  Each rank keeps its KV shard resident in HBM; the
-schedulers move the rotating blocks with grouped NCCL send/recv (``comm``)
-on NCCL's stream while the attention kernels run on the compute stream.
+One rank per GPU (or thread ranks sharing one GPU).  Each rank keeps its KV
+shard resident in HBM; the schedulers move the rotating blocks with
+copy-engine puts into the successor's arena (``comm.PeerTransport``) on a
+side stream while the attention kernels run on the compute stream, which
+waits on a stream-side flag only right before the kernel that consumes a hop.
 
   lvx   query rotation (strategies.py:175-276, Algorithm 1): the
         (O, L, Q) blocks travel, the fused split-combine+merge kernel folds
