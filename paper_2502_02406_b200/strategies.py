@@ -16,8 +16,12 @@ Round structure, block indices, epilogues, per-message metadata checks and
 byte accounting follow the reference exactly, so byte counters equal the
 closed forms of ``volumes`` (GQA-aware).  Deviations, all documented in
 DESIGN.md: partial states (O, L, D, dQ, dK/dV accumulators) travel in
-float32 when the inputs are bfloat16; the receive buffers are preallocated
-and double-buffered instead of freshly allocated per message.
+float32 when the inputs are bfloat16; the receive buffers live in the
+rank's arena, laid out per call identically on every rank, instead of being
+allocated per message; the backward schedules send their immutable blocks
+first and let dQ (LV-XAttn) or the dK/dV partials (Ring) lag one hop, so
+message counts differ from the reference's (``volumes.messages_per_rank``)
+while byte totals per rank are identical.
 """
 from __future__ import annotations
 
