@@ -63,3 +63,19 @@ def test_library_links_no_cublas():
     lib = build.build()
     deps = subprocess.run(["ldd", str(lib)], capture_output=True, text=True).stdout
     assert "cublas" not in deps.lower(), deps
+
+
+def test_integration_stub_binds_declared_symbols():
+    """The ctypes stub INTEGRATION.md shows a maintainer of the reference
+    package compiles, and every lvx_* function it calls is declared in the
+    header and exported by the library."""
+    import ast
+    blocks = re.findall(r"```python\n(.*?)```", (ROOT / "INTEGRATION.md").read_text(), re.S)
+    assert len(blocks) >= 2
+    declared = set(_declared())
+    used = set()
+    for b in blocks:
+        ast.parse(b)                       # valid Python
+        used |= set(re.findall(r"_lib\.(lvx_[a-z0-9_]+)", b))
+    assert used, "the stub calls the C ABI"
+    assert used <= declared, used - declared
