@@ -51,6 +51,9 @@ constexpr int kBN = 128;   // kv rows per tile
 constexpr int kThreads = 384;   // softmax WGs 0-1, WG 2 = producer, MMA, 2 idle warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kFastBound = 4096.f;       // single-pass acceptance bound on a P row sum
+#ifndef LVX_FWD_PREFETCH
+#define LVX_FWD_PREFETCH 0
+#endif
 #ifndef LVX_FWD_POLY
 #define LVX_FWD_POLY 3
 #endif
@@ -311,15 +314,29 @@ fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUte
         int fail_half = j > 0 ? 2 : 0;   // 2: both halves single-pass
         if (j > 0) {
           const float2 nm2 = make_float2(-m_used, -m_used);
+#if LVX_FWD_PREFETCH
+          // both halves' scores in one TMEM round trip (one load latency per tile)
+          uint32_t sall[4][32];
+          tmem_ld32(sa, sall[0]);
+          tmem_ld32(sa + 32, sall[1]);
+          tmem_ld32(sa + 64, sall[2]);
+          tmem_ld32(sa + 96, sall[3]);
+          tmem_wait_ld();
+#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t pk[2][16];
             float2 acc = make_float2(0.f, 0.f);
             auto half = [&](auto masked, auto poly) {
+#if LVX_FWD_PREFETCH
+              const uint32_t (&s0)[32] = sall[2 * h];
+              const uint32_t (&s1)[32] = sall[2 * h + 1];
+#else
               uint32_t s0[32], s1[32];
               tmem_ld32(sa + h * 64, s0);
               tmem_ld32(sa + h * 64 + 32, s1);
               tmem_wait_ld();
+#endif
               auto chunk = [&](const uint32_t (&sv)[32], int c) {
 #pragma unroll
                 for (int e = 0; e < 32; e += 2) {
