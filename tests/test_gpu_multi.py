@@ -307,3 +307,32 @@ def test_repeated_runs_bit_identical():
         outs.append((res.O, res.L, res.grads.dQ, res.grads.dK, res.grads.dV))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n", [3, 5])
+def test_ring_shift_closure_copy_engine(n):
+    """n shifts around the ring return every rank's block to it
+    (/root/reference/pkg/tests/test_cluster.py ring_shift closure), through the
+    copy-engine transport, in one call and across calls (one-shot flags)."""
+    from paper_2502_02406_b200.comm import ClusterSpec
+    from paper_2502_02406_b200.launch import spawn_ranks
+
+    def body(ctx):
+        mine = torch.full((2, 7, 16), float(ctx.rank + 1), device="cuda")
+        ok = []
+        for _ in range(3):                        # three calls
+            with ctx.call() as call:
+                slots = call.alloc({"r": (n, [("x", 2 * 7 * 16, torch.float32)])})["r"]
+                cur = mine
+                for j in range(n):
+                    recv = slots[j]["x"].view(2, 7, 16)
+                    hop, _ = ctx.shift([cur], [recv])
+                    hop.wait()
+                    cur = recv
+                ok.append(torch.equal(cur.clone(), mine))
+        ctx.synchronize()
+        return ok
+
+    res = spawn_ranks(ClusterSpec(n), body, timeout=30)
+    assert all(all(r) for r in res.results), res.results
+    assert res.stats.link(0, 1).message_count == 3 * n
