@@ -171,7 +171,9 @@ int lvx_convert(const lvx_view* src, const lvx_view* dst, void* stream);
  * exact SIMT kernel (f32 / f64, and bf16 views TMA cannot describe).
  * Row-major matrices; strides in elements; all operands one dtype.  Tall-K
  * products with few output tiles split K across the SMs and reduce in fp32
- * scratch from the stream-ordered allocator (cudaMallocAsync on `stream`). */
+ * scratch from the stream-ordered allocator (cudaMallocAsync on `stream`);
+ * the first such call raises the release threshold of the device's default
+ * memory pool so that scratch is not unmapped at every synchronisation. */
 typedef struct lvx_matrix {
   void* data;
   int64_t rows, cols, row_stride;
