@@ -67,6 +67,12 @@ for leg in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
         --log-file $out/${tag}_launches_c4.csv python bench.py --workload c4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph \
         > $out/${tag}_launches_c4.log 2>&1 ;;
+    ncu_fwd_dq)   # --set full of the forward and dQ launches of the C2 bench
+      for kn in fwd_kernel bwd_dq_kernel; do
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kn -c 1 \
+          -o $out/${tag}_ncu_$kn python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu \
+          > $out/${tag}_ncu_$kn.log 2>&1
+      done ;;
     ncu_full)   # one --set full capture per hot kernel
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd_dkv_kernel -c 1 \
         -o $out/${tag}_ncu_dkv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu \
