@@ -718,10 +718,13 @@ def layer_arm(args, env):
         w0 = time.time()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        h0 = time.perf_counter()
         for _ in range(steps):
             step(policy)
+        host_ms = (time.perf_counter() - h0) * 1e3 / steps
         e1.record()
         torch.cuda.synchronize()
+        timed.host_ms = env.max_over_ranks(host_ms)
         if cs:
             cs.mark(w0, time.time())
             time.sleep(0.15)
@@ -733,6 +736,7 @@ def layer_arm(args, env):
     cnt = OpCounter()
     step(ActivationPolicy.RECOMPUTE_KV, cnt)       # counts the recompute FLOP (per rank)
     ms, launches, clocks = timed(ActivationPolicy.RECOMPUTE_KV, args.steps, args.warmup, True)
+    host_ms = timed.host_ms
     ms_store, _, _ = timed(ActivationPolicy.STORE_KV, max(2, args.steps // 2), 1)
     att = volumes.attention_flops(s_q, s_kv, hq, d) * nl
     # projections per layer: fwd Q (2 sq e hq d), K+V (2 * 2 skv e hkv d), O
@@ -755,9 +759,10 @@ def layer_arm(args, env):
             "flop_split": {"attention": att, "projections": nl * (proj_fwd + proj_bwd),
                            "recompute_counted_per_rank": cnt.projection_flops},
             "store_kv_ms_per_step": ms_store, "recompute_overhead": ms / ms_store - 1.0,
-            "roofline": {"kernel": "whole step (attention + projection GEMMs)",
-                         "bound": "tensor", "achieved": value, "peak": sust,
-                         "unit": "TFLOP/s", "frac": value / sust, "traffic": None,
+            "host_submit_ms_per_step": host_ms,
+            "roofline": {"kernel": "whole step (attention + projection GEMMs), per GPU",
+                         "bound": "tensor", "achieved": value / world, "peak": sust,
+                         "unit": "TFLOP/s", "frac": value / world / sust, "traffic": None,
                          "peak_kind": f"{pk_kind} bf16 sustained"},
             "clocks": clocks, "gpu_launches": int(launches)}
 

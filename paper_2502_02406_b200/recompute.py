@@ -257,13 +257,19 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     g_wq = torch.empty_like(w.w_q)
     ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
     d_x += g_i
+    if ctx.n > 1:   # one all-reduce of the layer's weight gradients, packed
+        parts = (g_wq, g_wkv, g_wo)
+        flat = torch.cat([t.reshape(-1) for t in parts])
+        if group is not None:
+            dist.all_reduce(flat, group=group)
+        else:
+            ctx.all_reduce_sum_(flat)
+        offs = [0]
+        for t in parts:
+            offs.append(offs[-1] + t.numel())
+        g_wq, g_wkv, g_wo = (flat[a:b].view(t.shape)
+                             for t, a, b in zip(parts, offs[:-1], offs[1:]))
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
-    if ctx.n > 1:
-        for t in (g_wq, g_wk, g_wv, g_wo):
-            if group is not None:
-                dist.all_reduce(t, group=group)
-            else:
-                ctx.all_reduce_sum_(t)
     return CrossAttentionGrads(d_x=d_x, d_y=d_y, w_q=g_wq, w_k=g_wk, w_v=g_wv, w_o=g_wo)
 
 

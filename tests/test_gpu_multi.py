@@ -336,3 +336,41 @@ def test_ring_shift_closure_copy_engine(n):
     res = spawn_ranks(ClusterSpec(n), body, timeout=30)
     assert all(all(r) for r in res.results), res.results
     assert res.stats.link(0, 1).message_count == 3 * n
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_recompute_layer_on_thread_ranks_vs_oracle(n):
+    """The RECOMPUTE_KV cross-attention layer (src/mllm.py:290-301, :343-370)
+    sharded over n ranks: each rank re-projects K/V from its own rows of y,
+    the attention runs LV-XAttn over the ring, and the layer's weight
+    gradients are summed over the ranks in ONE packed all-reduce.  Gathered
+    outputs and gradients against the f64 oracle of the unsharded layer, at
+    the gate of the single-GPU test (tests/test_gpu_recompute.py)."""
+    from paper_2502_02406_b200.comm import ClusterSpec
+    from paper_2502_02406_b200.launch import spawn_ranks
+    from paper_2502_02406_b200.recompute import ActivationPolicy, ca_backward, ca_forward
+    from paper_2502_02406_b200.strategies import ShardSpec
+    from tests.test_gpu_recompute import _setup
+    w, x, y, g, h = _setup()
+    sh = ShardSpec.balanced(x.shape[0], y.shape[0], n)
+
+    def body(ctx):
+        (qa, qb), (ka, kb) = sh.q_ranges[ctx.rank], sh.kv_ranges[ctx.rank]
+        out, saved = ca_forward(ctx, sh, x[qa:qb], y[ka:kb], w, ActivationPolicy.RECOMPUTE_KV)
+        gr = ca_backward(ctx, sh, g[qa:qb], saved, y[ka:kb], w)
+        ctx.synchronize()
+        return [t.double().cpu().numpy() for t in
+                (out, gr.d_x, gr.d_y, gr.w_q, gr.w_k, gr.w_v, gr.w_o)]
+
+    res = spawn_ranks(ClusterSpec(n), body, timeout=60).results
+    got = [np.concatenate([r[i] for r in res]) for i in range(3)] + list(res[0][3:])
+    for r in res[1:]:                      # the all-reduced weight gradients agree on every rank
+        for a, b in zip(res[0][3:], r[3:]):
+            assert np.array_equal(a, b)
+    ro, O, L = orc.ca_block_forward(h["x"], h["y"], h["wq"], h["wk"], h["wv"], h["wo"], w.hq, w.hkv)
+    ref = [ro, *orc.ca_block_backward(h["g"], h["x"], O, L, h["y"], h["wq"], h["wk"], h["wv"],
+                                      h["wo"], w.hq, w.hkv)]
+    names = ("out", "d_x", "d_y", "w_q", "w_k", "w_v", "w_o")
+    errs = {nm: orc.max_norm_error(a, b) for nm, a, b in zip(names, got, ref)}
+    print(f"\nrecompute CA layer, {n} thread ranks, bf16 vs f64 oracle:", errs)
+    assert max(errs.values()) <= 3e-2
