@@ -738,6 +738,10 @@ def layer_arm(args, env):
     ms, launches, clocks = timed(ActivationPolicy.RECOMPUTE_KV, args.steps, args.warmup, True)
     host_ms = timed.host_ms
     ms_store, _, _ = timed(ActivationPolicy.STORE_KV, max(2, args.steps // 2), 1)
+    graph = None
+    if not args.no_graph:   # the whole layer-stack step recorded once and replayed
+        graph = graph_replay(env, ctx, lambda: step(ActivationPolicy.RECOMPUTE_KV),
+                             args.steps, 0.0)
     att = volumes.attention_flops(s_q, s_kv, hq, d) * nl
     # projections per layer: fwd Q (2 sq e hq d), K+V (2 * 2 skv e hkv d), O
     # (2 sq hq d e); bwd: recompute K+V, Q re-projection, dX / dW for Q, K, V, O
@@ -760,6 +764,8 @@ def layer_arm(args, env):
                            "recompute_counted_per_rank": cnt.projection_flops},
             "store_kv_ms_per_step": ms_store, "recompute_overhead": ms / ms_store - 1.0,
             "host_submit_ms_per_step": host_ms,
+            "graph_replay": ({**graph, "value": total / (graph["ms_per_step"] * 1e-3) / 1e12}
+                             if graph and "ms_per_step" in graph else graph),
             "roofline": {"kernel": "whole step (attention + projection GEMMs), per GPU",
                          "bound": "tensor", "achieved": value / world, "peak": sust,
                          "unit": "TFLOP/s", "frac": value / world / sust, "traffic": None,
