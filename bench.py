@@ -678,7 +678,8 @@ def layer_arm(args, env):
     import paper_2502_02406_b200 as lvx
     from paper_2502_02406_b200 import _lib, volumes
     from paper_2502_02406_b200.recompute import (ActivationPolicy, CrossAttentionWeights,
-                                                 OpCounter, ca_backward, ca_forward)
+                                                 OpCounter, VisualGradSink, ca_backward,
+                                                 ca_forward)
     world, rank, dev = env.world, env.rank, env.dev
     s_q, s_kv, hq, hkv, d = CFG["s_q"], CFG["s_kv"], CFG["hq"], CFG["hkv"], CFG["d"]
     e, nl = CFG["d_embed"], CFG["layers"]
@@ -700,13 +701,14 @@ def layer_arm(args, env):
         for w in layers:
             x, sv = ca_forward(ctx, sh, x, y, w, policy)
             saved.append(sv)
-        gx, dy = go, torch.zeros_like(y, dtype=torch.float32)
+        gx = go
+        # every layer leaves [dK | dV] in the sink; dY = ONE GEMM over all layers
+        sink = VisualGradSink(y, [w.kv_weight().shape[1] for w in layers])
         for w, sv in zip(reversed(layers), reversed(saved)):
-            # every layer's dY is reduce-added into the fp32 dy in its GEMM
             gr = ca_backward(ctx, sh, gx, sv, y, w, counter=counter, group=env.group,
-                             d_y_acc=dy)
+                             dy_sink=sink)
             gx = gr.d_x
-        return gx, dy
+        return gx, sink.finish(ctx)
 
     def timed(policy, steps, warm, sampler=False):
         for _ in range(warm):

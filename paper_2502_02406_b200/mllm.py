@@ -35,7 +35,7 @@ import torch.distributed as dist
 from .comm import DeviceContext
 from .kernels import default_scale, state_dtype
 from .recompute import (ActivationPolicy, CrossAttentionGrads, CrossAttentionWeights, OpCounter,
-                        SavedCA, ca_backward, ca_forward)
+                        SavedCA, VisualGradSink, ca_backward, ca_forward)
 from .strategies import ShardSpec
 
 _DTYPES = {"f32": torch.float32, "f64": torch.float64, "bf16": torch.bfloat16}
@@ -313,10 +313,10 @@ def mllm_backward(d_out: torch.Tensor, saved: SavedActivations, y: torch.Tensor,
     scale = default_scale(config.d)
     ca_set = set(config.ca_positions)
     g = d_out
-    # the visual tokens' gradient sums over the CA layers (mllm.py:368); each
-    # layer's dY is reduce-added into this accumulator inside its GEMM
-    d_y_acc = torch.zeros(y.shape, dtype=torch.float64 if y.dtype == torch.float64
-                          else torch.float32, device=y.device)
+    # the visual tokens' gradient sums over the CA layers (mllm.py:368): each
+    # layer leaves its [dK | dV] in the sink; one GEMM over all layers at the end
+    ca_order = [b for b in reversed(range(config.num_lm_blocks)) if b in ca_set]
+    sink = VisualGradSink(y, [params.ca[b].kv_weight().shape[1] for b in ca_order])
     ca_grads: dict = {}
     lm_grads: list = [None] * config.num_lm_blocks
     for blk in reversed(range(config.num_lm_blocks)):
@@ -335,10 +335,10 @@ def mllm_backward(d_out: torch.Tensor, saved: SavedActivations, y: torch.Tensor,
                 raise ValueError(f"layer {blk}: missing saved activations")
             gr: CrossAttentionGrads = ca_backward(ctx, shards, g, saved.ca[blk], y,
                                                   params.ca[blk], scale, counter=counter,
-                                                  d_y_acc=d_y_acc)
+                                                  dy_sink=sink)
             ca_grads[blk] = gr
             g = gr.d_x
-    d_y = d_y_acc.to(y.dtype)
+    d_y = sink.finish(ctx).to(y.dtype)
     return MllmGradients(d_x0=g, d_y=d_y, ca=ca_grads, lm=lm_grads)
 
 

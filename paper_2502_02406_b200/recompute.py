@@ -98,6 +98,52 @@ class SavedCA:
     extras: dict = field(default_factory=dict)
 
 
+class VisualGradSink:
+    """The visual tokens' gradient over the CA layers that share y
+    (``src/mllm.py:368``: ``d_y += dK-part + dV-part`` per layer) as ONE GEMM.
+
+    Each layer's backward writes its [dK | dV] into its own column block of
+    one [S, sum(widths)] buffer (``slot``) instead of multiplying it out; at
+    the end ``finish`` computes dY = [dKV_1 | dKV_2 | ...] [W_1 | W_2 | ...]^T,
+    i.e. sum_l dKV_l W_l^T with the layer sum inside the GEMM's K loop (fp32
+    in TMEM) and the [S, e] result written once.  Per-layer accumulation
+    instead reads and writes the fp32 [S, e] accumulator once per layer
+    (C4 at n = 1: 4.3 GB each way per layer).  ``widths`` are the layers'
+    2 hkv d in the order their backward runs."""
+
+    def __init__(self, y: torch.Tensor, widths):
+        self.rows, self.e = y.shape
+        self.widths = [int(w) for w in widths]
+        self.offs = [0]
+        for w in self.widths:
+            self.offs.append(self.offs[-1] + w)
+        self.dkv = torch.empty((self.rows, self.offs[-1]), dtype=y.dtype, device=y.device)
+        self.acc_dtype = torch.float64 if y.dtype == torch.float64 else torch.float32
+        self.weights: list = []
+
+    def slot(self, wkv: torch.Tensor) -> torch.Tensor:
+        """The next layer's [S, 2 hkv d] dKV block (a strided view); ``wkv``
+        is that layer's [W_K | W_V]."""
+        i = len(self.weights)
+        if i >= len(self.widths):
+            raise ValueError(f"sink holds {len(self.widths)} layers; a layer more was added")
+        if wkv.shape != (self.e, self.widths[i]):
+            raise ValueError(f"layer {i}: [W_K|W_V] is {tuple(wkv.shape)}, expected "
+                             f"({self.e}, {self.widths[i]})")
+        self.weights.append(wkv)
+        return self.dkv[:, self.offs[i]:self.offs[i + 1]]
+
+    def finish(self, ctx: DeviceContext, out: torch.Tensor | None = None) -> torch.Tensor:
+        """dY [S, e] in fp32 (f64 for f64 y) = sum over the slots of dKV W^T."""
+        if len(self.weights) != len(self.widths):
+            raise ValueError(f"{len(self.weights)} of {len(self.widths)} layers added")
+        if out is None:
+            out = torch.empty((self.rows, self.e), dtype=self.acc_dtype, device=self.dkv.device)
+        w = torch.cat(self.weights, dim=1) if len(self.weights) > 1 else self.weights[0]
+        ctx.ops.gemm(self.dkv, False, w, True, out)
+        return out
+
+
 def _heads(flat: torch.Tensor, heads: int) -> torch.Tensor:
     """[S, heads*d] -> [heads, S, d] as a zero-copy strided view
     (``src/kernels.py:236-240`` reshapes and copies): the tensor-core kernels
@@ -200,7 +246,8 @@ def ca_forward(ctx: DeviceContext, shards: ShardSpec, x_i: torch.Tensor, y_i: to
 def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved: SavedCA,
                 y_i: torch.Tensor, w: CrossAttentionWeights, scale: float | None = None,
                 strategy: str = "lvx", counter: OpCounter | None = None,
-                group=None, d_y_acc: torch.Tensor | None = None) -> CrossAttentionGrads:
+                group=None, d_y_acc: torch.Tensor | None = None,
+                dy_sink: VisualGradSink | None = None) -> CrossAttentionGrads:
     """Backward of ``ca_forward`` (``src/mllm.py:343-370``).  Weight gradients
     are all-reduced over the process group when n > 1.
 
@@ -208,7 +255,13 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
     over the CA layers that share y (``src/mllm.py:368`` ``d_y +=``).  Given,
     this layer's dY = [dK|dV] [W_K|W_V]^T is reduce-added into it inside the
     GEMM's epilogue (no bf16 dY, no separate add pass) and returned as
-    ``d_y``; else a fresh dY in y's dtype is returned."""
+    ``d_y``; else a fresh dY in y's dtype is returned.
+
+    ``dy_sink``: the layer's [dK | dV] goes into the sink's next slot and the
+    dY GEMM is left to ``VisualGradSink.finish`` (one GEMM over all layers);
+    ``d_y`` is then None."""
+    if dy_sink is not None and d_y_acc is not None:
+        raise ValueError("give d_y_acc or dy_sink, not both")
     scale = default_scale(w.d) if scale is None else scale
     dt = g_i.dtype
     d_o = _heads(_mm(ctx, g_i, w.w_o, tb=True), w.hq)                  # g W_O^T
@@ -224,7 +277,8 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
             counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
             counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
         dq, d_y, g_wkv = _backward_chunked(ctx, q, y_i, w, wkv, saved.state,
-                                           d_o.to(q.dtype), scale, chunk, d_y_acc)
+                                           d_o.to(q.dtype), scale, chunk, d_y_acc,
+                                           dy_sink.slot(wkv) if dy_sink is not None else None)
         dq = _flat(dq.to(dt))
     else:
         if saved.policy is ActivationPolicy.STORE_KV:
@@ -235,7 +289,8 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
                 counter.add(y_i.shape[0], w.w_k.shape[0], w.w_k.shape[1])
                 counter.add(y_i.shape[0], w.w_v.shape[0], w.w_v.shape[1])
         if strategy == "lvx":   # dK / dV written straight into the [S, 2 hkv d] GEMM operand
-            dkv = torch.empty((y_i.shape[0], 2 * hkd), dtype=dt, device=y_i.device)
+            dkv = dy_sink.slot(wkv) if dy_sink is not None else \
+                torch.empty((y_i.shape[0], 2 * hkd), dtype=dt, device=y_i.device)
             dq, _, _ = lvx_backward(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale,
                                     dk_out=_heads(dkv[:, :hkd], w.hkv),
                                     dv_out=_heads(dkv[:, hkd:], w.hkv))
@@ -243,10 +298,17 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
         else:
             dq, dk, dv = ring_backward(ctx, shards, q, k, v, saved.state, d_o.to(q.dtype), scale)
             dq, dk, dv = _flat(dq.to(dt)), _flat(dk.to(dt)), _flat(dv.to(dt))
-            dkv = torch.cat([dk, dv], dim=1)
+            if dy_sink is not None:
+                dkv = dy_sink.slot(wkv)
+                dkv[:, :hkd], dkv[:, hkd:] = dk, dv
+            else:
+                dkv = torch.cat([dk, dv], dim=1)
         del k, v
         g_wkv = torch.empty_like(wkv)
-        if d_y_acc is not None:
+        if dy_sink is not None:   # dY comes from the sink's one GEMM over all layers
+            ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
+            d_y = None
+        elif d_y_acc is not None:
             ctx.ops.gemm(dkv, False, wkv, True, d_y_acc, accumulate=True)   # += dKV W^T
             ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
             d_y = d_y_acc
@@ -274,18 +336,20 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
 
 
 def _backward_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, wkv, state,
-                      d_o, scale: float, chunk: int, d_y_acc=None):
+                      d_o, scale: float, chunk: int, d_y_acc=None, dkv_slot=None):
     """n = 1 backward over K/V chunks: per chunk re-project K/V, add its dQ
     contribution (fp32, in place), compute its dK/dV and fold them into the
-    chunk's d_y rows (or reduce-add them into ``d_y_acc``) and into the fp32
+    chunk's d_y rows (or reduce-add them into ``d_y_acc``; or, given a sink
+    slot ``dkv_slot``, leave them there for the sink's GEMM) and into the fp32
     K/V weight gradient (the GEMM accumulates across chunks in its epilogue).
-    Returns (dQ, d_y, g_wkv)."""
+    Returns (dQ, d_y or None, g_wkv)."""
     ops = ctx.ops
     sd = ops.state_dtype(q.dtype)
     D = torch.empty(state.L.shape, dtype=sd, device=q.device)
     ops.row_stats(state.O, d_o, D)
     dq = torch.empty(q.shape, dtype=sd, device=q.device)
-    d_y = d_y_acc if d_y_acc is not None else torch.empty_like(y)
+    d_y = None if dkv_slot is not None else d_y_acc if d_y_acc is not None else \
+        torch.empty_like(y)
     g_wkv = torch.empty(wkv.shape, dtype=ops.state_dtype(wkv.dtype), device=y.device)
     hkd = w.hkv * w.d
     for c, (a, b) in enumerate(_row_chunks(y.shape[0], chunk)):
@@ -293,11 +357,13 @@ def _backward_chunked(ctx: DeviceContext, q, y, w: CrossAttentionWeights, wkv, s
         ws = ops.bwd_workspace(q, k)
         ops.bwd_dq_partial(q, k, v, state.L, D, d_o, scale, ws)
         ops.bwd_dq_finish(q, k, ws, dq, accumulate=c > 0)
-        dkv = torch.empty((b - a, 2 * hkd), dtype=y.dtype, device=y.device)
+        dkv = dkv_slot[a:b] if dkv_slot is not None else \
+            torch.empty((b - a, 2 * hkd), dtype=y.dtype, device=y.device)
         ops.bwd_dkv(q, k, v, state.L, D, d_o, scale, _heads(dkv[:, :hkd], w.hkv),
                     _heads(dkv[:, hkd:], w.hkv), accumulate=False)
         del k, v
-        ops.gemm(dkv, False, wkv, True, d_y[a:b], accumulate=d_y_acc is not None)   # dKV W^T
+        if d_y is not None:
+            ops.gemm(dkv, False, wkv, True, d_y[a:b], accumulate=d_y_acc is not None)  # dKV W^T
         ops.gemm(y[a:b], True, dkv, False, g_wkv, accumulate=c > 0)                # y^T dKV
     return dq, d_y, g_wkv.to(wkv.dtype)
 

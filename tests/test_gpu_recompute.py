@@ -117,3 +117,40 @@ def test_chunked_recompute_bounds_kv_transient():
     full_kv = 2 * 65536 * w.hkv * w.d * 2
     chunk_kv = 2 * 8192 * w.hkv * w.d * 2
     assert peaks[None] - peaks[8192] >= 0.9 * (full_kv - chunk_kv), (peaks, full_kv)
+
+
+@pytest.mark.parametrize("chunk", [None, 200])
+def test_visual_grad_sink_equals_per_layer_accumulation(chunk):
+    """dY over three CA layers sharing y (src/mllm.py:368): the sink's ONE GEMM
+    over the concatenated [dK|dV] blocks vs per-layer reduce-adds into an fp32
+    accumulator.  Same bf16 products summed in fp32 in a different order, so
+    1e-5 max-normalised; every other gradient is bit-identical."""
+    import paper_2502_02406_b200 as lvx
+    from paper_2502_02406_b200.recompute import (ActivationPolicy, CrossAttentionWeights,
+                                                 VisualGradSink, ca_backward, ca_forward)
+    w0, x, y, g, _ = _setup()
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    layers = [w0] + [CrossAttentionWeights(
+        *(((torch.rand(t.shape, device="cuda", generator=gen) * 2 - 1) * 0.03).bfloat16()
+          for t in (w0.w_q, w0.w_k, w0.w_v, w0.w_o)), w0.hq, w0.hkv) for _ in range(2)]
+    ctx = lvx.DeviceContext(0, 1)
+    sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
+    saved = []
+    for w in layers:
+        _, sv = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, kv_chunk_rows=chunk)
+        saved.append(sv)
+    acc = torch.zeros(y.shape, dtype=torch.float32, device="cuda")
+    sink = VisualGradSink(y, [w.kv_weight().shape[1] for w in layers])
+    ga, gb = [], []
+    for w, sv in zip(reversed(layers), reversed(saved)):
+        ga.append(ca_backward(ctx, sh, g, sv, y, w, d_y_acc=acc))
+        gb.append(ca_backward(ctx, sh, g, sv, y, w, dy_sink=sink))
+    dy = sink.finish(ctx)
+    assert dy.dtype == torch.float32 and gb[0].d_y is None
+    err = orc.max_norm_error(dy.double().cpu().numpy(), acc.double().cpu().numpy())
+    assert err <= 1e-5, err
+    for a, b in zip(ga, gb):
+        for f in ("d_x", "w_q", "w_k", "w_v", "w_o"):
+            assert torch.equal(getattr(a, f), getattr(b, f)), f
+    with pytest.raises(ValueError):
+        sink.slot(layers[0].kv_weight())            # every slot is taken
