@@ -23,7 +23,7 @@ for leg in "$@"; do
       timeout 900 python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu --no-e2e \
         > $out/${tag}_bench_c3.json 2> $out/${tag}_bench_c3.err ;;
     c4)
-      timeout 900 python bench.py --workload c4 --steps 3 --warmup 3 --no-cpu \
+      timeout 900 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu \
         > $out/${tag}_bench_c4.json 2> $out/${tag}_bench_c4.err ;;
     c5)
       timeout 1200 python bench.py --workload c5 --steps 3 --warmup 3 --no-cpu --no-e2e \
