@@ -1173,7 +1173,7 @@ __global__ void dq_combine_kernel(const float* __restrict__ ws, int splits, int 
 #pragma unroll
   for (int e = 0; e < PER; ++e) acc[e] = 0.f;
   // batches of B splits with every load in flight; summation order unchanged
-  constexpr int B = 8;
+  constexpr int B = D == 64 ? 16 : 8;
   for (int s0 = 0; s0 < splits; s0 += B) {
     float v[B][PER];
 #pragma unroll

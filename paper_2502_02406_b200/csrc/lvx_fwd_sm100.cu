@@ -490,46 +490,48 @@ __global__ void fwd_combine_kernel(const float* __restrict__ ws_o, const float* 
   if (gw >= (int64_t)hq * rows) return;
   const int h = (int)(gw / rows), i = (int)(gw % rows);
   const size_t stride = (size_t)hq * rows;
-  // splits in batches of B: all loads of a batch are in flight together (with
-  // one query tile per head there are few rows and up to ~64 splits, and a
-  // load-use chain per split left this kernel latency-bound); the summation
-  // order stays s = 0, 1, ... (bit-identical results)
-  constexpr int B = 8;
+  // The split LSEs are read lane-parallel (split s0 + lane), their max is a
+  // warp reduction (order-free) and each weight w_s = exp(L_s - max) is
+  // broadcast from its lane; the O rows of the splits are read in batches of
+  // B with every load in flight (with one query tile per head there are few
+  // rows and up to 128 splits, so a load-use chain per split would leave the
+  // kernel latency-bound).  O and the weight total are summed in the order
+  // s = 0, 1, ... exactly as a sequential loop would (deterministic).
+  constexpr int B = D == 64 ? 16 : 8;
   float mx = -INFINITY;
-  for (int s0 = 0; s0 < splits; s0 += B) {
-    float lv[B];
+  for (int s = lane; s < splits; s += 32) mx = fmaxf(mx, __ldg(ws_l + (size_t)s * stride + gw));
 #pragma unroll
-    for (int b = 0; b < B; ++b)
-      lv[b] = s0 + b < splits ? __ldg(ws_l + (size_t)(s0 + b) * stride + gw) : -INFINITY;
-#pragma unroll
-    for (int b = 0; b < B; ++b) mx = fmaxf(mx, lv[b]);
-  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float acc[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) acc[e] = 0.f;
   float tot = 0.f;
-  for (int s0 = 0; s0 < splits; s0 += B) {
-    float lv[B], v[B][PER];
+  for (int c0 = 0; c0 < splits; c0 += 32) {
+    const int sl = c0 + lane;
+    const float wl = sl < splits ? __expf(__ldg(ws_l + (size_t)sl * stride + gw) - mx) : 0.f;
+    const int nc = min(32, splits - c0);
+    for (int b0 = 0; b0 < nc; b0 += B) {
+      float v[B][PER];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const bool live = s0 + b < splits;
-      lv[b] = live ? __ldg(ws_l + (size_t)(s0 + b) * stride + gw) : -INFINITY;
-      const float* src = ws_o + ((size_t)(s0 + b) * stride + gw) * D + lane * PER;
-      if constexpr (PER == 4) {
-        const float4 t = live ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0, 0, 0, 0);
-        v[b][0] = t.x; v[b][1] = t.y; v[b][2] = t.z; v[b][3] = t.w;
-      } else {
-        const float2 t = live ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0, 0);
-        v[b][0] = t.x; v[b][1] = t.y;
+      for (int b = 0; b < B; ++b) {
+        const bool live = b0 + b < nc;
+        const float* src = ws_o + ((size_t)(c0 + b0 + b) * stride + gw) * D + lane * PER;
+        if constexpr (PER == 4) {
+          const float4 t = live ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0, 0, 0, 0);
+          v[b][0] = t.x; v[b][1] = t.y; v[b][2] = t.z; v[b][3] = t.w;
+        } else {
+          const float2 t = live ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0, 0);
+          v[b][0] = t.x; v[b][1] = t.y;
+        }
       }
-    }
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (s0 + b >= splits) break;
-      const float w = __expf(lv[b] - mx);
-      tot += w;
+      for (int b = 0; b < B; ++b) {
+        const float w = __shfl_sync(0xffffffffu, wl, (b0 + b) & 31);
+        if (b0 + b >= nc) break;
+        tot += w;
 #pragma unroll
-      for (int e = 0; e < PER; ++e) acc[e] += w * v[b][e];
+        for (int e = 0; e < PER; ++e) acc[e] += w * v[b][e];
+      }
     }
   }
   float lse = mx + __logf(tot);

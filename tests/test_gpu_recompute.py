@@ -119,8 +119,8 @@ def test_chunked_recompute_bounds_kv_transient():
     assert peaks[None] - peaks[8192] >= 0.9 * (full_kv - chunk_kv), (peaks, full_kv)
 
 
-@pytest.mark.parametrize("chunk", [None, 200])
-def test_visual_grad_sink_equals_per_layer_accumulation(chunk):
+@pytest.mark.parametrize("chunk,strategy", [(None, "lvx"), (200, "lvx"), (None, "ring")])
+def test_visual_grad_sink_equals_per_layer_accumulation(chunk, strategy):
     """dY over three CA layers sharing y (src/mllm.py:368): the sink's ONE GEMM
     over the concatenated [dK|dV] blocks vs per-layer reduce-adds into an fp32
     accumulator.  Same bf16 products summed in fp32 in a different order, so
@@ -137,14 +137,15 @@ def test_visual_grad_sink_equals_per_layer_accumulation(chunk):
     sh = lvx.ShardSpec.balanced(x.shape[0], y.shape[0], 1)
     saved = []
     for w in layers:
-        _, sv = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, kv_chunk_rows=chunk)
+        _, sv = ca_forward(ctx, sh, x, y, w, ActivationPolicy.RECOMPUTE_KV, strategy=strategy,
+                           kv_chunk_rows=chunk)
         saved.append(sv)
     acc = torch.zeros(y.shape, dtype=torch.float32, device="cuda")
     sink = VisualGradSink(y, [w.kv_weight().shape[1] for w in layers])
     ga, gb = [], []
     for w, sv in zip(reversed(layers), reversed(saved)):
-        ga.append(ca_backward(ctx, sh, g, sv, y, w, d_y_acc=acc))
-        gb.append(ca_backward(ctx, sh, g, sv, y, w, dy_sink=sink))
+        ga.append(ca_backward(ctx, sh, g, sv, y, w, strategy=strategy, d_y_acc=acc))
+        gb.append(ca_backward(ctx, sh, g, sv, y, w, strategy=strategy, dy_sink=sink))
     dy = sink.finish(ctx)
     assert dy.dtype == torch.float32 and gb[0].d_y is None
     err = orc.max_norm_error(dy.double().cpu().numpy(), acc.double().cpu().numpy())
