@@ -1159,6 +1159,282 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   }
 }
 
+#ifdef LVX_DQ2_PROBE   // CTA-pair variant: measured 20-29 % slower, not in the product build
+// ================================================================ dQ on CTA pairs
+// bwd_dq_kernel on cta_group::2: a pair = two query tiles of the same GQA
+// group and KV split (M = 256 query rows, 128 per CTA); the leader issues
+// S = Q K^T, dP = dO V^T and dQ += dS K for both.  B splits by N, so each CTA
+// stages only its half of every B operand per 128-row KV step: K and V rows
+// [64 rank, 64 rank + 64) (B of S / dP, both 64-column panels) and the d-panel
+// `rank` of K over all 128 rows (B of dQ) — 48 KB instead of 64 KB, which
+// takes the per-SM L2 -> SMEM stream (the 1-CTA kernel's bound) below the
+// tensor rate.  The overlap of the two K halves is loaded twice: the leader's
+// descriptors address both CTAs' SMEM at the same offsets.  Softmax, TMEM
+// layout and epilogue are the 1-CTA kernel's; each CTA's softmax threads
+// arrive on the LEADER's q_ready / s_read / ds_full (512).
+struct Dq2Cfg {
+  static constexpr int D = 128;
+  static constexpr int Q_BYTES = 128 * D * 2;
+  static constexpr int HALF = 64 * 128;                        // 64 rows x one 128-byte panel
+  static constexpr int OFF_SB = 0, OFF_QB = 2 * HALF, OFF_VB = 4 * HALF;
+  static constexpr int SLOT = 6 * HALF;                        // 48 KB
+  static constexpr int STAGES = 4;
+  static constexpr int QSLOT = 2;                              // Q | dO staged over slots 2-3
+  static constexpr int NBAR = 3 + 2 * STAGES + 5;
+  static constexpr int SMEM = 1024 + STAGES * SLOT + NBAR * 8 + 16;
+  static constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384, G_COL = 448;
+  static_assert((STAGES - QSLOT) * SLOT >= 2 * Q_BYTES, "Q / dO staging must fit");
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmKh, const __grid_constant__ CUtensorMap tmVh,
+               const __grid_constant__ CUtensorMap tmG, const BwdParams p) {
+  using C = Dq2Cfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u = smem_u32(smem_raw);
+  uint8_t* sm = smem_raw + (((raw_u + 1023u) & ~1023u) - raw_u);
+  uint8_t* sKV = sm;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::SLOT);
+  uint64_t* qd_full = bars;                   // local: Q / dO staged
+  uint64_t* q_local = bars + 1;               // local: this CTA's Q / dO in TMEM (256)
+  uint64_t* q_ready = bars + 2;               // leader: both CTAs' Q / dO in TMEM (512)
+  uint64_t* kv_full = bars + 3;               // leader: both CTAs' K / V halves
+  uint64_t* kv_empty = kv_full + C::STAGES;   // both (multicast commit)
+  uint64_t* s_full = kv_empty + C::STAGES;    // both
+  uint64_t* s_read = s_full + 1;              // leader (512)
+  uint64_t* dp_full = s_read + 1;             // both
+  uint64_t* ds_full = dp_full + 1;            // leader (512)
+  uint64_t* dq_done = ds_full + 1;            // both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int tt = blockIdx.x, split = blockIdx.y, g = blockIdx.z;
+  const int kv_t0 = split * p.tiles_per_split;
+  const int nt = min(p.n_tiles, kv_t0 + p.tiles_per_split) - kv_t0;
+  const int qh = g * p.G + tt / p.tpq, row0 = (tt % p.tpq) * 128;
+  auto arrive_pair = [&](uint64_t* bar) {
+    if (rank == 0) mbar_arrive(bar);
+    else mbar_arrive_cluster(leader_addr(bar));
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(qd_full, 1);
+    mbar_init(q_local, 256);
+    mbar_init(q_ready, 512);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_read, 512);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 512);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmKh);
+      tma_prefetch(&tmVh);
+      tma_prefetch(&tmG);
+      uint8_t* qs = sKV + C::QSLOT * C::SLOT;
+      mbar_arrive_expect_tx(qd_full, 2 * C::Q_BYTES);
+      for (int pn = 0; pn < 2; ++pn) {
+        tma_load_3d(qs + pn * 128 * 128, &tmQ, qd_full, pn * 64, row0, qh);
+        tma_load_3d(qs + C::Q_BYTES + pn * 128 * 128, &tmG, qd_full, pn * 64, row0, qh);
+      }
+      const uint64_t pol = l2_evict_last();   // the pair's K / V step is read by 64 CTAs
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % C::STAGES, u = j / C::STAGES;
+        if (u > 0) mbar_wait(&kv_empty[s], (u - 1) & 1);
+        else if (s >= C::QSLOT) mbar_wait(q_local, 0);   // Q / dO have left these slots
+        uint8_t* slot = sKV + s * C::SLOT;
+        if (rank == 0) mbar_arrive_expect_tx(&kv_full[s], 2 * C::SLOT);
+        const uint32_t lb = leader_addr(&kv_full[s]);
+        const int kr = (kv_t0 + j) * 128, mine = kr + 64 * (int)rank;
+        for (int pn = 0; pn < 2; ++pn) {
+          tma2_load_3d(slot + C::OFF_SB + pn * C::HALF, &tmKh, lb, pn * 64, mine, g, pol);
+          tma2_load_3d(slot + C::OFF_VB + pn * C::HALF, &tmVh, lb, pn * 64, mine, g, pol);
+        }
+        tma2_load_3d(slot + C::OFF_QB, &tmK, lb, 64 * (int)rank, kr, g, pol);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------- MMA issuer (leader, converged warp)
+    if (rank == 0) {
+      constexpr uint32_t idS = idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idQ = idesc_bf16(256, D, false, true);
+      const uint64_t dh0 = umma_desc_sw128(smem_u32(sKV), 0, 1024);   // 64-row halves, K-major
+      const uint64_t dm0 = umma_desc_sw128(smem_u32(sKV + C::OFF_QB), 0, 1024);   // MN-major K
+      auto kslot = [&](int j) { return (uint64_t)(((j % C::STAGES) * C::SLOT) >> 4); };
+      auto issue_sdp = [&](int j, uint32_t a_col, uint32_t col, uint32_t boff, uint64_t* bar) {
+        if (elect_one()) {   // S = Q K^T / dP = dO V^T, A (Q / dO) from TMEM
+          const uint64_t b = dh0 + kslot(j) + (boff >> 4);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t o = ((kk >> 2) * C::HALF + (kk & 3) * 32) >> 4;
+            mma2_bf16_ts(tmem + col, tmem + a_col + kk * 8, b + o, idS, kk > 0);
+          }
+          mma2_commit_mc(bar);
+        }
+        __syncwarp();
+      };
+      auto wait_kv = [&](int j) {
+        mbar_wait_cluster(&kv_full[j % C::STAGES], (j / C::STAGES) & 1);
+        tc_fence_after();
+      };
+      mbar_wait_cluster(q_ready, 0);
+      tc_fence_after();
+      wait_kv(0);
+      issue_sdp(0, C::Q_COL, C::S_COL, C::OFF_SB, s_full);
+      issue_sdp(0, C::G_COL, C::DP_COL, C::OFF_VB, dp_full);
+      for (int j = 0; j < nt; ++j) {
+        const uint32_t ph = j & 1;
+        if (j + 1 < nt) {
+          wait_kv(j + 1);
+          mbar_wait_cluster(s_read, ph);
+          tc_fence_after();
+          issue_sdp(j + 1, C::Q_COL, C::S_COL, C::OFF_SB, s_full);            // S(j+1)
+        }
+        mbar_wait_cluster(ds_full, ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t b = dm0 + kslot(j);
+#pragma unroll
+          for (int kk = 0; kk < 128 / 16; ++kk)   // dQ += dS K (A = dS packed over dP)
+            mma2_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + dkv_a_col(kk),
+                         b + ((kk * 16 * 128) >> 4), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+          mma2_commit_mc(&kv_empty[j % C::STAGES]);
+        }
+        __syncwarp();
+        if (j + 1 < nt) issue_sdp(j + 1, C::G_COL, C::DP_COL, C::OFF_VB, dp_full);   // dP(j+1)
+      }
+      if (elect_one()) mma2_commit_mc(dq_done);
+      __syncwarp();
+    }
+  } else {
+    // ------------- softmax: query row per thread, 64 of the 128 kv columns per wg
+    const int wg = warp >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    {   // stage Q (wg 0) / dO (wg 1) rows into TMEM as bf16 pairs (A operands)
+      mbar_wait(qd_full, 0);
+      const uint32_t base = smem_u32(sKV + C::QSLOT * C::SLOT + wg * C::Q_BYTES) + r * 128;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t v[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t a, b2, c2, d2;
+          const uint32_t addr = base + c * 128 * 128 + ((q ^ (r & 7)) << 4);
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(a), "=r"(b2), "=r"(c2), "=r"(d2) : "r"(addr));
+          v[q * 4] = a; v[q * 4 + 1] = b2; v[q * 4 + 2] = c2; v[q * 4 + 3] = d2;
+        }
+        tmem_st32(tl + (wg ? C::G_COL : C::Q_COL) + c * 32, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(q_local);
+      arrive_pair(q_ready);
+    }
+    const int row = row0 + r;
+    const size_t prow = (size_t)qh * p.rows_pad + row;
+    const float2 nl2 = make_float2(p.Lp[prow], p.Lp[prow]);   // -L log2 e
+    const float2 nd2 = make_float2(p.Dp[prow], p.Dp[prow]);   // -D
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    for (int j = 0; j < nt; ++j) {
+      const uint32_t ph = j & 1;
+      const int nvalid = min(128, p.rows_kv - (kv_t0 + j) * 128) - wg * 64;
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      uint32_t sv[2][32];
+      tmem_ld32(tl + C::S_COL + wg * 64, sv[0]);
+      tmem_ld32(tl + C::S_COL + wg * 64 + 32, sv[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      arrive_pair(s_read);
+      float2 pf[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        auto pa = [&](auto masked) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int c = hh * 32 + e;
+            float2 x = ffma2(u2f2(sv[hh][e], sv[hh][e + 1]), sc2, nl2);
+            if constexpr (decltype(masked)::value) {
+              x.x = c < nvalid ? x.x : -INFINITY;
+              x.y = c + 1 < nvalid ? x.y : -INFINITY;
+            }
+            const float2 pq = (((c / 2) * 3) % 8) < kPolyPairsD<D> && !decltype(masked)::value
+                                  ? ex2_poly2(x)
+                                  : make_float2(ex2(x.x), ex2(x.y));
+            pf[c / 2] = pq;
+          }
+        };
+        if (nvalid < 64)
+          pa(std::true_type{});
+        else
+          pa(std::false_type{});
+      }
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      uint32_t gv[2][32], dd[32];
+      tmem_ld32(tl + C::DP_COL + wg * 64, gv[0]);
+      tmem_ld32(tl + C::DP_COL + wg * 64 + 32, gv[1]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int pi = (hh * 32 + e) / 2;
+          const float2 r2 = fmul2(pf[pi], fadd2(u2f2(gv[hh][e], gv[hh][e + 1]), nd2));
+          dd[pi] = pack_bf16(r2.x, r2.y);
+        }
+      }
+      tmem_st32(tl + C::DP_COL + wg * 64, dd);
+      tmem_wait_st();
+      tc_fence_before();
+      arrive_pair(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    const bool valid = row < p.rows_q;
+    float* dst = p.ws_dq + (((size_t)split * p.hq + qh) * p.rows_q + row) * D;
+#pragma unroll 1
+    for (int c = wg * (D / 64); c < (wg + 1) * (D / 64); ++c) {
+      uint32_t v[32];
+      tmem_ld32(tl + C::DQ_COL + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(dst + c * 32 + e) =
+              make_float4(__uint_as_float(v[e]) * p.scale, __uint_as_float(v[e + 1]) * p.scale,
+                          __uint_as_float(v[e + 2]) * p.scale, __uint_as_float(v[e + 3]) * p.scale);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+#endif  // LVX_DQ2_PROBE
+
 // dq (+)= sum_s ws_dq[s]  (fixed order, deterministic)
 template <int D>
 __global__ void dq_combine_kernel(const float* __restrict__ ws, int splits, int hq, int rows,
@@ -1372,6 +1648,22 @@ int launch_dq(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
+#ifdef LVX_DQ2_PROBE
+int launch_dq2(const lvx_view* q, const lvx_view* k, const lvx_view* v, const lvx_view* dO,
+               const BwdParams& p, const BwdPlan& pl, cudaStream_t st) {
+  CUtensorMap mq128, mg128, mk128, mk64, mv64;
+  if (!make_tma_3d(&mq128, q, 128) || !make_tma_3d(&mg128, dO, 128) ||
+      !make_tma_3d(&mk128, k, 128) || !make_tma_3d(&mk64, k, 64) || !make_tma_3d(&mv64, v, 64))
+    return LVX_ECUDA;
+  static std::atomic<unsigned> attr_done{0};
+  if (!ensure_smem_attr(bwd_dq2_kernel, Dq2Cfg::SMEM, attr_done)) return LVX_ECUDA;
+  bwd_dq2_kernel<<<dim3(pl.pairs, pl.splits, (unsigned)k->heads), 320, Dq2Cfg::SMEM, st>>>(
+      mq128, mk128, mk64, mv64, mg128, p);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
+}
+#endif  // LVX_DQ2_PROBE
+
 }  // namespace
 
 bool tc_bwd_eligible(const lvx_view* q, const lvx_view* k, const lvx_view* v) {
@@ -1403,6 +1695,9 @@ int tc_bwd_dq_partial(const lvx_view* q, const lvx_view* k, const lvx_view* v,
   fill_params(p, pl, q, k, scale, ws);
   int s = launch_prep(p, L, D, st);
   if (s) return s;
+#ifdef LVX_DQ2_PROBE
+  if (q->d == 128 && pl.pairs % 2 == 0) return launch_dq2(q, k, v, dO, p, pl, st);
+#endif
   return q->d == 128 ? launch_dq<128>(q, k, v, dO, p, pl, st) : launch_dq<64>(q, k, v, dO, p, pl, st);
 }
 
