@@ -708,7 +708,7 @@ def layer_arm(args, env):
             gr = ca_backward(ctx, sh, gx, sv, y, w, counter=counter, group=env.group,
                              dy_sink=sink)
             gx = gr.d_x
-        return gx, sink.finish(ctx)
+        return gx, sink.finish(ctx, dtype=y.dtype)   # dY in y's dtype, like the reference
 
     def timed(policy, steps, warm, sampler=False):
         for _ in range(warm):

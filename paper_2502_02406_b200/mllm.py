@@ -338,7 +338,7 @@ def mllm_backward(d_out: torch.Tensor, saved: SavedActivations, y: torch.Tensor,
                                                   dy_sink=sink)
             ca_grads[blk] = gr
             g = gr.d_x
-    d_y = sink.finish(ctx).to(y.dtype)
+    d_y = sink.finish(ctx, dtype=y.dtype)
     return MllmGradients(d_x0=g, d_y=d_y, ca=ca_grads, lm=lm_grads)
 
 

@@ -133,12 +133,16 @@ class VisualGradSink:
         self.weights.append(wkv)
         return self.dkv[:, self.offs[i]:self.offs[i + 1]]
 
-    def finish(self, ctx: DeviceContext, out: torch.Tensor | None = None) -> torch.Tensor:
-        """dY [S, e] in fp32 (f64 for f64 y) = sum over the slots of dKV W^T."""
+    def finish(self, ctx: DeviceContext, out: torch.Tensor | None = None,
+               dtype: torch.dtype | None = None) -> torch.Tensor:
+        """dY [S, e] = sum over the slots of dKV W^T, accumulated in fp32 (f64
+        for f64 y) and written once in ``dtype`` (default: that accumulator
+        dtype; y's bf16 rounds the fp32 sum once in the GEMM epilogue)."""
         if len(self.weights) != len(self.widths):
             raise ValueError(f"{len(self.weights)} of {len(self.widths)} layers added")
         if out is None:
-            out = torch.empty((self.rows, self.e), dtype=self.acc_dtype, device=self.dkv.device)
+            out = torch.empty((self.rows, self.e), dtype=dtype or self.acc_dtype,
+                              device=self.dkv.device)
         w = torch.cat(self.weights, dim=1) if len(self.weights) > 1 else self.weights[0]
         ctx.ops.gemm(self.dkv, False, w, True, out)
         return out

@@ -148,6 +148,8 @@ def test_visual_grad_sink_equals_per_layer_accumulation(chunk, strategy):
         gb.append(ca_backward(ctx, sh, g, sv, y, w, strategy=strategy, dy_sink=sink))
     dy = sink.finish(ctx)
     assert dy.dtype == torch.float32 and gb[0].d_y is None
+    # y's dtype straight from the GEMM epilogue = the fp32 sum rounded once
+    assert torch.equal(sink.finish(ctx, dtype=torch.bfloat16), dy.bfloat16())
     err = orc.max_norm_error(dy.double().cpu().numpy(), acc.double().cpu().numpy())
     assert err <= 1e-5, err
     for a, b in zip(ga, gb):
