@@ -45,7 +45,7 @@ for leg in "$@"; do
     c4_n)
       n=$(nvidia-smi -L | wc -l)
       timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-        --master-port 29522 bench.py --gpus $n --workload c4 --steps 3 --warmup 3 --no-e2e \
+        --master-port 29522 bench.py --gpus $n --workload c4 --steps 10 --warmup 3 --no-e2e \
         > $out/${tag}_bench_c4_n${n}.json 2> $out/${tag}_bench_c4_n${n}.err ;;
     c5small_n)
       n=$(nvidia-smi -L | wc -l)
