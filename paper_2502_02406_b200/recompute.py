@@ -19,8 +19,10 @@ the weights are replicated.  Every projection is row-local, so:
 
 Every projection GEMM runs on the library's own tcgen05 GEMM behind the C ABI
 (``lvx_kv_recompute``, ``lvx_project_bwd``, and ``lvx_gemm`` for W_Q / W_O;
-heads folded into the GEMM strides, no copies).  Fusing the K/V recompute into
-the attention kernels' producer is the next step.  ``OpCounter`` counts forward-direction projection FLOP
+heads folded into the GEMM strides, no copies); why the K/V recompute is not
+fused into the attention kernels is measured in DESIGN.md §4.  Across layers
+that share y, ``VisualGradSink`` turns the per-layer ``d_y +=`` into one GEMM.
+``OpCounter`` counts forward-direction projection FLOP
 done inside the backward, like ``src/mllm.py:242-253``.
 """
 from __future__ import annotations

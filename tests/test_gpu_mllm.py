@@ -2,7 +2,7 @@
 
 * f64: the whole 5-block / 3-CA-layer stack, both policies, against the
   reference's own outputs and gradients (tests/golden/golden_mllm_stack.npz),
-  1e-10 max-normalised (exact SIMT attention + cuBLAS f64 projections).
+  1e-10 max-normalised (exact SIMT attention + the library's exact f64 GEMM).
 * ledgers and frame budgets: identical to the reference's numbers when the
   layout matches (f32 / f64: one element size everywhere).
 * bf16: measured live bytes == the ledger categories, and the allocator agrees.

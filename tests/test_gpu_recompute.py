@@ -44,7 +44,7 @@ def test_recompute_equals_store_and_saves_kv_memory():
         ops[pol] = cnt.projection_flops
         res[pol] = [out, gr.d_x, gr.d_y, gr.w_q, gr.w_k, gr.w_v, gr.w_o]
     for a, b in zip(res[ActivationPolicy.STORE_KV], res[ActivationPolicy.RECOMPUTE_KV]):
-        assert torch.equal(a, b)          # cuBLAS recompute reproduces K/V bit for bit
+        assert torch.equal(a, b)          # the recompute GEMM reproduces K/V bit for bit
     kv_bytes = 2 * y.shape[0] * w.hkv * w.d * 2
     assert mem[ActivationPolicy.STORE_KV] - mem[ActivationPolicy.RECOMPUTE_KV] == kv_bytes
     e = x.shape[1]

@@ -1,7 +1,7 @@
 // Probe: can a KV-parallel single-pass backward afford its dQ reduction if
 // a thread-block cluster pre-reduces the dQ partials in distributed shared
 // memory (DSMEM) before one TMA bulk reduce-add per cluster goes to L2?
-// (VERDICT r01 "next" 3.)
+// (VERDICT r01 "next" 3; DESIGN.md §4 "The single-pass backward, measured".)
 //
 // Model of one fused dK/dV/dQ step per CTA: a 128 x 128 fp32 dQ partial
 // (64 KB, here already in shared memory - the real kernel would first drain it
