@@ -1,0 +1,128 @@
+"""The largest single-GPU shape the benchmark runs: C5's last point, Lkv
+15,000,000 with Llama-3-V heads (Lq 2048, hq 32, hkv 8, d 128, bf16,
+forward + backward; BASELINE.json configs[4]).  15,000,000 is not a multiple
+of the 128-row KV tile, so the last tile is ragged; K / V alone are 61 GB.
+
+* forward: O, L of sampled (head, query row) pairs against a float64 torch
+  reference over all 15M KV rows (chunked, on the GPU: the CPU oracle would
+  need the 61 GB of K / V on the host and minutes per row);
+* the ring's identity at this size: the forward over the two KV halves,
+  merged by the library's merge_states (src/kernels.py:144-161), equals the
+  forward over the whole block;
+* backward: dK / dV of sampled KV rows (first, middle, last ragged tile)
+  against the CPU oracle's blockwise_attention_backward over all 2048 query
+  rows, with L from the GPU forward and D = rowsum(dO * O) in f64; dQ of the
+  sampled query rows against the float64 torch reference.
+
+Tolerance (stated): max-normalised error <= 1e-2 on the same bf16 inputs, as
+the other bf16 tests (tests/test_gpu_fullscale.py); the split identity
+<= 5e-3: the two runs round P to bf16 against different running maxima, and
+each is ~2e-3 from the f64 result (max-normalised over all 65536 (head, row)
+pairs, as the smoke test and the sampled rows here measure), so their
+difference is bounded by the sum.
+Needs ~140 GB of HBM; runtime ~1 min."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import lvx_oracle as orc
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+HQ, HKV, SQ, SKV, D = 32, 8, 2048, 15_000_000, 128
+G = HQ // HKV
+Q_SAMPLES = [(0, 0), (5, 1023), (17, 2047), (31, 600)]          # (head, query row)
+KV_ROWS = [0, 7_654_321, SKV - 1]
+CHUNK = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def run():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * (1 << 30):
+        pytest.skip(f"needs ~150 GB of free HBM, {free >> 30} GB free")
+    from paper_2502_02406_b200 import build
+    build.build()
+    from paper_2502_02406_b200 import kernels as K
+    from paper_2502_02406_b200.comm import DeviceContext
+    from paper_2502_02406_b200.kernels import default_scale
+    from paper_2502_02406_b200.strategies import ShardSpec, lvx_backward, lvx_forward
+    g = torch.Generator(device="cuda").manual_seed(15)
+
+    def u(*shape):
+        return (torch.rand(*shape, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    q, do = u(HQ, SQ, D), u(HQ, SQ, D)
+    k, v = u(HKV, SKV, D), u(HKV, SKV, D)
+    ctx = DeviceContext(0, 1)
+    scale = default_scale(D)
+    st = lvx_forward(ctx, ShardSpec.balanced(SQ, SKV, 1), q, k, v, scale)
+    dq, dk, dv = lvx_backward(ctx, ShardSpec.balanced(SQ, SKV, 1), q, k, v, st, do, scale)
+    out = {"O": st.O.double().cpu().numpy(), "L": st.L.double().cpu().numpy(),
+           "dQ": dq.double().cpu().numpy(), "dK": dk[:, KV_ROWS].double().cpu().numpy(),
+           "dV": dv[:, KV_ROWS].double().cpu().numpy(), "scale": scale,
+           "Q": q.double().cpu().numpy(), "dO": do.double().cpu().numpy(),
+           "K_rows": k[:, KV_ROWS].double().cpu().numpy(),
+           "V_rows": v[:, KV_ROWS].double().cpu().numpy()}
+    del dq, dk, dv
+    torch.cuda.empty_cache()
+    # the two KV halves separately, merged
+    h = SKV // 2
+    parts = [lvx_forward(ctx, ShardSpec.balanced(SQ, b - a, 1), q, k[:, a:b], v[:, a:b], scale)
+             for a, b in ((0, h), (h, SKV))]
+    merged = K.merge_states(parts[0], parts[1])
+    out["O_split"] = merged.O.double().cpu().numpy()
+    out["L_split"] = merged.L.double().cpu().numpy()
+    del parts, merged, st
+    torch.cuda.empty_cache()
+    # float64 reference of the sampled query rows over all KV rows (GPU, chunked)
+    ref = {}
+    for hq_, row in Q_SAMPLES:
+        qi = q[hq_, row].double() * scale
+        gi = do[hq_, row].double()
+        kh, vh = k[hq_ // G], v[hq_ // G]
+        s = torch.cat([kh[a:a + CHUNK].double() @ qi for a in range(0, SKV, CHUNK)])
+        lse = torch.logsumexp(s, 0)
+        p = torch.exp(s - lse)
+        o = sum(p[a:a + CHUNK] @ vh[a:a + CHUNK].double() for a in range(0, SKV, CHUNK))
+        dd = torch.dot(gi, o)
+        dp = torch.cat([vh[a:a + CHUNK].double() @ gi for a in range(0, SKV, CHUNK)])
+        ds = p * (dp - dd)
+        dqr = sum(ds[a:a + CHUNK] @ kh[a:a + CHUNK].double() for a in range(0, SKV, CHUNK)) * scale
+        ref[(hq_, row)] = (o.cpu().numpy(), float(lse), dqr.cpu().numpy())
+    out["ref"] = ref
+    del q, k, v, do
+    torch.cuda.empty_cache()
+    return out
+
+
+def _stack(r, key, idx):
+    return np.stack([r[key][hq_, row] for hq_, row in Q_SAMPLES]), \
+        np.stack([r["ref"][(hq_, row)][idx] for hq_, row in Q_SAMPLES])
+
+
+def test_max_lkv_forward_and_dq_sampled_rows(run):
+    errs = {}
+    for key, idx in (("O", 0), ("L", 1), ("dQ", 2)):
+        got, want = _stack(run, key, idx)
+        errs[key] = orc.max_norm_error(got, want)
+    print(f"\nLkv 15M, (head, row) {Q_SAMPLES}: {errs}")
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_max_lkv_split_merge_identity(run):
+    errs = {"O": orc.max_norm_error(run["O_split"], run["O"]),
+            "L": orc.max_norm_error(run["L_split"], run["L"])}
+    print(f"\nLkv 15M, halves merged vs whole: {errs}")
+    assert max(errs.values()) <= 5e-3, errs
+
+
+def test_max_lkv_sampled_kv_rows_vs_oracle(run):
+    r = run
+    Dv = orc.attention_row_stats(r["O"], r["dO"])
+    _, dK, dV = orc.blockwise_attention_backward(r["Q"], r["K_rows"], r["V_rows"], r["L"], Dv,
+                                                 r["dO"], r["scale"])
+    errs = {"dK": orc.max_norm_error(r["dK"], dK), "dV": orc.max_norm_error(r["dV"], dV)}
+    print(f"\nLkv 15M, kv rows {KV_ROWS}: {errs}")
+    assert max(errs.values()) <= TOL, errs
