@@ -40,6 +40,9 @@ CHUNK = 1 << 20
 def run():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 150 * (1 << 30):
         pytest.skip(f"needs ~150 GB of free HBM, {free >> 30} GB free")
