@@ -374,3 +374,29 @@ def test_recompute_layer_on_thread_ranks_vs_oracle(n):
     errs = {nm: orc.max_norm_error(a, b) for nm, a, b in zip(names, got, ref)}
     print(f"\nrecompute CA layer, {n} thread ranks, bf16 vs f64 oracle:", errs)
     assert max(errs.values()) <= 3e-2
+
+
+def test_eight_process_ranks_copy_engine():
+    """8 PROCESS ranks (torchrun) over the copy-engine transport on however
+    many GPUs the box has (rank r on GPU r % n_gpus; CUDA IPC between
+    processes, same device or not): lvx, ring and head-parallel gathered
+    results against the single-rank run of the same inputs
+    (tools/procs_check.py) — the process path of an 8-GPU node."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "8",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(root / "tools" / "procs_check.py")]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert p.returncode == 0 and lines, p.stderr[-3000:]
+    res = json.loads(lines[-1])
+    print("\n8 process ranks:", res)
+    assert res["pass"] and res["n"] == 8 and set(res["errors"]) == {"lvx", "ring", "head"}
