@@ -794,6 +794,7 @@ def e2e_arm(args, ctx, shards, dev_inputs, scale, fwd, bwd, flops, world, dev):
     h2d, d2h = base.h2d_bytes(), base.d2h_bytes()
     pipe = HostLayerPipeline(ctx, shards, scale, chunks=8, prefetch=True)
     steps = max(2, args.steps)
+    pcie = _pcie_rates(dev, world)
     pipe.run([base, base])   # warm-up (allocations, both slots)
     if world > 1:
         dist.barrier()
@@ -807,11 +808,44 @@ def e2e_arm(args, ctx, shards, dev_inputs, scale, fwd, bwd, flops, world, dev):
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         el, h2d, d2h = tm[0].item(), int(t[1].item()), int(t[2].item())
+    per_rank_h2d, per_rank_d2h = base.h2d_bytes(), base.d2h_bytes()
+    pcie["copy_bound_ms_per_step"] = 1e3 * max(per_rank_h2d / (pcie["h2d_gbs"] * 1e9),
+                                               per_rank_d2h / (pcie["d2h_gbs"] * 1e9))
     return {"value": flops / el / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": el * 1e3, "steps": steps,
+            "pcie": pcie,
             "path": "HostLayerPipeline: pinned host shard -> HBM (chunked, prefetched) -> "
                     "lvx_forward/lvx_backward -> pinned host (host wall clock around "
                     f"{steps} steps incl. the first step's unhidden copies, max over ranks)"}
+
+
+def _pcie_rates(dev, world) -> dict:
+    """Pinned host <-> this GPU copy rates (GB/s, 512 MiB each way, best of 3,
+    min over ranks — all ranks copy at once, as in the e2e steps): what bounds
+    the e2e step when its copies are longer than its kernels."""
+    import torch
+    import torch.distributed as dist
+    n = 512 << 20
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    buf = torch.empty(n, dtype=torch.uint8, device=dev)
+    rates = []
+    for src, dst in ((host, buf), (buf, host)):
+        best = float("inf")
+        for _ in range(3):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        rates.append(n / best / 1e9)
+    if world > 1:
+        t = torch.tensor(rates, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        rates = t.tolist()
+    del host, buf
+    return {"h2d_gbs": rates[0], "d2h_gbs": rates[1], "probe_bytes": n}
 
 
 def main():
