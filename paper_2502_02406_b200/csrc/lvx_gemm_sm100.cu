@@ -53,6 +53,7 @@ struct GemmParams {
   int64_t ldc;
   float* Cf;          // fp32 output: split-K scratch or the caller's fp32 C, else null
   int64_t ldcf;       // its leading dimension
+  int64_t split_stride;   // split-K: elements between the splits' scratch slices
   int f32_store;      // into Cf: 1 store (one split, overwrite), 0 reduce-add
   int accumulate;     // bf16 C += A B
 };
@@ -183,7 +184,8 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
+          float* dst = p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride +
+                       (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
@@ -380,7 +382,8 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
+          float* dst = p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride +
+                       (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
@@ -431,15 +434,25 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
   }
 }
 
-// split-K finish: C (+)= bf16(Cf)
-__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
-                                     __nv_bfloat16* __restrict__ C, int64_t ldc, int accumulate) {
+// split-K finish: C (+)= sum_s Cf[s] in the fixed order s = 0, 1, ... (each
+// split stored its own fp32 slice, so the result does not depend on which
+// split finished first), written as bf16 (C) or fp32 (Cout)
+__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int splits, int M, int N,
+                                     __nv_bfloat16* __restrict__ C, float* __restrict__ Cout,
+                                     int64_t ldc, int accumulate) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)M * N) return;
+  const int64_t mn = (int64_t)M * N;
+  if (i >= mn) return;
   const int64_t r = i / N, c = i % N;
   float v = Cf[i];
-  if (accumulate) v += __bfloat162float(C[r * ldc + c]);
-  C[r * ldc + c] = __float2bfloat16_rn(v);
+  for (int s = 1; s < splits; ++s) v += Cf[s * mn + i];
+  if (Cout) {
+    if (accumulate) v += Cout[r * ldc + c];
+    Cout[r * ldc + c] = v;
+  } else {
+    if (accumulate) v += __bfloat162float(C[r * ldc + c]);
+    C[r * ldc + c] = __float2bfloat16_rn(v);
+  }
 }
 
 // ---------------------------------------------------------------- SIMT
@@ -571,27 +584,28 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   p.ldc = g.ldc;
   p.accumulate = g.accumulate ? 1 : 0;
   float* scratch = nullptr;
-  if (g.c_dtype == LVX_F32) {
-    // fp32 C: stored directly (one split, overwrite) or reduce-added into
-    // (accumulate, or several splits over a zeroed C); no scratch, no finish
-    p.C = nullptr;
-    p.Cf = static_cast<float*>(g.c);
-    p.ldcf = g.ldc;
-    // accumulate by reduce-add even with one split: fire-and-forget in L2,
-    // where a load-add-store made the epilogue wait on every load (measured
-    // 0.38 -> 0.75 ms per dY GEMM of the C4 layer)
-    p.f32_store = (p.splits == 1 && !g.accumulate) ? 1 : 0;
-    if (p.splits > 1 && !g.accumulate &&
-        cudaMemset2DAsync(g.c, g.ldc * 4, 0, g.N * 4, g.M, st) != cudaSuccess)
-      return LVX_ECUDA;
-  } else if (p.splits > 1) {
-    const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
+  p.split_stride = 0;
+  if (p.splits > 1) {
+    // split K: every split stores its own fp32 slice (plain stores, no
+    // zeroing) and the finish kernel sums the slices in a fixed order, so
+    // the result is the same bits on every run
+    const size_t bytes = (size_t)p.splits * (size_t)g.M * (size_t)g.N * 4;
     if (!keep_pool_memory()) return LVX_ECUDA;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
       return LVX_ECUDA;
-    if (cudaMemsetAsync(scratch, 0, bytes, st) != cudaSuccess) return LVX_ECUDA;
     p.Cf = scratch;
     p.ldcf = g.N;
+    p.split_stride = (int64_t)g.M * g.N;
+    p.f32_store = 1;
+  } else if (g.c_dtype == LVX_F32) {
+    // fp32 C, one split: stored directly, or reduce-added when accumulating
+    // (one add per element, so still deterministic): fire-and-forget in L2,
+    // where a load-add-store made the epilogue wait on every load (measured
+    // 0.38 -> 0.75 ms per dY GEMM of the C4 layer)
+    p.C = nullptr;
+    p.Cf = static_cast<float*>(g.c);
+    p.ldcf = g.ldc;
+    p.f32_store = g.accumulate ? 0 : 1;
   }
   if (pairs) {
     auto kern = gemm_bf16_pair_kernel<A_MN, B_MN>;
@@ -607,8 +621,10 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   note_launch();
   if (scratch) {
     const int64_t n = g.M * g.N;
-    splitk_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(scratch, p.M, p.N, p.C,
-                                                                      g.ldc, p.accumulate);
+    const bool f32 = g.c_dtype == LVX_F32;
+    splitk_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        scratch, p.splits, p.M, p.N, f32 ? nullptr : static_cast<__nv_bfloat16*>(g.c),
+        f32 ? static_cast<float*>(g.c) : nullptr, g.ldc, g.accumulate ? 1 : 0);
     note_launch();
     cudaFreeAsync(scratch, st);
   }

@@ -270,8 +270,20 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
         raise ValueError("give d_y_acc or dy_sink, not both")
     scale = default_scale(w.d) if scale is None else scale
     dt = g_i.dtype
+    # n > 1: the weight gradients are partial sums over the rank's rows; they
+    # come out of their GEMMs in the fp32 (f64) state dtype, packed in one
+    # buffer, are summed over the ranks in ONE all-reduce at that precision
+    # and rounded to the weights' dtype once
+    wbuf = None
+    if ctx.n > 1:
+        shapes = (tuple(w.w_q.shape), (w.w_k.shape[0], w.w_k.shape[1] + w.w_v.shape[1]),
+                  tuple(w.w_o.shape))
+        sizes = [a * b for a, b in shapes]
+        flat = torch.empty(sum(sizes), dtype=ctx.ops.state_dtype(dt), device=g_i.device)
+        wbuf = [t.view(sh) for t, sh in zip(torch.split(flat, sizes), shapes)]
     d_o = _heads(_mm(ctx, g_i, w.w_o, tb=True), w.hq)                  # g W_O^T
-    g_wo = _mm(ctx, _flat(saved.state.O.to(dt)), g_i, ta=True)         # flat(O)^T g
+    g_wo = _mm(ctx, _flat(saved.state.O.to(dt)), g_i, ta=True,         # flat(O)^T g
+               out=wbuf[2] if wbuf else None)
     q = _heads(_mm(ctx, saved.x, w.w_q), w.hq)
     if counter is not None:
         counter.add(saved.x.shape[0], w.w_q.shape[0], w.w_q.shape[1])
@@ -310,7 +322,7 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
             else:
                 dkv = torch.cat([dk, dv], dim=1)
         del k, v
-        g_wkv = torch.empty_like(wkv)
+        g_wkv = wbuf[1] if wbuf else torch.empty_like(wkv)
         if dy_sink is not None:   # dY comes from the sink's one GEMM over all layers
             ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
             d_y = None
@@ -318,25 +330,29 @@ def ca_backward(ctx: DeviceContext, shards: ShardSpec, g_i: torch.Tensor, saved:
             ctx.ops.gemm(dkv, False, wkv, True, d_y_acc, accumulate=True)   # += dKV W^T
             ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
             d_y = d_y_acc
+        elif wbuf:
+            d_y = torch.empty_like(y_i)
+            ctx.ops.gemm(dkv, False, wkv, True, d_y)                        # dKV W^T
+            ctx.ops.gemm(y_i, True, dkv, False, g_wkv)                      # y^T dKV
         else:
             d_y = torch.empty_like(y_i)
             ctx.ops.project_backward(y_i, wkv, _heads(dkv, 2 * w.hkv), d_y, g_wkv)
     d_x = torch.empty_like(g_i)
-    g_wq = torch.empty_like(w.w_q)
-    ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
+    if wbuf:
+        g_wq = wbuf[0]
+        ctx.ops.gemm(dq, False, w.w_q, True, d_x)                           # d_x = dq W_Q^T
+        ctx.ops.gemm(saved.x, True, dq, False, g_wq)                        # x^T dq
+    else:
+        g_wq = torch.empty_like(w.w_q)
+        ctx.ops.project_backward(saved.x, w.w_q, _heads(dq, w.hq), d_x, g_wq)   # d_x = dq W_Q^T
     d_x += g_i
-    if ctx.n > 1:   # one all-reduce of the layer's weight gradients, packed
-        parts = (g_wq, g_wkv, g_wo)
-        flat = torch.cat([t.reshape(-1) for t in parts])
+    if wbuf:   # one all-reduce of the layer's weight gradients, packed, at fp32
         if group is not None:
             dist.all_reduce(flat, group=group)
         else:
             ctx.all_reduce_sum_(flat)
-        offs = [0]
-        for t in parts:
-            offs.append(offs[-1] + t.numel())
-        g_wq, g_wkv, g_wo = (flat[a:b].view(t.shape)
-                             for t, a, b in zip(parts, offs[:-1], offs[1:]))
+        wd = w.w_q.dtype
+        g_wq, g_wkv, g_wo = (t.to(wd) for t in wbuf)
     g_wk, g_wv = g_wkv[:, :hkd].contiguous(), g_wkv[:, hkd:].contiguous()
     return CrossAttentionGrads(d_x=d_x, d_y=d_y, w_q=g_wq, w_k=g_wk, w_v=g_wv, w_o=g_wo)
 

@@ -161,3 +161,23 @@ def test_gemm_bf16_into_fp32(shape, accumulate):
     e = _err(c, want)
     print(f"\ngemm bf16->fp32 {shape} acc={accumulate}: {e:.2e}")
     assert e <= 1e-5
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_split_k_gemm_is_deterministic(out_dtype, accumulate):
+    """A tall-K product with few output tiles runs split-K (every split stores
+    its own fp32 slice; the finish sums them in a fixed order), so repeated
+    calls give the same bits — the weight gradients y^T dKV / x^T dQ of the
+    layers are such products."""
+    from paper_2502_02406_b200 import kernels as K
+    a, b = _bf(65536, 512, seed=41), _bf(65536, 256, seed=42)   # a^T b: M 512, N 256, K 65536
+    c0 = _bf(512, 256, seed=43).to(out_dtype)
+    outs = []
+    for _ in range(3):
+        c = c0.clone() if accumulate else torch.empty(512, 256, dtype=out_dtype, device="cuda")
+        K.gemm_into(a, True, b, False, c, accumulate=accumulate)
+        outs.append(c)
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    ref = a.float().T @ b.float() + (c0.float() if accumulate else 0)
+    assert _err(outs[0], ref) <= (4e-3 if out_dtype == torch.bfloat16 else 1e-5)
