@@ -21,6 +21,8 @@
 // Tall-K products with few output tiles (weight gradients x^T dOut over the
 // rank's visual rows) split K so every SM gets work; the partials are
 // reduce-added in fp32 (red.global.add.v4.f32) into stream-ordered scratch
+// (or the caller's fp32 C) in split order — per-warp flags make split s wait
+// for split s-1 of the same rows — so the sum is the same bits on every run,
 // and converted once.
 //
 // Exact SIMT kernel for f32 / f64 (and bf16 views TMA cannot describe): one
@@ -53,10 +55,34 @@ struct GemmParams {
   int64_t ldc;
   float* Cf;          // fp32 output: split-K scratch or the caller's fp32 C, else null
   int64_t ldcf;       // its leading dimension
-  int64_t split_stride;   // split-K: elements between the splits' scratch slices
+  int* flags;         // split-K: per (tile, CTA of the pair, epilogue warp) count of the
+                      // splits already added, so they add in the order 0, 1, ... (null: 1 split)
+  int first_store;    // split-K: split 0 stores (1) or adds (0: accumulating into C)
   int f32_store;      // into Cf: 1 store (one split, overwrite), 0 reduce-add
   int accumulate;     // bf16 C += A B
 };
+
+// Ordered split-K: the epilogue warp that owns 32 rows of a tile waits until
+// the splits before its own have added those rows (acquire), adds, and
+// publishes (fence + release by lane 0 after the warp's writes), so the fp32
+// sum is (((0 + s0) + s1) + ...) on every run.  A split only ever waits for a
+// smaller work unit, which every persistent CTA reaches first.
+__device__ __forceinline__ void splitk_wait(const int* flag, int split, int lane) {
+  if (split > 0 && lane == 0) {
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    } while (v < split);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void splitk_signal(int* flag, int split, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag), "r"(split + 1) : "memory");
+  }
+}
 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -176,6 +202,10 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
+      const int sp = kb0 / p.kb_per_split;
+      int* flag = p.flags ? p.flags + (size_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q : nullptr;
+      if (flag) splitk_wait(flag, sp, lane);
+      const bool store = flag ? (sp == 0 && p.first_store) : p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -184,15 +214,14 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride +
-                       (int64_t)row * p.ldcf + col0;
+          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
             const float4 v4 = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
                                           __uint_as_float(r[4 * g + 2]),
                                           __uint_as_float(r[4 * g + 3]));
-            if (p.f32_store == 1) {
+            if (store) {
               *reinterpret_cast<float4*>(dst + 4 * g) = v4;
             } else
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
@@ -223,6 +252,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
       }
+      if (flag) splitk_signal(flag, sp, lane);
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
     }
@@ -374,6 +404,12 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
       tc_fence_after();
       const int row = m0 + 128 * (int)rank + q * 32 + lane;
       const uint32_t tbase = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
+      const int sp = kb0 / p.kb_per_split;
+      int* flag = p.flags
+                      ? p.flags + ((size_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q
+                      : nullptr;
+      if (flag) splitk_wait(flag, sp, lane);
+      const bool store = flag ? (sp == 0 && p.first_store) : p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < 256 / 32; ++c) {
         uint32_t r[32];
@@ -382,15 +418,14 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride +
-                       (int64_t)row * p.ldcf + col0;
+          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
             const float4 v4 = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
                                           __uint_as_float(r[4 * g + 2]),
                                           __uint_as_float(r[4 * g + 3]));
-            if (p.f32_store == 1) {
+            if (store) {
               *reinterpret_cast<float4*>(dst + 4 * g) = v4;
             } else
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * g),
@@ -421,6 +456,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
           }
         }
       }
+      if (flag) splitk_signal(flag, sp, lane);
       tc_fence_before();
       if (rank == 0) mbar_arrive(&acc_empty[buf]);
       else mbar_arrive_cluster(leader_addr(&acc_empty[buf]));
@@ -434,25 +470,15 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
   }
 }
 
-// split-K finish: C (+)= sum_s Cf[s] in the fixed order s = 0, 1, ... (each
-// split stored its own fp32 slice, so the result does not depend on which
-// split finished first), written as bf16 (C) or fp32 (Cout)
-__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int splits, int M, int N,
-                                     __nv_bfloat16* __restrict__ C, float* __restrict__ Cout,
-                                     int64_t ldc, int accumulate) {
+// split-K finish: bf16 C (+)= the fp32 sum the splits added in order
+__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
+                                     __nv_bfloat16* __restrict__ C, int64_t ldc, int accumulate) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t mn = (int64_t)M * N;
-  if (i >= mn) return;
+  if (i >= (int64_t)M * N) return;
   const int64_t r = i / N, c = i % N;
   float v = Cf[i];
-  for (int s = 1; s < splits; ++s) v += Cf[s * mn + i];
-  if (Cout) {
-    if (accumulate) v += Cout[r * ldc + c];
-    Cout[r * ldc + c] = v;
-  } else {
-    if (accumulate) v += __bfloat162float(C[r * ldc + c]);
-    C[r * ldc + c] = __float2bfloat16_rn(v);
-  }
+  if (accumulate) v += __bfloat162float(C[r * ldc + c]);
+  C[r * ldc + c] = __float2bfloat16_rn(v);
 }
 
 // ---------------------------------------------------------------- SIMT
@@ -584,19 +610,32 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   p.ldc = g.ldc;
   p.accumulate = g.accumulate ? 1 : 0;
   float* scratch = nullptr;
-  p.split_stride = 0;
+  int* flags = nullptr;
   if (p.splits > 1) {
-    // split K: every split stores its own fp32 slice (plain stores, no
-    // zeroing) and the finish kernel sums the slices in a fixed order, so
-    // the result is the same bits on every run
-    const size_t bytes = (size_t)p.splits * (size_t)g.M * (size_t)g.N * 4;
+    // split K: the splits add into one fp32 target (the caller's fp32 C, or
+    // scratch converted by the finish kernel) in split order (ordered flags,
+    // see splitk_wait), so the result is the same bits on every run; split 0
+    // stores unless it must add to the caller's fp32 C
     if (!keep_pool_memory()) return LVX_ECUDA;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
+    const size_t nflags = (size_t)p.m_tiles * p.n_tiles * (pairs ? 2 : 1) * 4;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&flags), nflags * sizeof(int), st) !=
+            cudaSuccess ||
+        cudaMemsetAsync(flags, 0, nflags * sizeof(int), st) != cudaSuccess)
       return LVX_ECUDA;
-    p.Cf = scratch;
-    p.ldcf = g.N;
-    p.split_stride = (int64_t)g.M * g.N;
-    p.f32_store = 1;
+    p.flags = flags;
+    if (g.c_dtype == LVX_F32) {
+      p.Cf = static_cast<float*>(g.c);
+      p.ldcf = g.ldc;
+      p.first_store = g.accumulate ? 0 : 1;
+    } else {
+      const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
+        return LVX_ECUDA;
+      p.Cf = scratch;
+      p.ldcf = g.N;
+      p.first_store = 1;
+    }
+    p.f32_store = 0;
   } else if (g.c_dtype == LVX_F32) {
     // fp32 C, one split: stored directly, or reduce-added when accumulating
     // (one add per element, so still deterministic): fire-and-forget in L2,
@@ -619,12 +658,11 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
     kern<<<std::min(p.units, slots), GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
   }
   note_launch();
-  if (scratch) {
+  if (flags) cudaFreeAsync(flags, st);
+  if (scratch) {   // bf16 C (+)= the ordered fp32 sum
     const int64_t n = g.M * g.N;
-    const bool f32 = g.c_dtype == LVX_F32;
     splitk_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        scratch, p.splits, p.M, p.N, f32 ? nullptr : static_cast<__nv_bfloat16*>(g.c),
-        f32 ? static_cast<float*>(g.c) : nullptr, g.ldc, g.accumulate ? 1 : 0);
+        scratch, p.M, p.N, static_cast<__nv_bfloat16*>(g.c), g.ldc, g.accumulate ? 1 : 0);
     note_launch();
     cudaFreeAsync(scratch, st);
   }
