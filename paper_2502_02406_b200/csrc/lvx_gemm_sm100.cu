@@ -20,10 +20,10 @@
 //   B transposed:     stored [N, K] -> K-major tile (one 256 x 64 box)
 // Tall-K products with few output tiles (weight gradients x^T dOut over the
 // rank's visual rows) split K so every SM gets work; the partials are
-// reduce-added in fp32 (red.global.add.v4.f32) into stream-ordered scratch
-// (or the caller's fp32 C) in split order — per-warp flags make split s wait
-// for split s-1 of the same rows — so the sum is the same bits on every run,
-// and converted once.
+// stored as fp32 slices (one per split, stream-ordered scratch); the last
+// split to finish a tile's rows (an atomic count per epilogue warp) sums the
+// slices in split order and writes C, so the result is the same bits on every
+// run and no CTA ever waits for another.
 //
 // Exact SIMT kernel for f32 / f64 (and bf16 views TMA cannot describe): one
 // output element per thread, accumulated in fp32 (bf16, f32) or f64.
@@ -55,32 +55,75 @@ struct GemmParams {
   int64_t ldc;
   float* Cf;          // fp32 output: split-K scratch or the caller's fp32 C, else null
   int64_t ldcf;       // its leading dimension
-  int* flags;         // split-K: per (tile, CTA of the pair, epilogue warp) count of the
-                      // splits already added, so they add in the order 0, 1, ... (null: 1 split)
-  int first_store;    // split-K: split 0 stores (1) or adds (0: accumulating into C)
+  int* counters;      // split-K: per (tile, CTA of the pair, epilogue warp) count of the
+                      // splits whose slice is written (null: one split)
+  int64_t split_stride;   // split-K: elements between the fp32 slices in Cf
+  float* Cout;        // split-K with an fp32 C: the caller's C (else the bf16 C above)
+  int64_t ldcout;
   int f32_store;      // into Cf: 1 store (one split, overwrite), 0 reduce-add
   int accumulate;     // bf16 C += A B
 };
 
-// Ordered split-K: the epilogue warp that owns 32 rows of a tile waits until
-// the splits before its own have added those rows (acquire), adds, and
-// publishes (fence + release by lane 0 after the warp's writes), so the fp32
-// sum is (((0 + s0) + s1) + ...) on every run.  A split only ever waits for a
-// smaller work unit, which every persistent CTA reaches first.
-__device__ __forceinline__ void splitk_wait(const int* flag, int split, int lane) {
-  if (split > 0 && lane == 0) {
-    int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    } while (v < split);
-  }
+// Split-K: after a split has stored its fp32 slice of a warp's 32 rows, one
+// atomic per warp counts it (release: fence first); the warp that completes
+// the count (acquire: fence after) sums the slices in split order 0, 1, ...
+// for its rows and writes C (bf16 or fp32, + C when accumulating).  Nothing
+// waits, so concurrent GEMMs on other streams cannot deadlock it.
+__device__ __forceinline__ bool splitk_last(int* counter, int splits, int lane) {
   __syncwarp();
-}
-__device__ __forceinline__ void splitk_signal(int* flag, int split, int lane) {
-  __syncwarp();
+  int last = 0;
   if (lane == 0) {
     __threadfence();
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag), "r"(split + 1) : "memory");
+    last = atomicAdd(counter, 1) == splits - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  return last != 0;
+}
+
+__device__ __forceinline__ void splitk_reduce_row(const GemmParams& p, int row, int n0, int ncols) {
+  if (row >= p.M) return;
+  const float* src = p.Cf + (int64_t)row * p.ldcf;
+  for (int c = n0; c < min(n0 + ncols, p.N); c += 8) {
+    float v[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 t = *reinterpret_cast<const float4*>(src + c + 4 * h);
+      v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
+    }
+    for (int sp = 1; sp < p.splits; ++sp) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 t = *reinterpret_cast<const float4*>(src + sp * p.split_stride + c + 4 * h);
+        v[4 * h] += t.x; v[4 * h + 1] += t.y; v[4 * h + 2] += t.z; v[4 * h + 3] += t.w;
+      }
+    }
+    if (p.Cout) {
+      float4* d = reinterpret_cast<float4*>(p.Cout + (int64_t)row * p.ldcout + c);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 t = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+        if (p.accumulate) {
+          const float4 o = d[h];
+          t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
+        }
+        d[h] = t;
+      }
+    } else {
+      uint4* d4 = reinterpret_cast<uint4*>(p.C + (int64_t)row * p.ldc + c);
+      if (p.accumulate) {
+        const uint4 old = *d4;
+        const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+          v[2 * e] += __bfloat162float(o2.x);
+          v[2 * e + 1] += __bfloat162float(o2.y);
+        }
+      }
+      *d4 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                       pack_bf16(v[6], v[7]));
+    }
   }
 }
 
@@ -202,10 +245,9 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
-      const int sp = kb0 / p.kb_per_split;
-      int* flag = p.flags ? p.flags + (size_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q : nullptr;
-      if (flag) splitk_wait(flag, sp, lane);
-      const bool store = flag ? (sp == 0 && p.first_store) : p.f32_store == 1;
+      const bool sk = p.counters != nullptr;
+      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride : p.Cf;
+      const bool store = sk || p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -214,7 +256,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
+          float* dst = cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
@@ -252,9 +294,11 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
       }
-      if (flag) splitk_signal(flag, sp, lane);
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+      if (sk && splitk_last(p.counters + (size_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q,
+                            p.splits, lane))
+        splitk_reduce_row(p, row, n0, BN);
     }
   }
   tc_fence_before();
@@ -404,12 +448,9 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
       tc_fence_after();
       const int row = m0 + 128 * (int)rank + q * 32 + lane;
       const uint32_t tbase = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
-      const int sp = kb0 / p.kb_per_split;
-      int* flag = p.flags
-                      ? p.flags + ((size_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q
-                      : nullptr;
-      if (flag) splitk_wait(flag, sp, lane);
-      const bool store = flag ? (sp == 0 && p.first_store) : p.f32_store == 1;
+      const bool sk = p.counters != nullptr;
+      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride : p.Cf;
+      const bool store = sk || p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < 256 / 32; ++c) {
         uint32_t r[32];
@@ -418,7 +459,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
-          float* dst = p.Cf + (int64_t)row * p.ldcf + col0;
+          float* dst = cf + (int64_t)row * p.ldcf + col0;
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (col0 + 4 * g >= p.N) break;
@@ -456,10 +497,13 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
           }
         }
       }
-      if (flag) splitk_signal(flag, sp, lane);
       tc_fence_before();
       if (rank == 0) mbar_arrive(&acc_empty[buf]);
       else mbar_arrive_cluster(leader_addr(&acc_empty[buf]));
+      if (sk && splitk_last(p.counters +
+                                ((size_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q,
+                            p.splits, lane))
+        splitk_reduce_row(p, row, n0, 256);
     }
   }
   tc_fence_before();
@@ -468,17 +512,6 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
     tc_fence_after();
     tmem_dealloc2(tmem, 512);
   }
-}
-
-// split-K finish: bf16 C (+)= the fp32 sum the splits added in order
-__global__ void splitk_finish_kernel(const float* __restrict__ Cf, int M, int N,
-                                     __nv_bfloat16* __restrict__ C, int64_t ldc, int accumulate) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)M * N) return;
-  const int64_t r = i / N, c = i % N;
-  float v = Cf[i];
-  if (accumulate) v += __bfloat162float(C[r * ldc + c]);
-  C[r * ldc + c] = __float2bfloat16_rn(v);
 }
 
 // ---------------------------------------------------------------- SIMT
@@ -610,37 +643,32 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
   p.ldc = g.ldc;
   p.accumulate = g.accumulate ? 1 : 0;
   float* scratch = nullptr;
-  int* flags = nullptr;
   if (p.splits > 1) {
-    // split K: the splits add into one fp32 target (the caller's fp32 C, or
-    // scratch converted by the finish kernel) in split order (ordered flags,
-    // see splitk_wait), so the result is the same bits on every run; split 0
-    // stores unless it must add to the caller's fp32 C
+    // split K: per-split fp32 slices + per-warp counters in one stream-ordered
+    // allocation; the last split of each tile's rows reduces them in order
+    // and writes C (see splitk_last), so there is no finish kernel
     if (!keep_pool_memory()) return LVX_ECUDA;
-    const size_t nflags = (size_t)p.m_tiles * p.n_tiles * (pairs ? 2 : 1) * 4;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&flags), nflags * sizeof(int), st) !=
-            cudaSuccess ||
-        cudaMemsetAsync(flags, 0, nflags * sizeof(int), st) != cudaSuccess)
+    const size_t slice = (size_t)g.M * (size_t)g.N;
+    const size_t ncnt = (size_t)p.m_tiles * p.n_tiles * (pairs ? 2 : 1) * 4;
+    const size_t cnt_off = ((size_t)p.splits * slice * 4 + 255) / 256 * 256;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), cnt_off + ncnt * sizeof(int), st) !=
+        cudaSuccess)
       return LVX_ECUDA;
-    p.flags = flags;
+    p.counters = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + cnt_off);
+    if (cudaMemsetAsync(p.counters, 0, ncnt * sizeof(int), st) != cudaSuccess)
+      return LVX_ECUDA;
+    p.Cf = scratch;
+    p.ldcf = g.N;
+    p.split_stride = (int64_t)slice;
     if (g.c_dtype == LVX_F32) {
-      p.Cf = static_cast<float*>(g.c);
-      p.ldcf = g.ldc;
-      p.first_store = g.accumulate ? 0 : 1;
-    } else {
-      const size_t bytes = (size_t)g.M * (size_t)g.N * 4;
-      if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess)
-        return LVX_ECUDA;
-      p.Cf = scratch;
-      p.ldcf = g.N;
-      p.first_store = 1;
+      p.Cout = static_cast<float*>(g.c);
+      p.ldcout = g.ldc;
     }
-    p.f32_store = 0;
   } else if (g.c_dtype == LVX_F32) {
     // fp32 C, one split: stored directly, or reduce-added when accumulating
-    // (one add per element, so still deterministic): fire-and-forget in L2,
-    // where a load-add-store made the epilogue wait on every load (measured
-    // 0.38 -> 0.75 ms per dY GEMM of the C4 layer)
+    // (one add per element, so deterministic): fire-and-forget in L2, where a
+    // load-add-store made the epilogue wait on every load (measured 0.38 ->
+    // 0.75 ms per dY GEMM of the C4 layer)
     p.C = nullptr;
     p.Cf = static_cast<float*>(g.c);
     p.ldcf = g.ldc;
@@ -658,14 +686,7 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
     kern<<<std::min(p.units, slots), GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
   }
   note_launch();
-  if (flags) cudaFreeAsync(flags, st);
-  if (scratch) {   // bf16 C (+)= the ordered fp32 sum
-    const int64_t n = g.M * g.N;
-    splitk_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        scratch, p.M, p.N, static_cast<__nv_bfloat16*>(g.c), g.ldc, g.accumulate ? 1 : 0);
-    note_launch();
-    cudaFreeAsync(scratch, st);
-  }
+  if (scratch) cudaFreeAsync(scratch, st);
   return cudaGetLastError() == cudaSuccess ? LVX_OK : LVX_ECUDA;
 }
 
