@@ -81,20 +81,27 @@ __device__ __forceinline__ bool splitk_last(int* counter, int splits, int lane) 
   return last != 0;
 }
 
-__device__ __forceinline__ void splitk_reduce_row(const GemmParams& p, int row, int n0, int ncols) {
-  if (row >= p.M) return;
-  const float* src = p.Cf + (int64_t)row * p.ldcf;
-  for (int c = n0; c < min(n0 + ncols, p.N); c += 8) {
+// The completing warp reduces its 32 rows x 256 columns: row by row, lane l
+// takes columns [8 l, 8 l + 8), so every load / store of the warp is one
+// contiguous 512-byte (fp32) or 512-byte (bf16 pairs) run.
+__device__ __forceinline__ void splitk_reduce_rows(const GemmParams& p, int row0, int n0,
+                                                   int lane) {
+  const int c = n0 + 8 * lane;
+  if (c >= p.N) return;
+  for (int rr = 0; rr < 32; ++rr) {
+    const int row = row0 + rr;
+    if (row >= p.M) break;
+    const float* src = p.Cf + (int64_t)row * p.ldcf + c;
     float v[8];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const float4 t = *reinterpret_cast<const float4*>(src + c + 4 * h);
+      const float4 t = *reinterpret_cast<const float4*>(src + 4 * h);
       v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
     }
     for (int sp = 1; sp < p.splits; ++sp) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const float4 t = *reinterpret_cast<const float4*>(src + sp * p.split_stride + c + 4 * h);
+        const float4 t = *reinterpret_cast<const float4*>(src + sp * p.split_stride + 4 * h);
         v[4 * h] += t.x; v[4 * h + 1] += t.y; v[4 * h + 2] += t.z; v[4 * h + 3] += t.w;
       }
     }
@@ -159,9 +166,12 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
 
   auto decode = [&](int u, int& m0, int& n0, int& kb0, int& kb1) {
+    // split slowest (the splits running side by side share their K range of
+    // A and B in L2; split fastest measured 0.64x at the Flamingo weight
+    // gradient), then N: one A row band meets every B tile
     const int tiles = p.m_tiles * p.n_tiles;
     const int split = u / tiles, t = u % tiles;
-    m0 = (t / p.n_tiles) * BM;       // N fastest: one A row band meets every B tile in L2
+    m0 = (t / p.n_tiles) * BM;
     n0 = (t % p.n_tiles) * BN;
     kb0 = split * p.kb_per_split;
     kb1 = min(p.kb_total, kb0 + p.kb_per_split);
@@ -298,7 +308,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_arrive(&acc_empty[buf]);
       if (sk && splitk_last(p.counters + (size_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q,
                             p.splits, lane))
-        splitk_reduce_row(p, row, n0, BN);
+        splitk_reduce_rows(p, m0 + q * 32, n0, lane);
     }
   }
   tc_fence_before();
@@ -360,7 +370,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
 
   auto decode = [&](int u, int& m0, int& n0, int& kb0, int& kb1) {
     const int tiles = p.m_tiles * p.n_tiles;
-    const int split = u / tiles, t = u % tiles;
+    const int split = u / tiles, t = u % tiles;   // split slowest (see gemm_bf16_kernel)
     m0 = (t / p.n_tiles) * 256;
     n0 = (t % p.n_tiles) * 256;
     kb0 = split * p.kb_per_split;
@@ -503,7 +513,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
       if (sk && splitk_last(p.counters +
                                 ((size_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q,
                             p.splits, lane))
-        splitk_reduce_row(p, row, n0, 256);
+        splitk_reduce_rows(p, m0 + 128 * (int)rank + q * 32, n0, lane);
     }
   }
   tc_fence_before();
