@@ -359,8 +359,14 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
-    def rnd(*shape):
-        return (torch.rand(*shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+    def rnd(h, rows, dd):
+        # uniform[-1, 1) bf16, generated by row chunks: no full-size fp32
+        # temporaries (at Lkv 15M one would be 61 GB)
+        t = torch.empty((h, rows, dd), device=dev, dtype=torch.bfloat16)
+        for a in range(0, rows, 1 << 20):
+            b = min(rows, a + (1 << 20))
+            t[:, a:b] = torch.rand((h, b - a, dd), device=dev, generator=gen) * 2 - 1
+        return t
 
     q_i, k_i, v_i, do_i = rnd(hq, qb - qa, d), rnd(hkv, kb - ka, d), rnd(hkv, kb - ka, d), \
         rnd(hq, qb - qa, d)
