@@ -186,6 +186,31 @@ def test_bf16_rank_counts_vs_oracle(n):
         assert not sdpa_ref.gate(ours, sdpa), (strategy, sdpa_ref.gate(ours, sdpa))
 
 
+@pytest.mark.parametrize("hq,hkv,d,n", [(32, 2, 128, 3), (16, 8, 64, 3), (8, 1, 64, 2)])
+def test_bf16_gqa_ratios_vs_oracle(hq, hkv, d, n):
+    """Other GQA ratios than the configs' (16, 2 and 8 query heads per K/V
+    head; d 64 and 128) over thread ranks, uneven shards, dense oracle,
+    gated at 2x SDPA's error like the config shapes."""
+    import paper_2502_02406_b200 as lvx
+    sq, skv = 260, 3001
+    q, k, v, do = _bf16(hq, hkv, sq, skv, d, seed=hq + hkv + d)
+    Q, K, V, G = (t.double().numpy() for t in (q, k, v, do))
+    O, L = orc.dense_attention(Q, K, V)
+    rq, rk, rv = orc.dense_attention_backward(Q, K, V, O, L, G)
+    want = {"O": O, "L": L, "dQ": rq, "dK": rk, "dV": rv}
+    scale = lvx.default_scale(d)
+    so, sq_, sk, sv = (t.float().cpu() for t in sdpa_ref.sdpa_grads(
+        q.cuda(), k.cuda(), v.cuda(), do.cuda(), scale))
+    sdpa = sdpa_ref.errors({"O": so, "dQ": sq_, "dK": sk, "dV": sv}, want)
+    for strategy in ("lvx", "ring"):
+        res = lvx.run_distributed(strategy, q, k, v, dO=do, spec=lvx.ClusterSpec(n),
+                                  ranks="threads")
+        ours = sdpa_ref.errors({"O": res.O.float(), "L": res.L, "dQ": res.grads.dQ.float(),
+                                "dK": res.grads.dK.float(), "dV": res.grads.dV.float()}, want)
+        print(f"\nGQA {hq}/{hkv} d {d} {strategy} n={n}: ours {ours}\n    sdpa {sdpa}")
+        assert not sdpa_ref.gate(ours, sdpa), (strategy, sdpa_ref.gate(ours, sdpa))
+
+
 # ---------------------------------------------------------------------------
 # failure semantics on the device (cluster.py:35-47, :149-220, :300-335)
 # ---------------------------------------------------------------------------
