@@ -2,8 +2,12 @@
 # gpurun_out/<tag>_*.  Usage (from the repo root, on the GPU box):
 #   bash tools/gpu_session.sh <tag> <leg> [<leg> ...]
 # legs: probe (DSMEM dQ reduce probe), bench (C2 N=1), c3, c4, c5 (Lkv sweeps /
-#       layer stack at N=1), launches (ncu launch list of the C2 bench),
-#       ncu_full (ncu --set full of the dominant kernel), pytest (pytest -m gpu)
+#       layer stack at N=1), bench_n / c3_n / c4_n / c5_n / c5small_n (all
+#       visible GPUs, torchrun), launches / launches_c4 (ncu launch lists),
+#       ncu_full / ncu_fwd_dq (ncu --set full of the hot kernels), kernels /
+#       hbm / gemm / recompute (kernel-level rates), p2p / ce (transport
+#       probes), fullscale_n (n-way vs 1-way at full C2 size), guards,
+#       sanitize, pytest / pytest_multi / pytest_gemm (pytest -m gpu subsets)
 set -u
 tag=$1; shift
 out=gpurun_out
