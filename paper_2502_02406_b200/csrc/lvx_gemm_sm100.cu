@@ -81,55 +81,61 @@ __device__ __forceinline__ bool splitk_last(int* counter, int splits, int lane) 
   return last != 0;
 }
 
-// The completing warp reduces its 32 rows x 256 columns: row by row, lane l
-// takes columns [8 l, 8 l + 8), so every load / store of the warp is one
-// contiguous 512-byte (fp32) or 512-byte (bf16 pairs) run.
-__device__ __forceinline__ void splitk_reduce_rows(const GemmParams& p, int row0, int n0,
-                                                   int lane) {
-  const int c = n0 + 8 * lane;
-  if (c >= p.N) return;
-  for (int rr = 0; rr < 32; ++rr) {
-    const int row = row0 + rr;
-    if (row >= p.M) break;
-    const float* src = p.Cf + (int64_t)row * p.ldcf + c;
-    float v[8];
+// Split-K slices are private scratch, laid out per epilogue warp as
+// [32-column chunk c][float4 g][lane] (8192 floats = the warp's 32 rows x 256
+// columns), so every slice store and every reduction load of a warp is one
+// contiguous 512-byte run.  The completing warp sums its block over the
+// splits in order and writes its rows of C.
+constexpr int kSliceBlock = 32 * 256;
+
+__device__ __forceinline__ void splitk_reduce_block(const GemmParams& p, const float* blk0,
+                                                    int row0, int n0, int lane) {
+  const int row = row0 + lane;
+  const float4* b4 = reinterpret_cast<const float4*>(blk0);
+  const int64_t ss = p.split_stride / 4;   // float4s between splits
+#pragma unroll 1
+  for (int c = 0; c < 8; ++c) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float4 t = *reinterpret_cast<const float4*>(src + 4 * h);
-      v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
-    }
-    for (int sp = 1; sp < p.splits; ++sp) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float4 t = *reinterpret_cast<const float4*>(src + sp * p.split_stride + 4 * h);
-        v[4 * h] += t.x; v[4 * h + 1] += t.y; v[4 * h + 2] += t.z; v[4 * h + 3] += t.w;
-      }
-    }
-    if (p.Cout) {
-      float4* d = reinterpret_cast<float4*>(p.Cout + (int64_t)row * p.ldcout + c);
+    for (int gp = 0; gp < 4; ++gp) {
+      float v[8];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        float4 t = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-        if (p.accumulate) {
-          const float4 o = d[h];
+        const int idx = (c * 8 + 2 * gp + h) * 32 + lane;
+        float4 t = b4[idx];
+        for (int sp = 1; sp < p.splits; ++sp) {
+          const float4 o = b4[sp * ss + idx];
           t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
         }
-        d[h] = t;
+        v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
       }
-    } else {
-      uint4* d4 = reinterpret_cast<uint4*>(p.C + (int64_t)row * p.ldc + c);
-      if (p.accumulate) {
-        const uint4 old = *d4;
-        const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+      const int col = n0 + c * 32 + gp * 8;
+      if (row >= p.M || col >= p.N) continue;
+      if (p.Cout) {
+        float4* d = reinterpret_cast<float4*>(p.Cout + (int64_t)row * p.ldcout + col);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
-          v[2 * e] += __bfloat162float(o2.x);
-          v[2 * e + 1] += __bfloat162float(o2.y);
+        for (int h = 0; h < 2; ++h) {
+          float4 t = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+          if (p.accumulate) {
+            const float4 o = d[h];
+            t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
+          }
+          d[h] = t;
         }
+      } else {
+        uint4* d4 = reinterpret_cast<uint4*>(p.C + (int64_t)row * p.ldc + col);
+        if (p.accumulate) {
+          const uint4 old = *d4;
+          const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+            v[2 * e] += __bfloat162float(o2.x);
+            v[2 * e + 1] += __bfloat162float(o2.y);
+          }
+        }
+        *d4 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                         pack_bf16(v[6], v[7]));
       }
-      *d4 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                       pack_bf16(v[6], v[7]));
     }
   }
 }
@@ -256,13 +262,22 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int row = m0 + q * 32 + lane;
       const uint32_t tbase = tmem + buf * BN + ((uint32_t)(q * 32) << 16);
       const bool sk = p.counters != nullptr;
-      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride : p.Cf;
-      const bool store = sk || p.f32_store == 1;
+      const int64_t wblk = ((int64_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q) * kSliceBlock;
+      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride + wblk : p.Cf;
+      const bool store = p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_wait_ld();
+        if (sk) {   // this split's slice, [c][g][lane] (coalesced)
+          float4* w4 = reinterpret_cast<float4*>(cf) + c * 8 * 32 + lane;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            w4[g * 32] = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                     __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+          continue;
+        }
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
@@ -308,7 +323,7 @@ gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_arrive(&acc_empty[buf]);
       if (sk && splitk_last(p.counters + (size_t)(u % (p.m_tiles * p.n_tiles)) * 4 + q,
                             p.splits, lane))
-        splitk_reduce_rows(p, m0 + q * 32, n0, lane);
+        splitk_reduce_block(p, p.Cf + wblk, m0 + q * 32, n0, lane);
     }
   }
   tc_fence_before();
@@ -459,13 +474,23 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
       const int row = m0 + 128 * (int)rank + q * 32 + lane;
       const uint32_t tbase = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
       const bool sk = p.counters != nullptr;
-      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride : p.Cf;
-      const bool store = sk || p.f32_store == 1;
+      const int64_t wblk =
+          (((int64_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q) * kSliceBlock;
+      float* cf = sk ? p.Cf + (int64_t)(kb0 / p.kb_per_split) * p.split_stride + wblk : p.Cf;
+      const bool store = p.f32_store == 1;
 #pragma unroll 1
       for (int c = 0; c < 256 / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
         tmem_wait_ld();
+        if (sk) {   // this split's slice, [c][g][lane] (coalesced)
+          float4* w4 = reinterpret_cast<float4*>(cf) + c * 8 * 32 + lane;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            w4[g * 32] = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                     __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+          continue;
+        }
         const int col0 = n0 + c * 32;
         if (row >= p.M || col0 >= p.N) continue;
         if (p.Cf) {
@@ -513,7 +538,7 @@ gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA,
       if (sk && splitk_last(p.counters +
                                 ((size_t)(u % (p.m_tiles * p.n_tiles)) * 2 + rank) * 4 + q,
                             p.splits, lane))
-        splitk_reduce_rows(p, m0 + 128 * (int)rank + q * 32, n0, lane);
+        splitk_reduce_block(p, p.Cf + wblk, m0 + 128 * (int)rank + q * 32, n0, lane);
     }
   }
   tc_fence_before();
@@ -658,8 +683,8 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
     // allocation; the last split of each tile's rows reduces them in order
     // and writes C (see splitk_last), so there is no finish kernel
     if (!keep_pool_memory()) return LVX_ECUDA;
-    const size_t slice = (size_t)g.M * (size_t)g.N;
-    const size_t ncnt = (size_t)p.m_tiles * p.n_tiles * (pairs ? 2 : 1) * 4;
+    const size_t ncnt = (size_t)p.m_tiles * p.n_tiles * (pairs ? 2 : 1) * 4;   // warps
+    const size_t slice = ncnt * kSliceBlock;   // floats per split (padded tiles)
     const size_t cnt_off = ((size_t)p.splits * slice * 4 + 255) / 256 * 256;
     if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), cnt_off + ncnt * sizeof(int), st) !=
         cudaSuccess)
@@ -668,7 +693,7 @@ int launch_tc(const GemmCall& g, cudaStream_t st) {
     if (cudaMemsetAsync(p.counters, 0, ncnt * sizeof(int), st) != cudaSuccess)
       return LVX_ECUDA;
     p.Cf = scratch;
-    p.ldcf = g.N;
+    p.ldcf = 0;   // slices are [warp block][c][g][lane], not row-major
     p.split_stride = (int64_t)slice;
     if (g.c_dtype == LVX_F32) {
       p.Cout = static_cast<float*>(g.c);
