@@ -22,7 +22,9 @@ from __future__ import annotations
 import datetime
 import os
 import queue as _queue
+import shutil
 import socket
+import tempfile
 import threading
 import time
 import traceback
@@ -140,12 +142,13 @@ def _drain(device) -> None:
 # one process per GPU
 # ---------------------------------------------------------------------------
 
-def _worker(rank, n, port, args, q):
+def _worker(rank, n, store_path, args, q):
     try:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         torch.cuda.set_device(rank)
         strategy, Q, K, V, dO, scale, tile_rows, timeout = args
-        dist.init_process_group("nccl", rank=rank, world_size=n,
+        # file rendezvous: no TCP port to collide with another run's
+        dist.init_process_group("nccl", init_method=f"file://{store_path}", rank=rank,
+                                world_size=n,
                                 device_id=torch.device("cuda", rank),
                                 timeout=datetime.timedelta(seconds=max(timeout, 1.0)))
         from .strategies import run_distributed
@@ -181,10 +184,18 @@ def spawn_run(strategy, Q, K, V, dO, n, scale, tile_rows, timeout: float | None 
     tmo = resolve_timeout(timeout)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, n, port, (strategy, Q, K, V, dO, scale,
-                                                            tile_rows, tmo), q))
+    rdzv_dir = tempfile.mkdtemp(prefix="lvx_rdzv_")
+    store = os.path.join(rdzv_dir, "store")
+    procs = [ctx.Process(target=_worker, args=(r, n, store, (strategy, Q, K, V, dO, scale,
+                                                             tile_rows, tmo), q))
              for r in range(n)]
+    try:
+        return _collect(procs, q, n, tmo)
+    finally:
+        shutil.rmtree(rdzv_dir, ignore_errors=True)
+
+
+def _collect(procs, q, n, tmo):
     for p in procs:
         p.start()
     # process start-up + CUDA init + the run itself: the per-wait timeout

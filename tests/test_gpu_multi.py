@@ -413,13 +413,16 @@ def test_eight_process_ranks_copy_engine():
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "8",
-           "--master-addr", "127.0.0.1", "--master-port", str(port),
-           str(root / "tools" / "procs_check.py")]
-    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    for _ in range(3):   # a free port can be taken between the probe and torchrun's bind
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+               "8", "--master-addr", "127.0.0.1", "--master-port", str(port),
+               str(root / "tools" / "procs_check.py")]
+        p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+        if "EADDRINUSE" not in p.stderr and "address already in use" not in p.stderr:
+            break
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
     assert p.returncode == 0 and lines, p.stderr[-3000:]
     res = json.loads(lines[-1])

@@ -2,7 +2,7 @@
 multi-process gloo group on CPU, with the oracle as the kernel set.  Checks
 outputs and per-rank byte counters against the reference's golden vectors."""
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -14,15 +14,14 @@ from oracle import lvx_oracle as orc
 
 
 def _port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
+    """A fresh file-rendezvous path for one process group (no TCP port that
+    another run could take between the probe and the bind)."""
+    return os.path.join(tempfile.mkdtemp(prefix="lvx_gloo_"), "store")
 
 
 def _worker(rank, n, port, cases, q):
     try:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("gloo", rank=rank, world_size=n)
+        dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=n)
         from paper_2502_02406_b200.strategies import run_distributed
         from paper_2502_02406_b200.comm import ClusterSpec
         from tests.oracle_ops import OracleOps
@@ -94,8 +93,7 @@ def test_gloo_gqa_lvx_and_ring_agree_with_oracle():
 
 def _ca_worker(rank, n, port, golden, policy, q):
     try:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("gloo", rank=rank, world_size=n)
+        dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=n)
         from paper_2502_02406_b200.comm import DeviceContext
         from paper_2502_02406_b200.recompute import (CrossAttentionWeights, OpCounter, ca_backward,
                                                      ca_forward)
@@ -155,8 +153,7 @@ def _stream_worker(rank, n, port, q):
     """lvx fwd+bwd with K/V streamed in 3 chunks (KVStream) vs the resident
     call on the same rank: identical up to the chunked merge (f64)."""
     try:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("gloo", rank=rank, world_size=n)
+        dist.init_process_group("gloo", init_method=f"file://{port}", rank=rank, world_size=n)
         from paper_2502_02406_b200.comm import DeviceContext
         from paper_2502_02406_b200.strategies import (KVStream, ShardSpec, lvx_backward,
                                                       lvx_forward)
