@@ -481,6 +481,19 @@ def measure_point(args, env, ctx, ctx_nc, s_kv, head=True):
                 "frac_of_nominal_2250": achieved / 2250.0,
                 "per_launch_ms": kdur * 1e3,
                 "phase_ms_per_step": {k: v * 1e3 for k, v in phases.items()},
+                # every hot kernel: algorithmic FLOP (the paper's 4 / 10 units)
+                # and the tensor work it actually issues (dK/dV and dQ both
+                # recompute S and dP: 8 + 6 issued units for 10 algorithmic)
+                "kernels": {name: {
+                    "ms_per_step": phases[ph] * 1e3,
+                    "algorithmic_tflops": alg * unit * n_rounds / max(phases[ph], 1e-9) / 1e12,
+                    "issued_tflops": iss * unit * n_rounds / max(phases[ph], 1e-9) / 1e12,
+                    "issued_frac_of_peak": iss * unit * n_rounds / max(phases[ph], 1e-9) / 1e12
+                    / peak}
+                    for name, ph, alg, iss in (("fwd_kernel", "fwd_kernel", 4.0, 4.0),
+                                               ("dq_kernel", "dq_kernel", 2.0, 6.0),
+                                               ("dkv_kernel", "dkv_kernel", 8.0, 8.0))
+                    if phases.get(ph, 0) > 0 and args.strategy == "lvx"},
                 "fwd_tflops": 4.0 * unit * n_rounds / max(phases["fwd_kernel"], 1e-9) / 1e12,
                 "bwd_tflops": 10.0 * unit * n_rounds /
                 max(phases["dkv_kernel"] + phases["dq_kernel"] + phases["dq_finish"], 1e-9) / 1e12}
